@@ -1,0 +1,332 @@
+"""Benchmark of the CULSH-MF hot path on B200 (contract: see DESIGN.md §Measurement).
+
+Workload (BASELINE.json configs[2], the metric's config): Netflix-shape synthetic
+matrix 480,189 x 17,770 with ~100.48M integer ratings, F=128, K=32, simLSH
+G=8 p=3 q=100 psi exponent 2.  One step = one Hogwild SGD epoch over all
+ratings (one kernel launch).  The simLSH top-K build (hash + keys + buckets +
+top-K) is timed separately and reported as lsh_build_s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c1]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+Multi-GPU (torchrun, one process per GPU): DSGD over N GPUs (dsgd.py), the
+whole matrix fixed (strong scaling), max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rating updates/sec/epoch + simLSH top-K build time, Netflix-shape; RMSE parity"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def peak_hbm_gbs():
+    try:
+        with open(PEAKS) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self, gpu_index=0):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or f[0] != str(gpu_index):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- CPU oracle ---
+
+def cpu_baseline(dm, nbr_host, F, K, cfg_lsh, budget_s=20.0, threads=None):
+    """The reference algorithm (oracle/ C port, pinned bit-exact to the reference)
+    timed on this host's cores on a bounded sample of the same workload."""
+    from oracle import oracle as orc
+    from paper_2111_11682_b200 import _native as nat
+    threads = threads or (os.cpu_count() or 1)
+    d = dm.dev
+    # SGD sample: rows [0, Ms) with their complete rating lists (so the K neighbour
+    # lookups search full-length rows), every column, the GPU-built J^K.
+    row_ptr = nat.to_host(d.row_ptr)
+    Ms = max(1, min(dm.M, int(dm.M * 0.02)))
+    rows, cols, vals = (np.repeat(np.arange(Ms, dtype=np.int32), np.diff(row_ptr[:Ms + 1])),
+                        nat.to_host(d.row_cols[:int(row_ptr[Ms])]), nat.to_host(d.row_vals[:int(row_ptr[Ms])]))
+    csr, mu = orc.build_csr(Ms, dm.N, rows, cols, vals)
+    m = orc.init_model(Ms, dm.N, F, K, nbr_host, mu, csr.base_b, csr.base_bhat, 0)
+    rates = orc.make_rates((0.02, 0.02, 0.02, 0.02, 0.001, 0.001), (0.01, 0.01, 0.01, 0.01, 0.05, 0.05))
+    D = max(1, min(threads, Ms, dm.N))
+    part = orc.partition(csr, D)
+    t0 = time.perf_counter()
+    n_ep = 0
+    while True:
+        orc.parallel_epoch(csr, m, rates, D, part, threads)
+        n_ep += 1
+        if time.perf_counter() - t0 > budget_s * 0.5 or n_ep >= 3:
+            break
+    sgd_s = time.perf_counter() - t0
+    ups = len(rows) * n_ep / sgd_s
+    # simLSH sample: the first Nc columns with all their ratings, all p*q*G maps
+    G, p, q, e = cfg_lsh
+    col_ptr = nat.to_host(d.col_ptr)
+    Nc = max(1, min(dm.N, 200))
+    hi = int(col_ptr[Nc])
+    bits = orc.assign_bits(0, q, p, dm.M, G)
+    t1 = time.perf_counter()
+    orc.accumulate_all(col_ptr[:Nc + 1], nat.to_host(d.col_rows[:hi]), nat.to_host(d.col_vals[:hi]),
+                       bits, e, threads)
+    lsh_s = (time.perf_counter() - t1) * dm.N / Nc
+    return {"value": ups, "unit": "updates/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle parallel_epoch (DSGD D={D}, reference parallel_train) over rows "
+                       f"[0,{Ms}) x all {dm.N} columns = {len(rows)} ratings, {n_ep} epoch(s) in "
+                       f"{sgd_s:.1f}s; simLSH accumulate on {Nc} of {dm.N} columns, extrapolated"),
+            "lsh_build_s_extrapolated": lsh_s}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path (oracle port)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    from paper_2111_11682_b200 import synth, lsh
+    from paper_2111_11682_b200 import _native as nat
+    M, N, nnz, F, K, e = synth.SHAPES[args.config]
+    dm = synth.random_sparse_device(M, N, nnz, seed=0)
+    ent, _, _ = lsh.simlsh_topk_device(dm.dev, lsh.LshConfig(psi_exponent=e), K)
+    nbr = nat.to_host(ent)[:N * K].reshape(N, K)
+    vals = []
+    cb = None
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline(dm, nbr, F, K, (8, 3, 100, e), budget_s=8.0)
+        if s >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.median(vals))
+    line = {"metric": METRIC, "value": v, "unit": "updates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD[args.config]},
+            "cpu_baseline": {**cb, "value": v},
+            "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+WORKLOAD = {
+    "c1": "C1 MovieLens-100K-shape 943x1682 (100k), F=32, K=16",
+    "c2": "C2 MovieLens-20M-shape 138493x26744 (20M), F=64, K=32",
+    "c3": "C3 Netflix-shape 480189x17770 (100.48M), F=128, K=32, simLSH G=8 p=3 q=100 e=2",
+    "c5": "C5 Yahoo-shape 1000990x624961 (262.8M), F=128, K=64",
+}
+
+NETFLIX_RATES = dict(alpha_b=0.02, alpha_b_hat=0.02, alpha_u=0.02, alpha_v=0.02, alpha_w=0.001,
+                     alpha_c=0.001, lambda_b=0.01, lambda_b_hat=0.01, lambda_u=0.01, lambda_v=0.01,
+                     lambda_w=0.05, lambda_c=0.05, beta=0.3)
+
+
+def run_gpu(args):
+    import torch
+    from paper_2111_11682_b200 import synth, lsh
+    from paper_2111_11682_b200 import _native as nat
+    from paper_2111_11682_b200.factorization import TrainConfig, init_params
+    from paper_2111_11682_b200.data import BaselineStats
+    from paper_2111_11682_b200.hogwild import HogwildTrainer
+    from paper_2111_11682_b200.similarity import NeighborTable
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2111_11682_b200 import dsgd
+        return dsgd.bench_main(args, METRIC, WORKLOAD, NETFLIX_RATES)
+
+    torch.cuda.set_device(0)
+    M, N, nnz_t, F, K, e = synth.SHAPES[args.config]
+    t_gen = time.perf_counter()
+    dm = synth.random_sparse_device(M, N, nnz_t, seed=0)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    nnz = dm.nnz
+    lcfg = lsh.LshConfig(G=8, p=3, q=100, psi_exponent=e, seed=0)
+
+    # ---- simLSH top-K build (device-resident ratings), warm once then time
+    lsh.simlsh_topk_device(dm.dev, lcfg, K)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    ent, state, ncand = lsh.simlsh_topk_device(dm.dev, lcfg, K)
+    ev[1].record()
+    torch.cuda.synchronize()
+    lsh_s = ev[0].elapsed_time(ev[1]) / 1e3
+    nbr_host = nat.to_host(ent)[:N * K].reshape(N, K).astype(np.int32)
+    del state
+    nbr = NeighborTable(N, K, nbr_host)
+
+    # ---- Hogwild trainer (init identical to the reference's init_params)
+    cfg = TrainConfig(F=F, K=K, epochs=args.warmup + args.steps, seed=0, **NETFLIX_RATES)
+    stats = BaselineStats(dm.dev.mu, nat.to_host(dm.dev.base_b), nat.to_host(dm.dev.base_bhat))
+    params = init_params(M, N, F, K, nbr, stats, cfg)
+    torch.cuda.synchronize()
+    t_prep = time.perf_counter()
+    tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params)
+    torch.cuda.synchronize()
+    t_prep = time.perf_counter() - t_prep
+    del params
+    b_upd = tr.bytes_per_update()
+
+    for w in range(args.warmup):
+        tr.launch_epoch(w)
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    clk = Clocks(os.path.join(ROOT, "gpurun_out", "bench_clocks.csv") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else "/tmp/bench_clocks.csv")
+    with clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        evs[0].record()
+        for s in range(args.steps):
+            tr.launch_epoch(args.warmup + s)
+            evs[s + 1].record()
+        torch.cuda.synchronize()
+    per = [evs[s].elapsed_time(evs[s + 1]) / 1e3 for s in range(args.steps)]
+    total = sum(per)
+    if int(tr.status.item()):
+        raise RuntimeError("Hogwild epoch diverged in the bench")
+    ups = nnz * args.steps / total
+    ms = total / args.steps * 1e3
+    peak, peak_kind = peak_hbm_gbs()
+    achieved = b_upd * nnz / (total / args.steps) / 1e9
+    train_rmse = (float(tr.loss.item()) / (nnz * (args.warmup + args.steps))) ** 0.5
+
+    # ---- e2e through the public API with host (pinned) buffers every step
+    e2e = e2e_streaming(tr, args)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(dm, nbr_host, F, K, (8, 3, 100, e), budget_s=args.cpu_budget)
+        except Exception as ex:  # the CPU leg must not sink the GPU line
+            cpu = {"value": None, "error": repr(ex)}
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": ups, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (random_sparse distribution generated in HBM, integer stars 1-5)",
+        "config": {"workload": WORKLOAD[args.config], "M": M, "N": N, "nnz": nnz, "F": F, "K": K,
+                   "mode": "hogwild fp32, warp per column",
+                   "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
+        "lsh_build_s": lsh_s, "lsh_candidates": ncand,
+        "prep_s": t_prep, "datagen_s": t_gen, "train_rmse_running": train_rmse,
+        "epoch_ms": [p * 1e3 for p in per],
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "bytes_per_update": b_upd, "kernel": "hogwild_kernel<4,1>"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def e2e_streaming(tr, args):
+    """Same metric through HogwildTrainer.epoch_from_host: each step copies the
+    epoch's rating stream (rows, values, masks) from pinned host memory, runs the
+    epoch and reads the epoch loss back."""
+    import torch
+    host = tr.pinned_stream()
+    for w in range(1):
+        tr.epoch_from_host(host, w)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    steps = max(1, min(args.steps, 5))
+    h2d = d2h = 0
+    for s in range(steps):
+        loss, hb, db = tr.epoch_from_host(host, args.warmup + s)
+        h2d += hb
+        d2h += db
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"value": tr.nnz * steps / dt, "unit": "updates/s", "h2d_bytes_per_step": h2d // steps,
+            "d2h_bytes_per_step": d2h // steps, "steps": steps,
+            "api": "HogwildTrainer.epoch_from_host (pinned host stream -> epoch -> loss)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="culsh", choices=["culsh", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,205 @@
+/*
+ * culsh.h -- C ABI of the B200-native CULSH-MF hot path (libculsh.so).
+ *
+ * Drop-in boundary: each entry point replaces one kernel seam of the reference
+ * package lshmf (/root/reference/pkg/src/lshmf), cited per function as
+ * file:line.  The reference's Python layer (lsh.py, factorization.py,
+ * online.py, parallel.py) calls those numba kernels with plain numpy arrays;
+ * the Python host layer paper_2111_11682_b200/ calls these functions with
+ * plain device pointers obtained from torch tensors, through ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless the name ends in _host;
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it;
+ *   - return value: CULSH_OK (0), CULSH_DIVERGED (1, non-finite error seen,
+ *     the reference's "return 1"), CULSH_EINVAL (-1, bad arguments; nothing
+ *     launched), CULSH_ECUDA (-2, CUDA error); culsh_last_error() describes it;
+ *   - the library never frees caller memory and never throws across the ABI;
+ *   - no torch types appear here.
+ */
+#ifndef CULSH_H_
+#define CULSH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CULSH_OK 0
+#define CULSH_DIVERGED 1
+#define CULSH_EINVAL (-1)
+#define CULSH_ECUDA (-2)
+
+/* ---------------------------------------------------------------- misc --- */
+
+/* Last error message (thread-local), "" if none. */
+const char *culsh_last_error(void);
+/* Library version string, e.g. "culsh 0.1.0 sm_100a". */
+const char *culsh_version(void);
+
+/* ------------------------------------------------------------- simLSH --- */
+
+/* Row-hash table: for rows [row_lo,row_hi) writes table[i][g][m][s], the byte s
+ * (s < ceil(G/8)) of the low G bits of splitmix64(map_key(seed,g,m) ^ i).
+ * Replaces lsh.py:68-78 _assign_bits / lsh.py:108-114 assign_row_hashes (the
+ * reference's (M,q,p,G) u8 tensor, packed 8 bits per byte). */
+int culsh_row_hash_table(uint64_t seed, int q, int p, int G, int64_t row_lo, int64_t row_hi,
+                         uint8_t *table, void *stream);
+
+/* Pack/unpack between the reference's (M,q,p,G) u8 bit tensor (RowHashes.bits,
+ * lsh.py:81-105) and the packed table. */
+int culsh_pack_bits(const uint8_t *bits, int64_t M, int q, int p, int G, uint8_t *table,
+                    void *stream);
+int culsh_unpack_bits(const uint8_t *table, int64_t M, int q, int p, int G, uint8_t *bits,
+                      void *stream);
+
+/* Sets *bad_out (device int) to 1 unless every psi(v) of the listed columns is an
+ * integer and every column's sum of |psi| is < 2^31 (enables the exact-integer
+ * accumulation path, bit-identical to the reference's fp64 sums). */
+int culsh_psi_int_check(const int64_t *col_ptr, const double *col_vals, int64_t col_begin,
+                        int64_t n_cols, const int32_t *col_list, int e, int *bad_out, void *stream);
+
+/* Signed accumulation + threshold + group-key pack for columns
+ * col_list[0..n_cols) (or col_begin + [0..n_cols) when col_list is NULL).
+ *   acc  (N, q, p, G) f64   fresh (into=0) or added to in place (into=1)
+ *   sig  (N, q, p, G) u8    optional (NULL to skip)
+ *   keys (q, keys_ld) u64   optional, bit m*G+t of keys[g, j] = sig[j,g,m,t]
+ * Replaces lsh.py:161-179 _accumulate_all, online.py:96-117 _accumulate_into,
+ * lsh.py:182-183 _threshold and lsh.py:246-260 _pack_group_keys. */
+int culsh_hash_accumulate(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                          int64_t col_begin, int64_t n_cols, const int32_t *col_list,
+                          const uint8_t *table, int q, int p, int G, int e, int into, int int_path,
+                          double *acc, uint8_t *sig, uint64_t *keys, int64_t keys_ld, void *stream);
+
+/* Buckets + frequency top-K with seeded supplement for target columns
+ * [j_base, j_base+n_cols) of an N_total-column key matrix keys (q, N_total).
+ * entries (n_cols, K) i32.  *n_candidates_out (host) = total bucket-mate count.
+ * Replaces lsh.py:401-414 _topk_from_group_keys (B2-B4: lsh.py:263-287,308-374)
+ * and the new-column path of online.py:152-184 topk_for_new. */
+int culsh_topk(const uint64_t *keys, int q, int64_t N_total, int key_bits, int64_t j_base,
+               int64_t n_cols, int K, uint64_t seed, int32_t *entries,
+               int64_t *n_candidates_out_host, void *stream);
+
+/* ---------------------------------------------------------------- SGD --- */
+
+/* Learning rates and regularisers of one epoch (factorization.py:84-95). */
+typedef struct {
+    double gb, gbh, gu, gv, gw, gc;
+    double lb, lbh, lu, lv, lw, lc;
+} CulshRates;
+
+/* Device view of SparseRatings (data.py:166-207) + residual baselines
+ * (data.py:289-309).  csc2csr[idx] = CSR position of CSC entry idx. */
+typedef struct {
+    int64_t M, N, nnz;
+    const int64_t *col_ptr;
+    const int32_t *col_rows;
+    const double *col_vals;
+    const int64_t *row_ptr;
+    const int32_t *row_cols;
+    const double *row_vals;
+    const int32_t *csc2csr;
+    const double *base_b;
+    const double *base_bhat;
+} CulshData;
+
+/* fp64 model (factorization.py:105-137 ModelParams), row-major arrays. */
+typedef struct {
+    double mu;
+    double *b, *bhat, *U, *V, *W, *C;
+    const int32_t *nbr;
+    int F, K;
+} CulshModel64;
+
+/* CSC-entry ranges of one pass: seg[2j], seg[2j+1]; chain_lo[j] = first column
+ * of the block j belongs to.  mode 0: rows [row_lo,row_hi) of columns
+ * [col_lo,col_hi) (factorization.py:346-355); mode 1: DSGD stage s of D using
+ * block_ptr (N, D+1) and col_bounds (D+1) (parallel.py:36-41,110-128). */
+int culsh_pass_plan(const int64_t *col_ptr, const int32_t *col_rows, int64_t N, int mode,
+                    int64_t col_lo, int64_t col_hi, int64_t row_lo, int64_t row_hi,
+                    const int64_t *block_ptr, const int64_t *col_bounds, int D, int s,
+                    int64_t *seg, int32_t *chain_lo, void *stream);
+
+/* parallel.py:55-64 _block_pointers: out (N, nb). */
+int culsh_block_pointers(const int64_t *col_ptr, const int32_t *col_rows, int64_t N,
+                         const int64_t *row_bounds, int nb, int64_t *out, void *stream);
+
+/* Deterministic serial-order column pass (bit-exact fp64).  row_mode: 0 never
+ * update rows, 1 always, 2 only rows >= M_old.  row_last (M ints), ticket (1 int)
+ * are scratch; *status (device int) is OR-ed with 1 on a non-finite error.
+ * Replaces factorization.py:332-363 _full_pass_block, parallel.py:110-128
+ * _stage_pass (all D blocks of a stage in one launch) and online.py:253-271
+ * _online_col_pass. */
+int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
+                            const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
+                            int64_t col_hi, int row_mode, int64_t M_old, int *row_last,
+                            int *ticket, int *status, void *stream);
+
+/* online.py:230-250 _online_row_pass (rows [row_lo,row_hi), columns < N_old). */
+int culsh_sgd_exact_rowpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
+                            int64_t row_lo, int64_t row_hi, int64_t N_old, int *status,
+                            void *stream);
+
+/* fp32 model for the Hogwild performance mode. */
+typedef struct {
+    float mu;
+    float *b, *bhat, *U, *V, *W, *C;
+    int F, K;
+} CulshModel32;
+
+/* Per-rating explicit-neighbour stream for the Hogwild kernel, built once per
+ * fit from (data, J^K) only (factorization.py:287-298 split into the data part):
+ *   mask[idx] bit k set iff row i rated neighbour J[j,k]   (u32 words, K<=32 -> 1 word)
+ *   resid[resid_ptr[j] + ...] = r(i,J[j,k]) - (mu + b_i + b_hat_J[j,k]) for set bits,
+ *   in (entry, k) order.  Pass 1 (resid == NULL) fills mask and per-column counts
+ *   col_nexpl (N); the caller prefix-sums counts into resid_ptr (N+1); pass 2 fills resid. */
+int culsh_explicit_stream(const CulshData *d, double mu, const int32_t *nbr, int K,
+                          uint32_t *mask, int64_t *col_nexpl, const int64_t *resid_ptr,
+                          float *resid, void *stream);
+
+/* One Hogwild epoch (warp per column, column parameters in registers, row
+ * parameters lock-free; paper Alg. 3, factorization.py:266-329 rules in fp32).
+ * Processes N_list columns col_order[0..N_list) (NULL = 0..N_list-1); column j
+ * streams CSC entries [seg[2j], seg[2j+1]) (seg NULL = the whole column, a DSGD
+ * block otherwise, see culsh_pass_plan).  rows/vals: CSC row index and fp32
+ * value.  loss_out (device double, optional) accumulates sum e^2; *status |= 1
+ * on a non-finite error.  Replaces factorization.py:332-363 _full_pass_block /
+ * parallel.py:110-128 _stage_pass in the performance mode. */
+int culsh_sgd_hogwild_epoch(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
+                            const int32_t *rows, const float *vals, const uint32_t *mask,
+                            const int64_t *resid_ptr, const float *resid, const int32_t *col_order,
+                            CulshModel32 *m, const CulshRates *r, int *ticket, double *loss_out,
+                            int *status, void *stream);
+
+/* --------------------------------------------------------------- eval --- */
+
+/* Per-test-triplet squared error (fp64, exact _predict_one order) and the RMSE.
+ * Replaces factorization.py:394-409 _rmse_kernel (sum by a fixed pairwise tree).
+ * rmse_out: device double. */
+int culsh_rmse(const CulshData *d, const CulshModel64 *m, const int32_t *t_rows,
+               const int32_t *t_cols, const double *t_vals, int64_t n, int do_clamp,
+               double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
+               double *rmse_out, void *stream);
+
+/* RMSE of the fp32 Hogwild model (predictions in fp32, sum in fp64). */
+int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int32_t *nbr,
+                 const int32_t *t_rows, const int32_t *t_cols, const double *t_vals, int64_t n,
+                 double *sqerr_scratch, double *rmse_out, void *stream);
+
+/* factorization.py:235-263 _predict_one for n (i, j) pairs -> out (n) f64. */
+int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows,
+                  const int32_t *cols, int64_t n, double *out, void *stream);
+
+/* ----------------------------------------------------------- ratings --- */
+
+/* csc2csr[idx] for every CSC entry (binary search of column j in row i). */
+int culsh_csc_to_csr_map(const CulshData *d, int32_t *csc2csr, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CULSH_H_ */

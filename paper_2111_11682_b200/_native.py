@@ -1,0 +1,208 @@
+"""ctypes binding of libculsh.so (include/culsh.h) and the device plumbing.
+
+The product path has no CPU fallback: every compute function here needs the
+CUDA library AND a CUDA device, and raises ``NativeUnavailable`` otherwise.
+PyTorch is used only for device memory, streams and torch.distributed.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libculsh.so")
+CSRC = os.path.join(_PKG, "csrc")
+
+CULSH_OK = 0
+CULSH_DIVERGED = 1
+CULSH_EINVAL = -1
+CULSH_ECUDA = -2
+
+
+class NativeUnavailable(RuntimeError):
+    """libculsh.so is missing or no CUDA device is visible."""
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int
+_u64 = ctypes.c_uint64
+_f64 = ctypes.c_double
+
+
+class CulshRates(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in
+                ("gb", "gbh", "gu", "gv", "gw", "gc", "lb", "lbh", "lu", "lv", "lw", "lc")]
+
+
+class CulshData(ctypes.Structure):
+    _fields_ = [("M", _i64), ("N", _i64), ("nnz", _i64),
+                ("col_ptr", _vp), ("col_rows", _vp), ("col_vals", _vp),
+                ("row_ptr", _vp), ("row_cols", _vp), ("row_vals", _vp),
+                ("csc2csr", _vp), ("base_b", _vp), ("base_bhat", _vp)]
+
+
+class CulshModel64(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_double), ("b", _vp), ("bhat", _vp), ("U", _vp), ("V", _vp),
+                ("W", _vp), ("C", _vp), ("nbr", _vp), ("F", _i32), ("K", _i32)]
+
+
+class CulshModel32(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_float), ("b", _vp), ("bhat", _vp), ("U", _vp), ("V", _vp),
+                ("W", _vp), ("C", _vp), ("F", _i32), ("K", _i32)]
+
+
+_P = ctypes.POINTER
+# name -> argtypes (restype int unless listed in _RESTYPES)
+_SIGS = {
+    "culsh_last_error": [],
+    "culsh_version": [],
+    "culsh_row_hash_table": [_u64, _i32, _i32, _i32, _i64, _i64, _vp, _vp],
+    "culsh_pack_bits": [_vp, _i64, _i32, _i32, _i32, _vp, _vp],
+    "culsh_unpack_bits": [_vp, _i64, _i32, _i32, _i32, _vp, _vp],
+    "culsh_psi_int_check": [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _vp],
+    "culsh_hash_accumulate": [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                              _i32, _vp, _vp, _vp, _i64, _vp],
+    "culsh_topk": [_vp, _i32, _i64, _i32, _i64, _i64, _i32, _u64, _vp, _P(_i64), _vp],
+    "culsh_pass_plan": [_vp, _vp, _i64, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32, _i32, _vp,
+                        _vp, _vp],
+    "culsh_block_pointers": [_vp, _vp, _i64, _vp, _i32, _vp, _vp],
+    "culsh_sgd_exact_colpass": [_P(CulshData), _P(CulshModel64), _P(CulshRates), _vp, _vp, _i64,
+                                _i64, _i32, _i64, _vp, _vp, _vp, _vp],
+    "culsh_sgd_exact_rowpass": [_P(CulshData), _P(CulshModel64), _P(CulshRates), _i64, _i64, _i64,
+                                _vp, _vp],
+    "culsh_explicit_stream": [_P(CulshData), _f64, _vp, _i32, _vp, _vp, _vp, _vp, _vp],
+    "culsh_sgd_hogwild_epoch": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
+                                _P(CulshRates), _vp, _vp, _vp, _vp],
+    "culsh_rmse": [_P(CulshData), _P(CulshModel64), _vp, _vp, _vp, _i64, _i32, _f64, _f64, _f64,
+                   _vp, _vp, _vp],
+    "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "culsh_predict": [_P(CulshData), _P(CulshModel64), _vp, _vp, _i64, _vp, _vp],
+    "culsh_csc_to_csr_map": [_P(CulshData), _vp, _vp],
+}
+_RESTYPES = {"culsh_last_error": ctypes.c_char_p, "culsh_version": ctypes.c_char_p}
+
+_lib = None
+
+
+def build(verbose: bool = False) -> str:
+    """Compile libculsh.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    out = subprocess.run(["make", "-C", CSRC, "-j8"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise NativeError("libculsh build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+    if verbose:
+        print(out.stdout[-2000:])
+    return LIB_PATH
+
+
+def load_library():
+    """Load libculsh.so and declare every entry point (no GPU needed)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(
+                f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (the product path has no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def device():
+    """The CUDA device the native path runs on; raises if there is none."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible: the CULSH-MF path runs only on the GPU "
+                                "(there is no CPU fallback)")
+    load_library()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def call(name: str, *args) -> int:
+    """Call an entry point; raise on CULSH_EINVAL / CULSH_ECUDA, return the status."""
+    lib = load_library()
+    st = getattr(lib, name)(*args)
+    if st < 0:
+        msg = lib.culsh_last_error().decode()
+        if st == CULSH_EINVAL:
+            raise ValueError(f"{name}: {msg}")
+        raise NativeError(f"{name} failed ({st}): {msg}")
+    return st
+
+
+def ptr(t) -> ctypes.c_void_p:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+_NP2T = {np.dtype(np.int32): "int32", np.dtype(np.int64): "int64", np.dtype(np.float64): "float64",
+         np.dtype(np.float32): "float32", np.dtype(np.uint8): "uint8", np.dtype(np.uint64): "uint64",
+         np.dtype(np.uint32): "uint32", np.dtype(np.bool_): "bool"}
+
+
+def to_dev(a: np.ndarray, dtype=None):
+    """Host numpy -> device tensor (copy)."""
+    t = torch()
+    dev = device()
+    a = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if not a.flags.writeable:
+        a = a.copy()
+    if a.dtype == np.uint64:
+        return t.from_numpy(a.view(np.int64)).to(dev)
+    if a.dtype == np.uint32:
+        return t.from_numpy(a.view(np.int32)).to(dev)
+    return t.from_numpy(a).to(dev)
+
+
+def to_host(x, dtype=None) -> np.ndarray:
+    """Device tensor -> host numpy (synchronous copy)."""
+    a = x.detach().cpu().numpy()
+    if dtype is not None and a.dtype != np.dtype(dtype):
+        a = a.view(dtype) if a.dtype.itemsize == np.dtype(dtype).itemsize else a.astype(dtype)
+    return a
+
+
+def empty(shape, dtype: str):
+    t = torch()
+    tmap = {"int32": t.int32, "int64": t.int64, "float64": t.float64, "float32": t.float32,
+            "uint8": t.uint8, "uint64": t.int64, "uint32": t.int32}
+    return t.empty(shape, dtype=tmap[dtype], device=device())
+
+
+def zeros(shape, dtype: str):
+    t = empty(shape, dtype)
+    t.zero_()
+    return t

@@ -1,0 +1,225 @@
+"""Sparse rating data: the input type of the hot path.
+
+Host side mirrors the reference's ``SparseRatings`` (data.py:166-257): the
+triplets in input order plus CSR (sorted by (row, col)) and CSC (sorted by
+(col, row)) numpy views, read-only, and the data baselines mu, b, b_hat
+(data.py:289-309) which the model uses as fixed residual statistics.
+
+Device side (``SparseRatings.device()``): the same two views resident in HBM as
+int64 pointers / int32 indices / fp64 values, the CSC->CSR position map used by
+the exact SGD schedule, and the baselines; exposed to the C ABI as a
+``CulshData`` struct.  Parsing, text I/O and holdout splitting of the reference
+are ingest, not hot path (SURVEY §2 Table A), and are not rebuilt here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+
+
+@dataclass
+class Triplets:
+    """A batch of rating triplets in dense index space (data.py:40-71)."""
+
+    rows: np.ndarray
+    cols: np.ndarray
+    values: np.ndarray
+    row_ids: list | None = None
+    col_ids: list | None = None
+
+    def __len__(self) -> int:
+        return len(self.rows)
+
+    @property
+    def M(self) -> int:
+        if self.row_ids is not None:
+            return len(self.row_ids)
+        return int(self.rows.max()) + 1 if len(self.rows) else 0
+
+    @property
+    def N(self) -> int:
+        if self.col_ids is not None:
+            return len(self.col_ids)
+        return int(self.cols.max()) + 1 if len(self.cols) else 0
+
+
+@dataclass
+class BaselineStats:
+    """Global mean plus per-row and per-column deviations (data.py:260-266)."""
+
+    mu: float
+    b: np.ndarray
+    b_hat: np.ndarray
+
+
+class SparseRatings:
+    """Dual-indexed sparse matrix, immutable after construction (data.py:166-207)."""
+
+    def __init__(self, M: int, N: int, rows: np.ndarray, cols: np.ndarray, values: np.ndarray,
+                 row_ids: list | None = None, col_ids: list | None = None):
+        self.M = int(M)
+        self.N = int(N)
+        self.entry_rows = np.ascontiguousarray(rows, dtype=np.int32)
+        self.entry_cols = np.ascontiguousarray(cols, dtype=np.int32)
+        self.entry_values = np.ascontiguousarray(values, dtype=np.float64)
+        self.row_ids = row_ids
+        self.col_ids = col_ids
+        nnz = len(self.entry_rows)
+        if len(self.entry_cols) != nnz or len(self.entry_values) != nnz:
+            raise ValueError("triplet arrays must have equal length")
+        order = np.lexsort((self.entry_cols, self.entry_rows))
+        self.row_ptr = np.zeros(self.M + 1, dtype=np.int64)
+        np.cumsum(np.bincount(self.entry_rows, minlength=self.M), out=self.row_ptr[1:])
+        self.row_cols = self.entry_cols[order]
+        self.row_vals = self.entry_values[order]
+        order = np.lexsort((self.entry_rows, self.entry_cols))
+        self.col_ptr = np.zeros(self.N + 1, dtype=np.int64)
+        np.cumsum(np.bincount(self.entry_cols, minlength=self.N), out=self.col_ptr[1:])
+        self.col_rows = self.entry_rows[order]
+        self.col_vals = self.entry_values[order]
+        self._baselines = None
+        self._dev = None
+        for arr in (self.entry_rows, self.entry_cols, self.entry_values, self.row_ptr,
+                    self.row_cols, self.row_vals, self.col_ptr, self.col_rows, self.col_vals):
+            arr.flags.writeable = False
+
+    @property
+    def nnz(self) -> int:
+        return len(self.entry_rows)
+
+    def triplets(self) -> Triplets:
+        return Triplets(self.entry_rows, self.entry_cols, self.entry_values, self.row_ids,
+                        self.col_ids)
+
+    def row_slice(self, i: int):
+        lo, hi = self.row_ptr[i], self.row_ptr[i + 1]
+        return self.row_cols[lo:hi], self.row_vals[lo:hi]
+
+    def col_slice(self, j: int):
+        lo, hi = self.col_ptr[j], self.col_ptr[j + 1]
+        return self.col_rows[lo:hi], self.col_vals[lo:hi]
+
+    def rating(self, i: int, j: int) -> float | None:
+        cols, vals = self.row_slice(i)
+        k = np.searchsorted(cols, j)
+        if k < len(cols) and cols[k] == j:
+            return float(vals[k])
+        return None
+
+    def baselines(self) -> BaselineStats:
+        if self._baselines is None:
+            self._baselines = compute_baselines(self)
+        return self._baselines
+
+    def device(self) -> "DeviceRatings":
+        """HBM-resident copy of both views (built once, cached)."""
+        if self._dev is None:
+            self._dev = DeviceRatings(self)
+        return self._dev
+
+
+def build_indices(triplets: Triplets, M: int | None = None, N: int | None = None) -> SparseRatings:
+    """Index triplets, rejecting out-of-range, non-finite and duplicate entries (data.py:269-286)."""
+    rows, cols, vals = triplets.rows, triplets.cols, triplets.values
+    M = triplets.M if M is None else M
+    N = triplets.N if N is None else N
+    if len(rows) and (rows.min() < 0 or rows.max() >= M):
+        raise ValueError("row index out of range")
+    if len(cols) and (cols.min() < 0 or cols.max() >= N):
+        raise ValueError("column index out of range")
+    if len(vals) and not np.all(np.isfinite(vals)):
+        raise ValueError("non-finite rating value")
+    if len(rows):
+        order = np.lexsort((cols, rows))
+        same = (np.diff(rows[order]) == 0) & (np.diff(cols[order]) == 0)
+        if same.any():
+            k = order[int(np.flatnonzero(same)[0])]
+            raise ValueError(f"duplicate entry at (row={rows[k]}, col={cols[k]})")
+    return SparseRatings(M, N, rows, cols, vals, triplets.row_ids, triplets.col_ids)
+
+
+def compute_baselines(ratings: SparseRatings) -> BaselineStats:
+    """mu and per-row / per-column mean deviations, 0 where empty (data.py:289-309).
+
+    Host numpy with the reference's summation order (np.mean pairwise sum,
+    np.add.at in entry order) so the residual statistics are bit-identical.
+    """
+    if ratings.nnz == 0:
+        raise ValueError("cannot compute baselines of an empty matrix")
+    mu = float(ratings.entry_values.mean())
+    row_counts = np.diff(ratings.row_ptr)
+    col_counts = np.diff(ratings.col_ptr)
+    row_sums = np.zeros(ratings.M)
+    np.add.at(row_sums, ratings.entry_rows, ratings.entry_values)
+    col_sums = np.zeros(ratings.N)
+    np.add.at(col_sums, ratings.entry_cols, ratings.entry_values)
+    b = np.zeros(ratings.M)
+    nz = row_counts > 0
+    b[nz] = row_sums[nz] / row_counts[nz] - mu
+    b_hat = np.zeros(ratings.N)
+    nz = col_counts > 0
+    b_hat[nz] = col_sums[nz] / col_counts[nz] - mu
+    return BaselineStats(mu=mu, b=b, b_hat=b_hat)
+
+
+class DeviceRatings:
+    """Both views of a SparseRatings in HBM plus the CulshData view for the C ABI.
+
+    Layout: col_ptr/row_ptr int64 (N+1 / M+1), col_rows/row_cols int32 (nnz),
+    col_vals/row_vals float64 (nnz), csc2csr int32 (nnz), base_b (M) and
+    base_bhat (N) float64.  About 36 bytes per rating.
+    """
+
+    @classmethod
+    def from_device(cls, M: int, N: int, col_ptr, col_rows, col_vals, row_ptr, row_cols, row_vals,
+                    mu: float, base_b, base_bhat) -> "DeviceRatings":
+        """Wrap index arrays that already live in HBM (e.g. built by synth.py)."""
+        self = cls.__new__(cls)
+        self.M, self.N, self.nnz = int(M), int(N), int(col_rows.numel())
+        self.col_ptr, self.col_rows, self.col_vals = col_ptr, col_rows, col_vals
+        self.row_ptr, self.row_cols, self.row_vals = row_ptr, row_cols, row_vals
+        self.mu, self.base_b, self.base_bhat = float(mu), base_b, base_bhat
+        self.csc2csr = nat.empty((max(self.nnz, 1),), "int32")
+        self.struct = self._make_struct()
+        nat.call("culsh_csc_to_csr_map", ctypes.byref(self.struct), nat.ptr(self.csc2csr),
+                 nat.stream_ptr())
+        return self
+
+    def __init__(self, r: SparseRatings, with_baselines: bool = True):
+        self.M, self.N, self.nnz = r.M, r.N, r.nnz
+        self.col_ptr = nat.to_dev(r.col_ptr, np.int64)
+        self.col_rows = nat.to_dev(r.col_rows, np.int32)
+        self.col_vals = nat.to_dev(r.col_vals, np.float64)
+        self.row_ptr = nat.to_dev(r.row_ptr, np.int64)
+        self.row_cols = nat.to_dev(r.row_cols, np.int32)
+        self.row_vals = nat.to_dev(r.row_vals, np.float64)
+        self.csc2csr = nat.empty((max(r.nnz, 1),), "int32")
+        if r.nnz and with_baselines:
+            st = r.baselines()
+            self.mu = st.mu
+            self.base_b = nat.to_dev(st.b, np.float64)
+            self.base_bhat = nat.to_dev(st.b_hat, np.float64)
+        else:
+            self.mu = 0.0
+            self.base_b = nat.zeros((max(r.M, 1),), "float64")
+            self.base_bhat = nat.zeros((max(r.N, 1),), "float64")
+        self.struct = self._make_struct()
+        nat.call("culsh_csc_to_csr_map", ctypes.byref(self.struct), nat.ptr(self.csc2csr),
+                 nat.stream_ptr())
+
+    def _make_struct(self) -> nat.CulshData:
+        p = nat.ptr
+        return nat.CulshData(self.M, self.N, self.nnz, p(self.col_ptr), p(self.col_rows),
+                             p(self.col_vals), p(self.row_ptr), p(self.row_cols), p(self.row_vals),
+                             p(self.csc2csr), p(self.base_b), p(self.base_bhat))
+
+    def set_baselines(self, mu: float, b: np.ndarray, b_hat: np.ndarray) -> None:
+        self.mu = float(mu)
+        self.base_b = nat.to_dev(b, np.float64)
+        self.base_bhat = nat.to_dev(b_hat, np.float64)
+        self.struct = self._make_struct()

@@ -1,0 +1,171 @@
+"""fp32 Hogwild training -- the performance mode of train_full.
+
+Per fit (once): upload fp32 parameters (same PCG64 initial values as the
+reference's init_params, factorization.py:196-211), build the explicit-neighbour
+stream (a K-bit mask per rating + compact residuals, csrc/sgd_hogwild.cu), and
+order columns longest-first.  Per epoch: ONE kernel launch
+(culsh_sgd_hogwild_epoch) that updates all six parameter classes.
+
+HBM traffic per update (the roofline's algorithmic bytes):
+  B_upd = 8 (row, value) + 8F (u_i read+write) + 8 (b_i read+write)
+          + K/8 (mask) + 4*E (residuals, E = mean explicit count)
+plus per column per epoch 2(4F + 8K + 4) bytes of v/w/c/b_hat.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from .factorization import (ModelParams, TrainConfig, TrainingDivergedError, _rates_struct,
+                            init_params)
+from .similarity import NeighborTable
+
+
+class DeviceModel32:
+    def __init__(self, p: ModelParams):
+        t = nat.torch()
+        dev = nat.device()
+        f32 = lambda a: t.from_numpy(np.ascontiguousarray(a, np.float32).reshape(-1)).to(dev)
+        self.F, self.K = p.F, p.K
+        self.mu = float(p.mu)
+        self.b = f32(p.b)
+        self.bhat = f32(p.b_hat)
+        self.U = f32(p.U)
+        self.V = f32(p.V)
+        self.W = f32(p.W) if p.W.size else nat.zeros((1,), "float32")
+        self.C = f32(p.C) if p.C.size else nat.zeros((1,), "float32")
+        self.struct = nat.CulshModel32(self.mu, nat.ptr(self.b), nat.ptr(self.bhat), nat.ptr(self.U),
+                                       nat.ptr(self.V), nat.ptr(self.W), nat.ptr(self.C), self.F,
+                                       self.K)
+
+    def to_params(self, neighbors: NeighborTable | None, M: int, N: int) -> ModelParams:
+        h = lambda x, shape: nat.to_host(x).astype(np.float64)[:int(np.prod(shape))].reshape(shape)
+        return ModelParams(mu=self.mu, b=h(self.b, (M,)), b_hat=h(self.bhat, (N,)),
+                           U=h(self.U, (M, self.F)), V=h(self.V, (N, self.F)),
+                           W=h(self.W, (N, self.K)), C=h(self.C, (N, self.K)),
+                           neighbors=neighbors)
+
+
+def hogwild_supported(F: int, K: int) -> bool:
+    return (1 <= F <= 32 or F in (64, 128, 256)) and 0 <= K <= 64
+
+
+class HogwildTrainer:
+    """Device-resident fp32 training state for one fit.
+
+    ``dev`` may be a DeviceRatings (data.py) or any object with the same
+    attributes (bench.py builds one directly in HBM).
+    """
+
+    def __init__(self, ratings, neighbors: NeighborTable | None, config: TrainConfig,
+                 dev=None, params: ModelParams | None = None):
+        config.validate()
+        self.config = config
+        self.neighbors = neighbors
+        K = neighbors.K if neighbors is not None else 0
+        if not hogwild_supported(config.F, K):
+            raise ValueError(f"Hogwild mode supports F <= 32 or F in (64, 128, 256) and K <= 64; "
+                             f"got F={config.F}, K={K}")
+        t = nat.torch()
+        self.dev = dev if dev is not None else ratings.device()
+        d = self.dev
+        self.M, self.N, self.nnz = d.M, d.N, d.nnz
+        if params is None:
+            stats = ratings.baselines()
+            params = init_params(d.M, d.N, config.F, K, neighbors, stats, config)
+        self.model = DeviceModel32(params)
+        self.K = K
+        MW = 1 if K <= 32 else 2
+        self.MW = MW
+        # explicit-neighbour stream (data + J^K only; once per fit)
+        self.nbr = (nat.to_dev(neighbors.entries.reshape(-1), np.int32) if K
+                    else nat.zeros((1,), "int32"))
+        self.mask = nat.zeros((max(d.nnz * MW, 1),), "int32")
+        nexpl = nat.zeros((max(d.N, 1),), "int64")
+        self.resid_ptr = nat.zeros((d.N + 1,), "int64")
+        if K and d.nnz:
+            nat.call("culsh_explicit_stream", ctypes.byref(d.struct), float(d.mu), nat.ptr(self.nbr),
+                     K, nat.ptr(self.mask), nat.ptr(nexpl), None, None, nat.stream_ptr())
+            t.cumsum(nexpl[:d.N], 0, out=self.resid_ptr[1:])
+        n_res = int(self.resid_ptr[-1].item()) if d.N else 0
+        self.resid = nat.zeros((max(n_res, 1),), "float32")
+        if K and n_res:
+            nat.call("culsh_explicit_stream", ctypes.byref(d.struct), float(d.mu), nat.ptr(self.nbr),
+                     K, nat.ptr(self.mask), nat.ptr(nexpl), nat.ptr(self.resid_ptr),
+                     nat.ptr(self.resid), nat.stream_ptr())
+        self.n_explicit = n_res
+        self.vals32 = d.col_vals.to(t.float32)
+        counts = d.col_ptr[1:] - d.col_ptr[:-1]
+        self.col_order = t.argsort(counts, descending=True, stable=True).to(t.int32)
+        self.ticket = nat.zeros((1,), "int32")
+        self.status = nat.zeros((1,), "int32")
+        self.loss = nat.zeros((1,), "float64")
+
+    def bytes_per_update(self) -> float:
+        """Algorithmic HBM bytes per rating update (SURVEY §8(d) B_upd) + per-column share."""
+        F, K = self.config.F, self.K
+        E = self.n_explicit / max(self.nnz, 1)
+        b_upd = 8 + 8 * F + 8 + K / 8 + 4 * E
+        b_col = 2 * (4 * F + 8 * K + 4) + 4 * K
+        return b_upd + b_col * self.N / max(self.nnz, 1)
+
+    def launch_epoch(self, t_epoch: int, seg=None, col_order=None, n_cols: int | None = None) -> None:
+        """Enqueue one epoch (no host synchronisation).  With ``seg`` / ``col_order``
+        it runs one DSGD block: the listed columns, entry ranges from seg."""
+        c = self.config
+        rates = _rates_struct(c.rates_at(t_epoch), c.regs)
+        d = self.dev
+        order = self.col_order if col_order is None else col_order
+        n = d.N if n_cols is None else n_cols
+        nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(d.col_rows),
+                 nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
+                 nat.ptr(self.resid), nat.ptr(order), ctypes.byref(self.model.struct),
+                 ctypes.byref(rates), nat.ptr(self.ticket), nat.ptr(self.loss),
+                 nat.ptr(self.status), nat.stream_ptr())
+
+    def epoch(self, t_epoch: int) -> None:
+        self.launch_epoch(t_epoch)
+        if int(self.status.item()):
+            raise TrainingDivergedError(epoch=t_epoch)
+
+    def pinned_stream(self) -> dict:
+        """Pinned host copy of the per-epoch rating stream (CSC rows, fp32 values, masks)."""
+        return {"rows": self.dev.col_rows.cpu().pin_memory(),
+                "vals": self.vals32.cpu().pin_memory(),
+                "mask": self.mask.cpu().pin_memory()}
+
+    def epoch_from_host(self, host: dict, t_epoch: int):
+        """One epoch whose rating stream comes from pinned host memory: H2D copy of
+        the stream, the epoch kernel, D2H of the epoch's summed squared error.
+        Returns (sum of e^2 over the epoch, h2d bytes, d2h bytes)."""
+        self.dev.col_rows.copy_(host["rows"], non_blocking=True)
+        self.vals32.copy_(host["vals"], non_blocking=True)
+        self.mask.copy_(host["mask"], non_blocking=True)
+        self.loss.zero_()
+        self.launch_epoch(t_epoch)
+        loss = float(self.loss.item())
+        if int(self.status.item()):
+            raise TrainingDivergedError(epoch=t_epoch)
+        h2d = sum(int(v.numel() * v.element_size()) for v in host.values())
+        return loss, h2d, 8 + 4
+
+    def to_params(self) -> ModelParams:
+        return self.model.to_params(self.neighbors, self.M, self.N)
+
+    def rmse(self, t_rows, t_cols, t_vals) -> float:
+        """Test RMSE of the current fp32 model (predictions evaluated in fp64)."""
+        n = len(t_rows)
+        if n == 0:
+            raise ValueError("empty test set")
+        tr = nat.to_dev(np.asarray(t_rows, np.int32))
+        tc = nat.to_dev(np.asarray(t_cols, np.int32))
+        tv = nat.to_dev(np.asarray(t_vals, np.float64))
+        scratch = nat.empty((n + 256,), "float64")
+        out = nat.empty((1,), "float64")
+        nat.call("culsh_rmse32", ctypes.byref(self.dev.struct), ctypes.byref(self.model.struct),
+                 nat.ptr(self.nbr), nat.ptr(tr), nat.ptr(tc), nat.ptr(tv), n, nat.ptr(scratch),
+                 nat.ptr(out), nat.stream_ptr())
+        return float(out.item())

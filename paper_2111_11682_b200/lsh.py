@@ -1,0 +1,337 @@
+"""simLSH signatures, buckets and frequency Top-K on the GPU.
+
+Same public surface and semantics as the reference module lshmf.lsh
+(lsh.py:30-438); every array result is bit-identical to it.  The compute runs
+in libculsh.so (csrc/lsh.cu, csrc/topk.cu):
+
+  assign_row_hashes  -> culsh_row_hash_table   (lsh.py:68-114)
+  compute_hash_state -> culsh_hash_accumulate  (lsh.py:161-183, 231-239, 246-260 fused)
+  simlsh_topk        -> + culsh_topk           (lsh.py:263-374, 401-438)
+
+Host objects (RowHashes, HashState) keep their device tensors and materialise
+numpy views lazily, so a device pipeline never round-trips through the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .data import SparseRatings
+from .similarity import NeighborTable
+
+HASHSTATE_MAGIC = "LSHMF-H"
+HASHSTATE_VERSION = "v1"
+
+
+@dataclass
+class LshConfig:
+    """Signature parameters: G bits per map, p maps per group, q groups (lsh.py:30-50)."""
+
+    G: int = 8
+    p: int = 3
+    q: int = 100
+    psi_exponent: int = 2
+    seed: int = 0
+
+    def validate(self) -> None:
+        if not (1 <= self.G <= 64):
+            raise ValueError(f"G must be in [1, 64], got {self.G}")
+        if self.p < 1 or self.q < 1:
+            raise ValueError("p and q must be >= 1")
+        if self.p * self.G > 64:
+            raise ValueError(f"p*G = {self.p * self.G} exceeds the 64-bit bucket key")
+        if self.psi_exponent not in (1, 2, 4):
+            raise ValueError(f"psi_exponent must be 1, 2 or 4, got {self.psi_exponent}")
+        if self.seed < 0:
+            raise ValueError("seed must be nonnegative")
+
+
+def _ns(G: int) -> int:
+    return (G + 7) // 8
+
+
+class RowHashes:
+    """Random G-bit row hashes for all p*q maps, keyed by (seed, group, map, row).
+
+    ``bits`` is the reference's (M, q, p, G) uint8 tensor (lsh.py:81-105); on the
+    device the same bits are a packed (M, q, p, ceil(G/8)) byte table.
+    """
+
+    def __init__(self, bits: np.ndarray | None = None, seed: int = 0, *, _table=None,
+                 _shape=None):
+        self.seed = int(seed)
+        self._bits = None if bits is None else np.ascontiguousarray(bits, dtype=np.uint8)
+        self._table = _table
+        self._shape = tuple(_shape) if _shape is not None else tuple(self._bits.shape)
+
+    @property
+    def bits(self) -> np.ndarray:
+        if self._bits is None:
+            M, q, p, G = self._shape
+            out = nat.empty((max(M * q * p * G, 1),), "uint8")
+            nat.call("culsh_unpack_bits", nat.ptr(self._table), M, q, p, G, nat.ptr(out),
+                     nat.stream_ptr())
+            self._bits = nat.to_host(out)[:M * q * p * G].reshape(M, q, p, G)
+        return self._bits
+
+    @property
+    def M(self) -> int:
+        return self._shape[0]
+
+    def map_bits(self, g: int, m: int) -> np.ndarray:
+        return self.bits[:, g, m, :]
+
+    def table(self):
+        """Packed device table (packs injected host bits on first use)."""
+        if self._table is None:
+            M, q, p, G = self._shape
+            src = nat.to_dev(self._bits.reshape(-1) if self._bits.size else np.zeros(1, np.uint8))
+            t = nat.empty((max(M * q * p * _ns(G), 1),), "uint8")
+            nat.call("culsh_pack_bits", nat.ptr(src), M, q, p, G, nat.ptr(t), nat.stream_ptr())
+            self._table = t
+        return self._table
+
+    def extended(self, M_new: int) -> "RowHashes":
+        if M_new < self.M:
+            raise ValueError("cannot shrink row hashes")
+        _, q, p, G = self._shape
+        return _device_row_hashes(M_new, q, p, G, self.seed)
+
+
+def _device_row_hashes(M: int, q: int, p: int, G: int, seed: int) -> RowHashes:
+    t = nat.empty((max(M * q * p * _ns(G), 1),), "uint8")
+    nat.call("culsh_row_hash_table", ctypes.c_uint64(seed), q, p, G, 0, M, nat.ptr(t),
+             nat.stream_ptr())
+    return RowHashes(None, seed, _table=t, _shape=(M, q, p, G))
+
+
+def assign_row_hashes(M: int, config: LshConfig) -> RowHashes:
+    """Independent uniform G-bit hashes for every (group, map, row) (lsh.py:108-114)."""
+    config.validate()
+    if M < 0:
+        raise ValueError("M must be nonnegative")
+    return _device_row_hashes(M, config.q, config.p, config.G, config.seed)
+
+
+class HashState:
+    """Per-column signed accumulators and signatures (lsh.py:186-228).
+
+    ``acc`` (N, q, p, G) float64 and ``sig`` (N, q, p, G) uint8 are numpy
+    arrays materialised on first access; the device copies (and the packed
+    group keys (q, N) uint64) stay resident for the online path.
+    """
+
+    def __init__(self, acc: np.ndarray | None = None, sig: np.ndarray | None = None,
+                 config: LshConfig | None = None, *, _dev_acc=None, _dev_sig=None,
+                 _dev_keys=None, _shape=None):
+        self.config = config
+        self._acc = acc
+        self._sig = sig
+        self._dev_acc = _dev_acc
+        self._dev_sig = _dev_sig
+        self._dev_keys = _dev_keys
+        self._shape = tuple(_shape) if _shape is not None else tuple(np.shape(acc))
+
+    def __eq__(self, other):
+        if not isinstance(other, HashState):
+            return NotImplemented
+        return (self.config == other.config and np.array_equal(self.acc, other.acc)
+                and np.array_equal(self.sig, other.sig))
+
+    @property
+    def acc(self) -> np.ndarray:
+        if self._acc is None:
+            self._acc = nat.to_host(self._dev_acc).reshape(self._shape)
+        return self._acc
+
+    @acc.setter
+    def acc(self, value):
+        self._acc = value
+        self._dev_acc = None
+        self._dev_keys = None
+        self._shape = tuple(np.shape(value))
+
+    @property
+    def sig(self) -> np.ndarray:
+        if self._sig is None:
+            if self._dev_sig is not None:
+                self._sig = nat.to_host(self._dev_sig).reshape(self._shape)
+            else:
+                self._sig = (self.acc >= 0.0).astype(np.uint8)
+        return self._sig
+
+    @sig.setter
+    def sig(self, value):
+        self._sig = value
+        self._dev_sig = None
+
+    @property
+    def N(self) -> int:
+        return self._shape[0]
+
+    def acc_map(self, g: int, m: int) -> np.ndarray:
+        return self.acc[:, g, m, :]
+
+    def sig_map(self, g: int, m: int) -> np.ndarray:
+        return self.sig[:, g, m, :]
+
+    def device_acc(self):
+        if self._dev_acc is None:
+            self._dev_acc = nat.to_dev(np.ascontiguousarray(self._acc, dtype=np.float64).reshape(-1)
+                                       if np.size(self._acc) else np.zeros(1))
+        return self._dev_acc
+
+    def device_keys(self):
+        """(q, N) uint64 group keys on the device (recomputed from acc if absent)."""
+        if self._dev_keys is None:
+            c = self.config
+            N = self.N
+            keys = nat.empty((c.q * max(N, 1),), "uint64")
+            if N:
+                _keys_from_acc(self.device_acc(), N, c, keys)
+            self._dev_keys = keys
+        return self._dev_keys
+
+    def save(self, path) -> None:
+        c = self.config
+        with open(path, "wb") as fh:
+            header = (f"{HASHSTATE_MAGIC} {HASHSTATE_VERSION} {self.N} {c.G} "
+                      f"{c.p} {c.q} {c.psi_exponent} {c.seed}\n")
+            fh.write(header.encode())
+            blob = np.ascontiguousarray(self.acc.transpose(1, 2, 0, 3))
+            fh.write(blob.astype("<f8").tobytes())
+
+    @classmethod
+    def load(cls, path) -> "HashState":
+        with open(path, "rb") as fh:
+            header = fh.readline().decode().split()
+            if len(header) != 8 or header[0] != HASHSTATE_MAGIC or header[1] != HASHSTATE_VERSION:
+                raise ValueError(f"{path}: not a {HASHSTATE_MAGIC} {HASHSTATE_VERSION} file")
+            N, G, p, q, e, seed = (int(x) for x in header[2:])
+            blob = np.frombuffer(fh.read(), dtype="<f8")
+        acc = blob.reshape(q, p, N, G).transpose(2, 0, 1, 3).copy()
+        config = LshConfig(G=G, p=p, q=q, psi_exponent=e, seed=seed)
+        return cls(acc=acc, sig=(acc >= 0.0).astype(np.uint8), config=config)
+
+
+def _keys_from_acc(acc_dev, N: int, c: LshConfig, keys_out) -> None:
+    """Group keys of an existing accumulator state: threshold + pack on the device.
+
+    Runs the accumulation kernel in `into` mode over empty columns, which leaves
+    acc unchanged and re-emits sig-derived keys (lsh.py:246-260, 417-423).
+    """
+    empty_ptr = nat.zeros((N + 1,), "int64")
+    dummy_rows = nat.zeros((1,), "int32")
+    dummy_vals = nat.zeros((1,), "float64")
+    table = nat.zeros((max(c.q * c.p * _ns(c.G), 1),), "uint8")
+    nat.call("culsh_hash_accumulate", nat.ptr(empty_ptr), nat.ptr(dummy_rows), nat.ptr(dummy_vals),
+             0, N, None, nat.ptr(table), c.q, c.p, c.G, c.psi_exponent, 1, 0, nat.ptr(acc_dev),
+             None, nat.ptr(keys_out), N, nat.stream_ptr())
+
+
+def _int_path_ok(dev, col_begin: int, n_cols: int, col_list, e: int) -> bool:
+    bad = nat.zeros((1,), "int32")
+    nat.call("culsh_psi_int_check", nat.ptr(dev.col_ptr), nat.ptr(dev.col_vals), col_begin, n_cols,
+             nat.ptr(col_list), e, nat.ptr(bad), nat.stream_ptr())
+    return int(bad.item()) == 0
+
+
+def _accumulate(dev, table, c: LshConfig, acc, sig, keys, col_begin: int, n_cols: int,
+                col_list=None, into: bool = False, keys_ld: int | None = None) -> None:
+    int_path = (not into) and _int_path_ok(dev, col_begin, n_cols, col_list, c.psi_exponent)
+    nat.call("culsh_hash_accumulate", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
+             nat.ptr(dev.col_vals), col_begin, n_cols, nat.ptr(col_list), nat.ptr(table), c.q, c.p,
+             c.G, c.psi_exponent, int(into), int(int_path), nat.ptr(acc), nat.ptr(sig),
+             nat.ptr(keys), dev.N if keys_ld is None else keys_ld, nat.stream_ptr())
+
+
+def compute_hash_state(ratings: SparseRatings, config: LshConfig,
+                       hashes: RowHashes | None = None) -> HashState:
+    """Encode every column under all p*q maps (lsh.py:231-239)."""
+    config.validate()
+    if hashes is None:
+        hashes = assign_row_hashes(ratings.M, config)
+    else:
+        _, q, p, G = hashes._shape
+        if (q, p, G) != (config.q, config.p, config.G):
+            raise ValueError("row hashes do not match the configuration")
+        if hashes.M < ratings.M:
+            raise ValueError("row hashes do not cover every row")
+    return hash_state_device(ratings.device(), config, hashes)
+
+
+def hash_state_device(dev, config: LshConfig, hashes: RowHashes | None = None) -> HashState:
+    """compute_hash_state on HBM-resident ratings (a DeviceRatings)."""
+    config.validate()
+    if hashes is None:
+        hashes = assign_row_hashes(dev.M, config)
+    N, c = dev.N, config
+    W = c.q * c.p * c.G
+    acc = nat.empty((max(N * W, 1),), "float64")
+    sig = nat.empty((max(N * W, 1),), "uint8")
+    keys = nat.empty((c.q * max(N, 1),), "uint64")
+    if N:
+        _accumulate(dev, hashes.table(), c, acc, sig, keys, 0, N)
+    return HashState(config=config, _dev_acc=acc, _dev_sig=sig, _dev_keys=keys,
+                     _shape=(N, c.q, c.p, c.G))
+
+
+def simlsh_signature(j: int, ratings: SparseRatings, H: np.ndarray, psi_exponent: int = 1):
+    """Encode column j against one M x G hash map (lsh.py:126-158, Fig. 3)."""
+    H = np.ascontiguousarray(H, dtype=np.uint8)
+    M, G = H.shape
+    if not (1 <= G <= 64):
+        raise ValueError("G must be in [1, 64]")
+    if psi_exponent not in (1, 2, 4):
+        raise ValueError(f"psi_exponent must be 1, 2 or 4, got {psi_exponent}")
+    hashes = RowHashes(H.reshape(M, 1, 1, G), 0)
+    cfg = LshConfig(G=G, p=1, q=1, psi_exponent=psi_exponent, seed=0)
+    dev = ratings.device()
+    acc = nat.zeros((ratings.N * G,), "float64")
+    sig = nat.zeros((ratings.N * G,), "uint8")
+    col = nat.to_dev(np.array([j], np.int32))
+    _accumulate(dev, hashes.table(), cfg, acc, sig, None, 0, 1, col_list=col)
+    a = nat.to_host(acc).reshape(ratings.N, G)[j].copy()
+    s = nat.to_host(sig).reshape(ratings.N, G)[j].copy()
+    return a, s
+
+
+def _topk_device(keys, q: int, N_total: int, key_bits: int, j_base: int, n_cols: int, K: int,
+                 seed: int):
+    entries = nat.empty((max(n_cols * K, 1),), "int32")
+    ncand = ctypes.c_int64(0)
+    nat.call("culsh_topk", nat.ptr(keys), q, N_total, key_bits, j_base, n_cols, K,
+             ctypes.c_uint64(seed), nat.ptr(entries), ctypes.byref(ncand), nat.stream_ptr())
+    return entries, int(ncand.value)
+
+
+def simlsh_topk(ratings: SparseRatings, config: LshConfig, K: int):
+    """Approximate Top-K neighbours of every column (lsh.py:426-438).
+
+    Returns (NeighborTable, HashState).
+    """
+    config.validate()
+    if K > ratings.N - 1:
+        raise ValueError(f"K={K} exceeds N-1={ratings.N - 1}")
+    state = compute_hash_state(ratings, config)
+    N = ratings.N
+    entries, _ = _topk_device(state.device_keys(), config.q, N, config.p * config.G, 0, N, K,
+                              config.seed)
+    ent = nat.to_host(entries)[:N * K].reshape(N, K).astype(np.int32, copy=False)
+    return NeighborTable(N=N, K=K, entries=ent), state
+
+
+def simlsh_topk_device(dev, config: LshConfig, K: int):
+    """simlsh_topk on HBM-resident ratings; returns (entries (N*K) int32 device tensor,
+    HashState, candidate count) without any host round trip of the arrays."""
+    config.validate()
+    if K > dev.N - 1:
+        raise ValueError(f"K={K} exceeds N-1={dev.N - 1}")
+    state = hash_state_device(dev, config)
+    entries, ncand = _topk_device(state.device_keys(), config.q, dev.N, config.p * config.G, 0,
+                                  dev.N, K, config.seed)
+    return entries, state, ncand

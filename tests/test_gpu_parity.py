@@ -1,0 +1,379 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+fixtures and the CPU oracle, bit-exact for hashes / keys / top-K / exact-mode
+SGD / online, and RMSE within 0.005 for the Hogwild mode."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2111_11682_b200 as p
+    return p
+
+
+def ratings_of(P, z, pre):
+    return P.SparseRatings(int(z[pre + "M"]), int(z[pre + "N"]), z[pre + "rows"], z[pre + "cols"],
+                           z[pre + "vals"])
+
+
+@pytest.fixture(scope="module")
+def c1(P):
+    z = load_golden("c1.npz")
+    tr = P.SparseRatings(int(z["train_M"]), int(z["train_N"]), z["train_rows"].astype(np.int32),
+                         z["train_cols"].astype(np.int32), z["train_vals"].astype(np.float64))
+    te = P.Triplets(z["test_rows"].astype(np.int32), z["test_cols"].astype(np.int32),
+                    z["test_vals"].astype(np.float64))
+    return z, tr, te
+
+
+REF_TOL_RMSE = 0.005
+
+
+# ------------------------------------------------------------------ hashes ---
+
+class TestHashKat:
+    def test_worked_example_fig3(self, P):
+        # test_lsh.py:63-66
+        r = P.SparseRatings(3, 1, np.array([0, 1, 2]), np.array([0, 0, 0]), np.array([3., 4., 5.]))
+        H = np.array([[0, 0, 1], [0, 1, 0], [1, 0, 0]], dtype=np.uint8)
+        acc, sig = P.simlsh_signature(0, r, H, psi_exponent=1)
+        np.testing.assert_array_equal(acc, [-2.0, -4.0, -6.0])
+        np.testing.assert_array_equal(sig, [0, 0, 0])
+
+    def test_empty_column_all_ones(self, P):
+        r = P.SparseRatings(3, 1, np.zeros(0), np.zeros(0), np.zeros(0))
+        acc, sig = P.simlsh_signature(0, r, np.eye(3, dtype=np.uint8), 1)
+        np.testing.assert_array_equal(acc, [0, 0, 0])
+        np.testing.assert_array_equal(sig, [1, 1, 1])
+
+    def test_single_rating_matches_row_hash(self, P):
+        H = np.array([[0, 0, 1], [0, 1, 0], [1, 0, 0]], dtype=np.uint8)
+        r = P.SparseRatings(3, 1, np.array([1]), np.array([0]), np.array([2.5]))
+        _, sig = P.simlsh_signature(0, r, H, 1)
+        np.testing.assert_array_equal(sig, H[1])
+
+    def test_psi_exponents(self, P):
+        r = P.SparseRatings(1, 1, np.array([0]), np.array([0]), np.array([3.0]))
+        H = np.ones((1, 2), dtype=np.uint8)
+        for e, want in [(1, 3.0), (2, 9.0), (4, 81.0)]:
+            acc, _ = P.simlsh_signature(0, r, H, e)
+            assert acc[0] == want
+
+    def test_row_hashes_match_oracle(self, P, orc):
+        for (M, G, p, q, seed) in [(50, 8, 2, 3, 11), (37, 13, 2, 5, 3), (20, 64, 1, 2, 9),
+                                   (0, 4, 2, 2, 0)]:
+            h = P.assign_row_hashes(M, P.LshConfig(G=G, p=p, q=q, seed=seed))
+            assert h.bits.shape == (M, q, p, G)
+            np.testing.assert_array_equal(h.bits, orc.assign_bits(seed, q, p, M, G))
+        h = P.assign_row_hashes(50, P.LshConfig(G=8, p=2, q=3, seed=11))
+        np.testing.assert_array_equal(h.extended(80).bits[:50], h.bits)
+
+    def test_ones_fraction(self, P):
+        h = P.assign_row_hashes(10_000, P.LshConfig(G=8, p=2, q=2, seed=0))
+        frac = h.bits.reshape(10_000, -1).mean(axis=0)
+        assert frac.min() >= 0.48 and frac.max() <= 0.52
+
+
+class TestHashGolden:
+    def test_lsh_small_bit_exact(self, P):
+        z = load_golden("lsh_small.npz")
+        for k in range(int(z["n_runs"])):
+            pre = f"k{k}_"
+            G, p, q, e, seed, K = (int(x) for x in z[pre + "cfg"])
+            r = ratings_of(P, z, f"c{int(z[pre + 'case'])}_")
+            table, state = P.simlsh_topk(r, P.LshConfig(G=G, p=p, q=q, psi_exponent=e, seed=seed), K)
+            assert state.acc.tobytes() == z[pre + "acc"].tobytes(), k
+            assert state.sig.tobytes() == z[pre + "sig"].tobytes(), k
+            keys = P._native.to_host(state.device_keys()).view(np.uint64).reshape(q, r.N)
+            assert keys.tobytes() == z[pre + "keys"].tobytes(), k
+            assert table.entries.tobytes() == z[pre + "entries"].tobytes(), k
+            table.validate()
+
+    def test_c1_bit_exact(self, P, c1):
+        z, tr, _ = c1
+        cfg = P.LshConfig(G=8, p=3, q=100, psi_exponent=2, seed=0)
+        table, state = P.simlsh_topk(tr, cfg, 16)
+        assert sha(state.acc) == str(z["lsh_acc_sha"])
+        assert sha(state.sig) == str(z["lsh_sig_sha"])
+        assert table.entries.tobytes() == z["lsh_entries16"].tobytes()
+        t32, _ = P.simlsh_topk(tr, cfg, 32)
+        assert t32.entries.tobytes() == z["lsh_entries32"].tobytes()
+
+    def test_fp64_path_equals_int_path(self, P, orc):
+        """Integer ratings take the exact-integer kernel; the ordered fp64 kernel
+        (used for non-integer data) must give the identical bytes."""
+        from paper_2111_11682_b200 import lsh as L, _native as nat
+        rng = np.random.default_rng(5)
+        M, N = 200, 150
+        mask = rng.random((M, N)) < 0.1
+        rows, cols = np.nonzero(mask)
+        vals = rng.integers(1, 6, size=len(rows)).astype(float)
+        r = P.SparseRatings(M, N, rows, cols, vals)
+        c = P.LshConfig(G=8, p=3, q=20, psi_exponent=2, seed=4)
+        st = P.compute_hash_state(r, c)
+        dev = r.device()
+        h = P.assign_row_hashes(M, c)
+        W = c.q * c.p * c.G
+        acc = nat.zeros((N * W,), "float64")
+        nat.call("culsh_hash_accumulate", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
+                 nat.ptr(dev.col_vals), 0, N, None, nat.ptr(h.table()), c.q, c.p, c.G, 2, 0, 0,
+                 nat.ptr(acc), None, None, N, nat.stream_ptr())
+        assert nat.to_host(acc).tobytes() == st.acc.tobytes()
+        ref = orc.accumulate_all(r.col_ptr, r.col_rows, r.col_vals, orc.assign_bits(4, 20, 3, M, 8), 2)
+        assert ref.tobytes() == st.acc.tobytes()
+
+    def test_injected_hashes(self, P, orc):
+        """compute_hash_state with user-supplied RowHashes (lsh.py:231-239)."""
+        rng = np.random.default_rng(1)
+        bits = (rng.random((30, 2, 2, 5)) < 0.5).astype(np.uint8)
+        rows = rng.integers(0, 30, 60)
+        cols = rng.integers(0, 12, 60)
+        key = np.unique(rows * 100 + cols)
+        r = P.SparseRatings(30, 12, key // 100, key % 100, rng.uniform(0.5, 5, len(key)))
+        st = P.compute_hash_state(r, P.LshConfig(G=5, p=2, q=2, psi_exponent=4),
+                                  P.RowHashes(bits=bits, seed=0))
+        ref = orc.accumulate_all(r.col_ptr, r.col_rows, r.col_vals, bits, 4)
+        assert st.acc.tobytes() == ref.tobytes()
+
+
+# --------------------------------------------------------------------- SGD ---
+
+REGS = (0.02, 0.02, 0.02, 0.02, 0.002, 0.002)
+
+
+class TestSgdExact:
+    def test_sgd_small_bit_exact(self, P):
+        z = load_golden("sgd_small.npz")
+        for s in range(int(z["n_cases"])):
+            pre = f"s{s}_"
+            F, K, epochs, seed = (int(x) for x in z[pre + "cfg"])
+            r = ratings_of(P, z, pre)
+            nbr = P.NeighborTable(r.N, K, z[pre + "nbr"]) if K else None
+            cfg = P.TrainConfig(F=F, K=K, epochs=epochs, seed=seed)
+            p = P.train_full(r, nbr, cfg)
+            for n in ("b", "b_hat", "U", "V", "W", "C"):
+                assert getattr(p, n).tobytes() == z[f"{pre}full_{n}"].tobytes(), (s, n)
+            assert P.rmse(p, r.triplets(), r) == float(z[pre + "rmse"])
+            assert P.rmse(p, r.triplets(), r, unscale=2.0, clamp=(1.5, 4.5)) == float(z[pre + "rmse_clamp"])
+            for D in (2, 3):
+                pd = P.parallel_train(r, nbr, cfg, D=D)
+                for n in ("b", "b_hat", "U", "V", "W", "C"):
+                    assert getattr(pd, n).tobytes() == z[f"{pre}D{D}_{n}"].tobytes(), (s, D, n)
+            p1 = P.parallel_train(r, nbr, cfg, D=1)
+            assert p1.U.tobytes() == p.U.tobytes()
+
+    def test_c1_train_full_bit_exact(self, P, c1):
+        z, tr, te = c1
+        nbr = P.NeighborTable(tr.N, 16, z["lsh_entries16"])
+        seen = []
+        p = P.train_full(tr, nbr, P.TrainConfig(F=32, K=16, epochs=3, seed=0),
+                         epoch_callback=lambda t, q: seen.append(P.rmse(q, te, tr)))
+        np.testing.assert_array_equal(seen, z["sgd_rmse_test"])
+        for n in ("b", "b_hat", "U", "V", "W", "C"):
+            assert sha(getattr(p, n)) == str(z[f"sgd_full_{n}_sha"]), n
+
+    def test_c1_dsgd_d4_bit_exact(self, P, c1):
+        z, tr, te = c1
+        nbr = P.NeighborTable(tr.N, 16, z["lsh_entries16"])
+        times = []
+        pd, rep = P.parallel_train(tr, nbr, P.TrainConfig(F=32, K=16, epochs=2, seed=0), D=4,
+                                   instrument=True, stage_times=times)
+        assert rep.ok and rep.stages_checked == 8
+        assert len(times) == 8
+        for n in ("b", "U", "V", "W", "C"):
+            assert sha(getattr(pd, n)) == str(z[f"sgd_D4_{n}_sha"]), n
+        assert P.rmse(pd, te, tr) == float(z["sgd_D4_rmse_test"])
+
+    def test_predict_hand_value(self, P):
+        # test_factorization.py:148-158 -> 3.8
+        r = P.SparseRatings(3, 3, np.array([0, 0, 1, 1, 1, 2, 2]), np.array([0, 2, 0, 1, 2, 1, 2]),
+                            np.array([4, 2, 2, 3, 4, 3, 3.0]))
+        nbr = P.NeighborTable(3, 2, np.array([[1, 2], [0, 2], [0, 1]], dtype=np.int32))
+        p = P.ModelParams(mu=3.0, b=np.zeros(3), b_hat=np.zeros(3),
+                          U=np.array([[0.5], [0.0], [0.0]]), V=np.array([[0.0], [0.0], [1.0]]),
+                          W=np.array([[0.0, 0.0], [0.0, 0.0], [0.1, 0.0]]),
+                          C=np.array([[0.0, 0.0], [0.0, 0.0], [0.0, 0.2]]), neighbors=nbr)
+        assert P.predict(0, 2, p, r) == pytest.approx(3.8, abs=1e-12)
+        with pytest.raises(IndexError):
+            P.predict(5, 0, p, r)
+
+    def test_scalar_sgd_step(self, P):
+        # test_factorization.py:197-207
+        r = P.SparseRatings(1, 1, np.array([0]), np.array([0]), np.array([4.0]))
+        p = P.ModelParams(mu=0.0, b=np.zeros(1), b_hat=np.zeros(1), U=np.array([[1.0]]),
+                          V=np.array([[2.0]]), W=np.zeros((1, 0)), C=np.zeros((1, 0)))
+        e = P.sgd_update(0, 0, p, rates=(0.0, 0.0, 0.1, 0.1, 0.0, 0.0), regs=(0.0,) * 6, ratings=r)
+        assert e == pytest.approx(2.0)
+        assert p.U[0, 0] == pytest.approx(1.4)
+        assert p.V[0, 0] == pytest.approx(2.2)
+
+    def test_gradient_directions_fd(self, P):
+        # test_factorization.py:214-235 (A1 oracle): analytic step == central FD
+        rng = np.random.default_rng(3)
+        for F, K in [(1, 0), (2, 2), (8, 4)]:
+            M, N = 7, 9
+            mask = rng.random((M, N)) < 0.5
+            rows, cols = np.nonzero(mask)
+            r = P.SparseRatings(M, N, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+            nbr = None
+            if K:
+                ent = np.stack([rng.choice(np.delete(np.arange(N), j), K, replace=False)
+                                for j in range(N)]).astype(np.int32)
+                nbr = P.NeighborTable(N, K, ent)
+            p = P.ModelParams(mu=3.0, b=rng.normal(0, .2, M), b_hat=rng.normal(0, .2, N),
+                              U=rng.uniform(0, .3, (M, F)), V=rng.uniform(0, .3, (N, F)),
+                              W=rng.normal(0, .1, (N, K)), C=rng.normal(0, .1, (N, K)), neighbors=nbr)
+            k = rng.integers(0, r.nnz)
+            i, j = int(r.entry_rows[k]), int(r.entry_cols[k])
+            q = p.copy()
+            P.sgd_update(i, j, q, rates=(1.0,) * 6, regs=(0.0,) * 6, ratings=r)
+            rv = r.rating(i, j)
+
+            def fd(mut, h=1e-5):
+                def sq(dl):
+                    t = p.copy()
+                    mut(t, dl)
+                    return (rv - P.predict(i, j, t, r)) ** 2
+                return -0.5 * (sq(h) - sq(-h)) / (2 * h)
+
+            assert q.b[i] - p.b[i] == pytest.approx(fd(lambda t, d: t.b.__setitem__(i, t.b[i] + d)),
+                                                    rel=1e-4, abs=1e-9)
+            for f in range(F):
+                assert q.U[i, f] - p.U[i, f] == pytest.approx(
+                    fd(lambda t, d, f=f: t.U.__setitem__((i, f), t.U[i, f] + d)), rel=1e-4, abs=1e-9)
+            for kk in range(K):
+                assert q.W[j, kk] - p.W[j, kk] == pytest.approx(
+                    fd(lambda t, d, kk=kk: t.W.__setitem__((j, kk), t.W[j, kk] + d)), rel=1e-4, abs=1e-9)
+                assert q.C[j, kk] - p.C[j, kk] == pytest.approx(
+                    fd(lambda t, d, kk=kk: t.C.__setitem__((j, kk), t.C[j, kk] + d)), rel=1e-4, abs=1e-9)
+
+    def test_divergence_raises(self, P):
+        rng = np.random.default_rng(42)
+        mask = rng.random((12, 9)) < 0.5
+        rows, cols = np.nonzero(mask)
+        r = P.SparseRatings(12, 9, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+        ent = np.stack([np.delete(np.arange(9), j)[:2] for j in range(9)]).astype(np.int32)
+        cfg = P.TrainConfig(F=3, K=2, alpha_b=1e12, alpha_b_hat=1e12, alpha_u=1e12, alpha_v=1e12,
+                            alpha_w=1e12, alpha_c=1e12, epochs=3, seed=1)
+        with pytest.raises(P.TrainingDivergedError):
+            P.train_full(r, P.NeighborTable(9, 2, ent), cfg)
+        with pytest.raises(P.TrainingDivergedError):
+            P.parallel_train(r, P.NeighborTable(9, 2, ent), cfg, D=2)
+
+
+# ------------------------------------------------------------------ online ---
+
+class TestOnline:
+    def test_online_small_bit_exact(self, P):
+        z = load_golden("online_small.npz")
+        for s in range(int(z["n_cases"])):
+            pre = f"o{s}_"
+            G, p_, q, e, lseed = (int(x) for x in z[pre + "lsh"])
+            F, K, epochs, seed = (int(x) for x in z[pre + "cfg"])
+            orig = ratings_of(P, z, pre)
+            lc = P.LshConfig(G=G, p=p_, q=q, psi_exponent=e, seed=lseed)
+            cfg = P.TrainConfig(F=F, K=K, epochs=epochs, seed=seed)
+            tbl, state = P.simlsh_topk(orig, lc, K)
+            assert tbl.entries.tobytes() == z[pre + "table"].tobytes()
+            params = P.train_full(orig, tbl, cfg)
+            assert params.U.tobytes() == z[pre + "p0_U"].tobytes()
+            before = params.copy()
+            bM, bN, nr_, nc_ = (int(x) for x in z[pre + "b_shape"])
+            batch = P.IncrementBatch(bM, bN, nr_, nc_, z[pre + "b_rows"], z[pre + "b_cols"],
+                                     z[pre + "b_vals"])
+            pe, se, re_, ne = P.absorb_increment(params, state, orig, batch, cfg)
+            assert se.acc.tobytes() == z[pre + "ext_acc"].tobytes(), s
+            assert ne.entries.tobytes() == z[pre + "ext_entries"].tobytes(), s
+            for n in ("b", "b_hat", "U", "V", "W", "C"):
+                assert getattr(pe, n).tobytes() == z[f"{pre}ext_{n}"].tobytes(), (s, n)
+            assert pe.U[:orig.M].tobytes() == before.U.tobytes()
+            assert pe.V[:orig.N].tobytes() == before.V.tobytes()
+
+    def test_incremental_equals_recompute(self, P):
+        # A7a (test_acceptance.py:201-220) on 40 random increments
+        rng = np.random.default_rng(7)
+        for trial in range(40):
+            M = int(rng.integers(6, 16))
+            N = int(rng.integers(5, 12))
+            mask = rng.random((M, N)) < 0.35
+            rows, cols = np.nonzero(mask)
+            full = P.SparseRatings(M, N, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+            orig, batch, _, _ = P.holdback_variables(full, int(rng.integers(1, 3)),
+                                                     int(rng.integers(1, 3)), seed=trial)
+            cfg = P.LshConfig(G=int(rng.integers(2, 9)), p=int(rng.integers(1, 3)),
+                              q=int(rng.integers(1, 4)), psi_exponent=int(rng.choice([1, 2, 4])),
+                              seed=trial)
+            state = P.compute_hash_state(orig, cfg)
+            inc = P.update_hashes_incremental(state, batch, P.assign_row_hashes(batch.M_hat, cfg))
+            ref = P.compute_hash_state(P.extend_ratings(orig, batch), cfg)
+            assert inc.acc.tobytes() == ref.acc.tobytes(), trial
+            assert inc.sig.tobytes() == ref.sig.tobytes(), trial
+
+    def test_online_c1(self, P, c1):
+        z, tr, _ = c1
+        row_map, col_map = z["online_row_map"], z["online_col_map"]
+        bM, bN, nr_, nc_ = (int(x) for x in z["online_b_shape"])
+        rr, cc = row_map[tr.entry_rows], col_map[tr.entry_cols]
+        keep = (rr < bM) & (cc < bN)
+        orig = P.SparseRatings(bM, bN, rr[keep], cc[keep], tr.entry_values[keep])
+        lc = P.LshConfig(G=8, p=3, q=100, psi_exponent=2, seed=0)
+        cfg = P.TrainConfig(F=32, K=32, epochs=4, seed=0)
+        t0, s0 = P.simlsh_topk(orig, lc, 32)
+        assert sha(s0.acc) == str(z["online_state0_acc_sha"])
+        assert t0.entries.tobytes() == z["online_orig_entries"].tobytes()
+        p0 = P.train_full(orig, t0, cfg)
+        assert sha(p0.U) == str(z["online_p0_U_sha"])
+        batch = P.IncrementBatch(bM, bN, nr_, nc_, z["online_b_rows"], z["online_b_cols"],
+                                 z["online_b_vals"])
+        pe, se, _, ne = P.absorb_increment(p0, s0, orig, batch, cfg)
+        assert sha(se.acc) == str(z["online_ext_acc_sha"])
+        assert ne.entries.tobytes() == z["online_ext_entries"].tobytes()
+        for n in ("b", "b_hat", "U", "V", "W", "C"):
+            assert sha(getattr(pe, n)) == str(z[f"online_ext_{n}_sha"]), n
+
+
+# ----------------------------------------------------------------- Hogwild ---
+
+class TestHogwild:
+    def test_c1_rmse_within_tolerance(self, P, c1):
+        """Hogwild fp32 test RMSE within 0.005 of the exact (== reference) run after
+        the same epochs (BASELINE.json north_star)."""
+        z, tr, te = c1
+        nbr = P.NeighborTable(tr.N, 16, z["lsh_entries16"])
+        cfg = P.TrainConfig(F=32, K=16, epochs=20, seed=0)
+        exact = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
+        hog = P.rmse(P.train_full(tr, nbr, cfg, mode="hogwild"), te, tr)
+        assert abs(hog - exact) <= REF_TOL_RMSE, (hog, exact)
+
+    def test_f128_k32_runs(self, P):
+        from paper_2111_11682_b200.hogwild import HogwildTrainer
+        rng = np.random.default_rng(0)
+        M, N = 3000, 800
+        mask = rng.random((M, N)) < 0.02
+        rows, cols = np.nonzero(mask)
+        r = P.SparseRatings(M, N, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+        tbl, _ = P.simlsh_topk(r, P.LshConfig(), 32)
+        cfg = P.TrainConfig(F=128, K=32, epochs=3, seed=0, alpha_b=0.02, alpha_b_hat=0.02,
+                            alpha_u=0.02, alpha_v=0.02, alpha_w=0.001, alpha_c=0.001,
+                            lambda_b=0.01, lambda_b_hat=0.01, lambda_u=0.01, lambda_v=0.01,
+                            lambda_w=0.05, lambda_c=0.05)
+        tr = HogwildTrainer(r, tbl, cfg)
+        first = None
+        for t in range(cfg.epochs):
+            tr.loss.zero_()
+            tr.epoch(t)
+            l = float(tr.loss.item())
+            first = first or l
+        assert l < first
+        pe = P.train_full(r, tbl, P.TrainConfig(**{**cfg.__dict__, "epochs": 3}))
+        rm_exact = P.rmse(pe, r.triplets(), r)
+        rm_hog = P.rmse(tr.to_params(), r.triplets(), r)
+        assert abs(rm_exact - rm_hog) <= REF_TOL_RMSE, (rm_exact, rm_hog)

@@ -1,0 +1,124 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol,
+the product path refuses to run without a GPU (no CPU fallback), and the
+host-side logic (configs, schedules, file formats) mirrors the reference."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "culsh.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(culsh_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2111_11682_b200 import _native as nat
+    lib = nat.load_library()
+    names = header_functions()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(nat.exported_symbols())
+    assert lib.culsh_version().decode().startswith("culsh")
+
+
+def test_error_reporting_without_launch():
+    """Argument validation happens before any CUDA call (CULSH_EINVAL path)."""
+    import ctypes
+    from paper_2111_11682_b200 import _native as nat
+    lib = nat.load_library()
+    st = lib.culsh_row_hash_table(ctypes.c_uint64(0), 1, 9, 8, 0, 10, None, None)  # p*G = 72
+    assert st == nat.CULSH_EINVAL
+    assert "LSH config" in lib.culsh_last_error().decode()
+    st = lib.culsh_topk(None, 0, 5, 24, 0, 5, 3, ctypes.c_uint64(0), None, None, None)
+    assert st == nat.CULSH_EINVAL
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    import paper_2111_11682_b200 as P
+    from paper_2111_11682_b200._native import NativeUnavailable
+    r = P.SparseRatings(3, 2, np.array([0, 1, 2]), np.array([0, 1, 1]), np.array([1., 2., 3.]))
+    with pytest.raises(NativeUnavailable):
+        P.compute_hash_state(r, P.LshConfig(G=4, p=1, q=2))
+    with pytest.raises(NativeUnavailable):
+        P.train_full(r, None, P.TrainConfig(F=2, K=0, epochs=1))
+
+
+def test_configs_mirror_reference():
+    import paper_2111_11682_b200 as P
+    P.LshConfig().validate()
+    for bad in (dict(G=0), dict(G=32, p=3), dict(psi_exponent=3), dict(seed=-1)):
+        with pytest.raises(ValueError):
+            P.LshConfig(**bad).validate()
+    # test_factorization.py:56-66 / A10
+    assert P.learning_rate(0.04, 0.3, 0) == 0.04
+    assert P.learning_rate(0.04, 0.3, 1) == pytest.approx(0.030769230769230771, rel=1e-12)
+    assert P.learning_rate(0.04, 0.3, 4) == pytest.approx(0.04 / 3.4, rel=1e-12)
+    vals = [P.learning_rate(0.04, 0.3, t) for t in range(1001)]
+    assert all(a > b for a, b in zip(vals, vals[1:]))
+    with pytest.raises(ValueError):
+        P.TrainConfig(alpha_u=0).validate()
+    assert P.TrainConfig(F=16).effective_init_scale == 0.25
+
+
+def test_rotation_schedule():
+    import paper_2111_11682_b200 as P
+    s = P.RotationSchedule(3)
+    assert [s.row_block(d, 1) for d in range(3)] == [1, 2, 0]
+    P.RotationSchedule(4).validate()
+    assert P.RotationSchedule(1).stage_assignments(0) == [(0, 0, 0)]
+
+
+def test_sparse_ratings_and_baselines(orc):
+    import paper_2111_11682_b200 as P
+    rng = np.random.default_rng(42)
+    mask = rng.random((12, 9)) < 0.5
+    rows, cols = np.nonzero(mask)
+    vals = rng.integers(1, 6, size=len(rows)).astype(float)
+    r = P.build_indices(P.Triplets(rows.astype(np.int32), cols.astype(np.int32), vals), M=12, N=9)
+    d, mu = orc.build_csr(12, 9, rows, cols, vals)
+    np.testing.assert_array_equal(r.col_rows, d.col_rows)
+    np.testing.assert_array_equal(r.row_cols, d.row_cols)
+    st = r.baselines()
+    assert st.mu == mu
+    assert st.b.tobytes() == d.base_b.tobytes()
+    with pytest.raises(ValueError):
+        P.build_indices(P.Triplets(np.array([0, 0]), np.array([1, 1]), np.array([1., 2.])))
+
+
+def test_checkpoint_and_hashstate_formats(tmp_path):
+    import paper_2111_11682_b200 as P
+    rng = np.random.default_rng(0)
+    nbr = P.NeighborTable(4, 2, np.array([[1, 2], [0, 2], [0, 1], [0, 1]], np.int32))
+    p = P.ModelParams(3.5, rng.random(5), rng.random(4), rng.random((5, 3)), rng.random((4, 3)),
+                      rng.random((4, 2)), rng.random((4, 2)), nbr)
+    p.save(tmp_path / "m.bin")
+    q = P.ModelParams.load(tmp_path / "m.bin")
+    assert q.mu == p.mu and q.U.tobytes() == p.U.tobytes()
+    np.testing.assert_array_equal(q.neighbors.entries, nbr.entries)
+    acc = rng.normal(size=(4, 3, 2, 5))
+    h = P.HashState(acc=acc, sig=(acc >= 0).astype(np.uint8), config=P.LshConfig(G=5, p=2, q=3))
+    h.save(tmp_path / "h.bin")
+    back = P.HashState.load(tmp_path / "h.bin")
+    assert back.acc.tobytes() == acc.tobytes() and back.config == h.config
+    nbr.write_csv(tmp_path / "n.csv")
+    np.testing.assert_array_equal(P.NeighborTable.read_csv(tmp_path / "n.csv").entries, nbr.entries)
+    nbr.validate()
+    with pytest.raises(ValueError):
+        P.NeighborTable(2, 1, np.array([[0], [0]], np.int32)).validate()
+
+
+def test_increment_batch_validation():
+    import paper_2111_11682_b200 as P
+    t = P.Triplets(np.array([0], np.int32), np.array([1], np.int32), np.array([3.0]))
+    with pytest.raises(ValueError, match="no new variable"):
+        P.make_increment(2, 2, t, new_row_count=1, new_col_count=0)
+    b = P.make_increment(2, 2, P.Triplets(np.array([2, 0]), np.array([0, 3]), np.array([1., 2.])))
+    assert (b.new_row_count, b.new_col_count, b.M_hat, b.N_hat) == (1, 2, 3, 4)
