@@ -399,3 +399,12 @@ def absorb_increment(m: Model, acc, lsh_cfg, orig: Csr, orig_triplets, batch, F,
         if bad:
             raise FloatingPointError(f"diverged at epoch {t}")
     return me, acc_ext, entries, d_ext
+
+
+def stage_pass(d: Csr, m: Model, rates: Rates, col_lo: int, col_hi: int, rb: int,
+               block_ptr: np.ndarray) -> int:
+    """parallel.py:110-128 _stage_pass: one worker's (row block rb) x (columns) block."""
+    nb = block_ptr.shape[1]
+    return lib().orc_stage_pass(ctypes.c_int64(col_lo), ctypes.c_int64(col_hi), rb,
+                                _p(block_ptr), nb, _p(d.col_rows), _p(d.col_vals),
+                                *_model_args(d, m), ctypes.byref(rates))

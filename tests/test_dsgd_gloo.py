@@ -1,0 +1,96 @@
+"""Multi-rank DSGD orchestration (dsgd.py) on CPU: world_size 2 and 3 over gloo.
+The per-stage compute is the oracle's _stage_pass restatement, so the test
+isolates the ring schedule, the U/b ring shift and the final block gather:
+the result must equal the reference's parallel_train(D) bit for bit (golden)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, load_golden
+
+REGS = (0.02, 0.02, 0.02, 0.02, 0.002, 0.002)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    from paper_2111_11682_b200.dsgd import RingPlan, allgather_blocks, run_epoch
+    z = load_golden("sgd_small.npz")
+    pre = f"s{case}_"
+    F, K, epochs, seed = (int(x) for x in z[pre + "cfg"])
+    d, mu = orc.build_csr(int(z[pre + "M"]), int(z[pre + "N"]), z[pre + "rows"], z[pre + "cols"],
+                          z[pre + "vals"])
+    m = orc.init_model(d.M, d.N, F, K, z[pre + "nbr"], mu, d.base_b, d.base_bhat, seed)
+    plan = RingPlan(world, d.M, d.N)
+    _, col_bounds, bp = orc.partition(d, world)
+    assert np.array_equal(col_bounds, plan.col_bounds)
+    U, b = torch.from_numpy(m.U), torch.from_numpy(m.b)
+    for t in range(epochs):
+        rates = orc.make_rates(tuple(a / (1.0 + 0.3 * t ** 1.5)
+                                     for a in (0.035, 0.035, 0.035, 0.035, 0.002, 0.002)), REGS)
+        cs = plan.cols(rank)
+
+        def stage(s, rb):
+            assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb, bp) == 0
+        run_epoch(plan, rank, stage, [U, b])
+    # after D stages per epoch every rank holds row block `rank` again
+    allgather_blocks(U, plan.row_bounds, rank, world)
+    allgather_blocks(b, plan.row_bounds, rank, world)
+    for arr in (m.V, m.W, m.C, m.bhat):
+        allgather_blocks(torch.from_numpy(arr), plan.col_bounds, rank, world)
+    if rank == 0:
+        out_q.put({n: getattr(m, n).tobytes() for n in ("b", "bhat", "U", "V", "W", "C")})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,case", [(2, 0), (3, 0), (2, 1), (3, 3)])
+def test_dsgd_ring_equals_reference_parallel_train(world, case):
+    z = load_golden("sgd_small.npz")
+    if world not in (2, 3):
+        pytest.skip()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pre = f"s{case}_D{world}_"
+    names = {"b": "b", "bhat": "b_hat", "U": "U", "V": "V", "W": "W", "C": "C"}
+    for k, n in names.items():
+        assert res[k] == z[pre + n].tobytes(), (world, case, n)
+
+
+def test_ring_plan_covers_every_block():
+    from paper_2111_11682_b200.dsgd import RingPlan
+    for D in (1, 2, 3, 8):
+        p = RingPlan(D, 1000, 700)
+        seen = set()
+        for s in range(D):
+            rbs = [p.row_block(r, s) for r in range(D)]
+            assert sorted(rbs) == list(range(D))
+            seen |= {(rb, r) for r, rb in enumerate(rbs)}
+            for r in range(D):   # the block rank r trains next is the one its recv peer trained now
+                assert p.row_block(r, s + 1) == p.row_block(p.recv_peer(r), s)
+        assert len(seen) == D * D
