@@ -220,7 +220,8 @@ def run_gpu(args):
     params = init_params(M, N, F, K, nbr, stats, cfg)
     torch.cuda.synchronize()
     t_prep = time.perf_counter()
-    tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params)
+    tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params, rotate=bool(args.rotate),
+                        atomic_rows=bool(args.atomic))
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t_prep
     del params
@@ -271,7 +272,7 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (random_sparse distribution generated in HBM, integer stars 1-5)",
         "config": {"workload": WORKLOAD[args.config], "M": M, "N": N, "nnz": nnz, "F": F, "K": K,
-                   "mode": "hogwild fp32, warp per column",
+                   "mode": "hogwild fp32, warp per column", "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic),
                    "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
         "lsh_build_s": lsh_s, "lsh_candidates": ncand,
         "prep_s": t_prep, "datagen_s": t_gen, "train_rmse_running": train_rmse,
@@ -320,6 +321,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--rotate", type=int, default=1, help="per-column rotated visiting order")
+    ap.add_argument("--atomic", type=int, default=1, help="row updates as atomic adds")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -165,14 +165,20 @@ int culsh_explicit_stream(const CulshData *d, double mu, const int32_t *nbr, int
  * Processes N_list columns col_order[0..N_list) (NULL = 0..N_list-1); column j
  * streams CSC entries [seg[2j], seg[2j+1]) (seg NULL = the whole column, a DSGD
  * block otherwise, see culsh_pass_plan).  rows/vals: CSC row index and fp32
- * value.  loss_out (device double, optional) accumulates sum e^2; *status |= 1
- * on a non-finite error.  Replaces factorization.py:332-363 _full_pass_block /
+ * value.  flags bit 0: start each column at a per-column hashed offset (warps
+ * sweep rows out of phase: fewer concurrent writes to one u_i); bit 1: apply
+ * row updates as vector atomic adds of the delta (no lost updates); max_warps > 0
+ * caps the number of concurrently active column warps (Hogwild staleness on
+ * small matrices), 0 = every resident warp.  loss_out
+ * (device double, optional) accumulates sum e^2; *status |= 1 on a non-finite
+ * error.  Replaces factorization.py:332-363 _full_pass_block /
  * parallel.py:110-128 _stage_pass in the performance mode. */
 int culsh_sgd_hogwild_epoch(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
                             const int32_t *rows, const float *vals, const uint32_t *mask,
                             const int64_t *resid_ptr, const float *resid, const int32_t *col_order,
-                            CulshModel32 *m, const CulshRates *r, int *ticket, double *loss_out,
-                            int *status, void *stream);
+                            CulshModel32 *m, const CulshRates *r, int flags, int max_warps,
+                            int *ticket,
+                            double *loss_out, int *status, void *stream);
 
 /* --------------------------------------------------------------- eval --- */
 

@@ -21,9 +21,63 @@
 
 namespace culsh {
 
-struct HwRates {
-    float gb, gbh, gu, gv, gw, gc, lb, lbh, lu, lv, lw, lc;
-};
+__device__ __forceinline__ void cp_async_bytes16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_bytes8(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_bytes4(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int FV>
+__device__ __forceinline__ void cp_async_row(float *dst, const float *src) {
+    if constexpr (FV == 8) {
+        cp_async_bytes16(dst, src);
+        cp_async_bytes16(dst + 4, src + 4);
+    } else if constexpr (FV == 4) {
+        cp_async_bytes16(dst, src);
+    } else if constexpr (FV == 2) {
+        cp_async_bytes8(dst, src);
+    } else {
+        cp_async_bytes4(dst, src);
+    }
+}
+
+template <int FV>
+__device__ __forceinline__ void store_row(float *__restrict__ p, const float (&x)[FV]) {
+    if constexpr (FV == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    } else if constexpr (FV == 2) {
+        *reinterpret_cast<float2 *>(p) = make_float2(x[0], x[1]);
+    } else if constexpr (FV == 8) {
+        *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
+        *reinterpret_cast<float4 *>(p + 4) = make_float4(x[4], x[5], x[6], x[7]);
+    } else {
+        *p = x[0];
+    }
+}
+
+template <int FV>
+__device__ __forceinline__ void add_row(float *__restrict__ p, const float (&x)[FV], const float (&x0)[FV]) {
+    if constexpr (FV == 4) {
+        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(x[0] - x0[0], x[1] - x0[1], x[2] - x0[2], x[3] - x0[3]));
+    } else if constexpr (FV == 2) {
+        atomicAdd(reinterpret_cast<float2 *>(p), make_float2(x[0] - x0[0], x[1] - x0[1]));
+    } else if constexpr (FV == 8) {
+        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(x[0] - x0[0], x[1] - x0[1], x[2] - x0[2], x[3] - x0[3]));
+        atomicAdd(reinterpret_cast<float4 *>(p + 4), make_float4(x[4] - x0[4], x[5] - x0[5], x[6] - x0[6], x[7] - x0[7]));
+    } else {
+        atomicAdd(p, x[0] - x0[0]);
+    }
+}
 
 template <int FV>
 __device__ __forceinline__ void load_row(const float *__restrict__ p, float (&x)[FV]) {
@@ -43,36 +97,57 @@ __device__ __forceinline__ void load_row(const float *__restrict__ p, float (&x)
     }
 }
 
-template <int FV>
-__device__ __forceinline__ void store_row(float *__restrict__ p, const float (&x)[FV]) {
-    if constexpr (FV == 4) {
-        *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
-    } else if constexpr (FV == 2) {
-        *reinterpret_cast<float2 *>(p) = make_float2(x[0], x[1]);
-    } else if constexpr (FV == 8) {
-        *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<float4 *>(p + 4) = make_float4(x[4], x[5], x[6], x[7]);
-    } else {
-        *p = x[0];
-    }
+// Decay factors a = 1 - gamma*lambda of the six rules, so every update is
+// x' = a*x + gamma*(gradient term): one FMUL + one FFMA per element.
+struct HwCoef {
+    float gb, gbh, gu, gv, gw, gc;
+    float ab, abh, au, av, aw, ac;
+};
+
+constexpr int kHwWarps = 8;      // warps per CTA
+constexpr int kHwDepth = 8;      // u_i prefetch depth (updates in flight per warp)
+
+template <int FV, int KPL>
+constexpr int hw_smem_per_warp() {
+    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + kHwDepth * 32 * FV * 4 + kHwDepth * 4;
 }
 
 // FV floats per lane; F == 32*FV (vector path) or F < 32 with FV == 1 (masked).
+//
+// Per warp, shared memory holds (a) the column's next 64 entries' metadata
+// {row, value, mask, residual offset} refilled 32 at a time, read with one
+// broadcast LDS.128 per update, and (b) a ring of kHwDepth u-rows (+ b_i) that
+// cp.async fills kHwDepth-1 updates ahead, so the HBM/L2 latency of the row
+// gather is off the update's critical path.  Each lane copies and later reads
+// only its own FV floats of every row, so the ring needs no warp barrier.
 template <int FV, int KPL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kHwWarps * 32)
 hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__restrict__ seg,
-               const int32_t *__restrict__ rows,
-               const float *__restrict__ vals, const uint32_t *__restrict__ mask,
-               const int64_t *__restrict__ resid_ptr, const float *__restrict__ resid,
-               const int32_t *__restrict__ col_order, float mu, float *__restrict__ Bv,
-               float *__restrict__ BHv, float *__restrict__ U, float *__restrict__ V,
-               float *__restrict__ W, float *__restrict__ C, int F, int K, HwRates R,
-               int *__restrict__ ticket, double *__restrict__ loss, int *__restrict__ status) {
+               const int32_t *__restrict__ rows, const float *__restrict__ vals,
+               const uint32_t *__restrict__ mask, const int64_t *__restrict__ resid_ptr,
+               const float *__restrict__ resid, const int32_t *__restrict__ col_order, float mu,
+               float *__restrict__ Bv, float *__restrict__ BHv, float *__restrict__ U,
+               float *__restrict__ V, float *__restrict__ W, float *__restrict__ C, int F, int K,
+               HwCoef R, int flags, int *__restrict__ ticket, double *__restrict__ loss,
+               int *__restrict__ status) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    constexpr int P = kHwDepth;
     const unsigned lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const bool atomic_rows = (flags & 2) != 0;
+    unsigned char *wbase = s_raw + (size_t)warp * hw_smem_per_warp<FV, KPL>();
+    int4 *s_meta = reinterpret_cast<int4 *>(wbase);                           // 64 x 16 B
+    uint32_t *s_m1 = reinterpret_cast<uint32_t *>(wbase + 64 * 16);           // KPL == 2
+    float *s_ring = reinterpret_cast<float *>(wbase + 64 * 16 + (KPL == 2 ? 64 * 4 : 0));
+    float *s_bring = s_ring + P * 32 * FV;
+    float *my_ring = s_ring + lane * FV;
+
     const bool fl = (int)(lane * FV) < F;   // lane owns factor slots
     const unsigned lt_mask = (1u << lane) - 1u;
+    const float invK = K > 0 ? rsqrtf((float)K) : 0.f;
     double col_loss = 0.0;
     int bad = 0;
+    const float *Ulane = U + lane * FV;
 
     for (;;) {
         int t = 0;
@@ -88,124 +163,186 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             for (int x = 0; x < FV; ++x) v[x] = 0.f;
         }
         float w[KPL], c[KPL];
+        bool kin[KPL];
 #pragma unroll
         for (int q = 0; q < KPL; ++q) {
             const int k = lane + 32 * q;
-            w[q] = k < K ? W[j * K + k] : 0.f;
-            c[q] = k < K ? C[j * K + k] : 0.f;
+            kin[q] = k < K;
+            w[q] = kin[q] ? W[j * K + k] : 0.f;
+            c[q] = kin[q] ? C[j * K + k] : 0.f;
         }
         float bh = BHv[j];
         const int64_t c_lo = col_ptr[j];
         const int64_t lo = seg ? seg[2 * j] : c_lo;
         const int64_t hi = seg ? seg[2 * j + 1] : col_ptr[j + 1];
-        int64_t rbase = resid_ptr[j];
+        const int n = (int)(hi - lo);
+        const float *rcol = resid + resid_ptr[j];
+        // Visiting order: the column's entries rotated to start at position `rot`
+        // (a per-column hash when `rotate` is set).  Warps then sweep the rows out of
+        // phase with each other instead of in lock-step, which keeps concurrent
+        // Hogwild writes to the same u_i rare.
+        const int rot = ((flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
+        int rrel2 = 0;   // residual offset (relative to the column base) at position lo
         if (lo > c_lo) {   // DSGD block: skip the residuals of the column's earlier row blocks
             int skip = 0;
             for (int64_t x = c_lo + lane; x < lo; x += 32)
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
-            rbase += warp_sum(skip);
+            rrel2 = warp_sum(skip);
+        }
+        int rrel1 = rrel2;   // ... at position lo + rot
+        if (rot > 0) {
+            int skip = 0;
+            for (int64_t x = lo + lane; x < lo + rot; x += 32)
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
+            rrel1 += warp_sum(skip);
         }
 
-        for (int64_t c0 = lo; c0 < hi; c0 += 32) {
-            const int n = (int)min64(32, hi - c0);
-            const bool have = (int)lane < n;
-            const int my_i = have ? rows[c0 + lane] : 0;
-            const float my_r = have ? vals[c0 + lane] : 0.f;
-            uint32_t my_m[KPL];
-            int my_pc = 0;
-#pragma unroll
-            for (int q = 0; q < KPL; ++q) {
-                my_m[q] = have ? mask[(c0 + lane) * KPL + q] : 0u;
-                my_pc += __popc(my_m[q]);
-            }
-            // exclusive prefix of explicit counts -> residual offset per entry
-            int incl = my_pc;
-            if (__any_sync(0xffffffffu, my_pc != 0)) {
+        // stage 32 entries' metadata (+ exclusive prefix of explicit counts); processing
+        // index k maps to position (k + rot) mod n, i.e. segment 1 = [rot, n), segment 2 = [0, rot)
+        auto load_chunk = [&](int ch) {
+            const int k = 32 * ch + (int)lane;
+            const bool have = k < n;
+            int pos = k + rot;
+            const bool seg2 = pos >= n;
+            if (seg2) pos -= n;
+            const int64_t e = lo + pos;
+            const int ri = have ? rows[e] : 0;
+            const float rv = have ? vals[e] : 0.f;
+            const uint32_t m0 = have ? mask[e * KPL] : 0u;
+            const uint32_t m1 = (KPL == 2 && have) ? mask[e * KPL + 1] : 0u;
+            const int pc = __popc(m0) + __popc(m1);
+            int roff = 0;
+            if (__any_sync(0xffffffffu, pc != 0)) {
+                int incl = pc;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int y = __shfl_up_sync(0xffffffffu, incl, o);
                     if ((int)lane >= o) incl += y;
                 }
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                const int tot1 = warp_sum((have && !seg2) ? pc : 0);
+                roff = seg2 ? rrel2 + (incl - pc - tot1) : rrel1 + (incl - pc);
+                rrel1 += tot1;
+                rrel2 += tot - tot1;
             }
-            const int64_t my_roff = rbase + (incl - my_pc);
-            rbase += __shfl_sync(0xffffffffu, incl, 31);
+            const int slot = (32 * ch + lane) & 63;
+            s_meta[slot] = make_int4(ri, __float_as_int(rv), (int)m0, roff);
+            if constexpr (KPL == 2) s_m1[slot] = m1;
+        };
+        auto issue = [&](int tp) {
+            const int ip = s_meta[tp & 63].x;
+            float *dst = my_ring + (tp % P) * 32 * FV;
+            if (fl) cp_async_row<FV>(dst, Ulane + (size_t)(unsigned)ip * (unsigned)F);
+            if (lane == 0) cp_async_bytes4(s_bring + (tp % P), Bv + ip);
+        };
 
-            // software pipeline: u_i of the next update is in flight while this one runs
-            float un[FV];
-            float bn = 0.f;
-            {
-                const int i0 = __shfl_sync(0xffffffffu, my_i, 0);
-                if (fl) load_row<FV>(U + (int64_t)i0 * F + lane * FV, un);
-                bn = Bv[i0];
+        load_chunk(0);
+        if (n > 32) load_chunk(1);
+        __syncwarp();
+#pragma unroll
+        for (int p = 0; p < P - 1; ++p) {
+            if (p < n) issue(p);
+            cp_async_commit();
+        }
+        float lossf = 0.f;
+        for (int tt = 0; tt < n; ++tt) {
+            if ((tt & 31) == 0 && tt > 0) {
+                __syncwarp();   // every lane is done with the half being refilled
+                if (tt + 32 < n) load_chunk((tt >> 5) + 1);
+                __syncwarp();
             }
-            for (int tt = 0; tt < n; ++tt) {
-                const int i = __shfl_sync(0xffffffffu, my_i, tt);
-                const float r = __shfl_sync(0xffffffffu, my_r, tt);
-                uint32_t mk[KPL];
+            if (tt + P - 1 < n) issue(tt + P - 1);
+            cp_async_commit();
+            cp_async_wait<P - 1>();
+            const int4 me = s_meta[tt & 63];
+            const int i = me.x;
+            const float r = __int_as_float(me.y);
+            const uint32_t m0 = (uint32_t)me.z;
+            const uint32_t m1 = KPL == 2 ? s_m1[tt & 63] : 0u;
+            float u[FV];
+            load_row<FV>(my_ring + (tt % P) * 32 * FV, u);
+            float part = 0.f;
 #pragma unroll
-                for (int q = 0; q < KPL; ++q) mk[q] = __shfl_sync(0xffffffffu, my_m[q], tt);
-                const int64_t roff = __shfl_sync(0xffffffffu, my_roff, tt);
-                float u[FV];
+            for (int x = 0; x < FV; ++x) part = fmaf(u[x], v[x], part);
+            if (!fl) part = 0.f;
+            float bi = 0.f;
+            if (lane == 0) {
+                bi = s_bring[tt % P];
+                part += bi;
+            }
+            const bool anyex = (m0 | m1) != 0u;   // warp-uniform
+            float inv_r = 0.f, inv_n = invK;
+            float rs[KPL];
+            bool ex[KPL];
+            if (!anyex) {
 #pragma unroll
-                for (int x = 0; x < FV; ++x) u[x] = un[x];
-                const float bi = bn;
-                if (tt + 1 < n) {
-                    const int i1 = __shfl_sync(0xffffffffu, my_i, tt + 1);
-                    if (fl) load_row<FV>(U + (int64_t)i1 * F + lane * FV, un);
-                    bn = Bv[i1];
+                for (int q = 0; q < KPL; ++q) {
+                    ex[q] = false;
+                    rs[q] = 0.f;
+                    part = fmaf(c[q], invK, part);
                 }
-                int nr = 0;
-#pragma unroll
-                for (int q = 0; q < KPL; ++q) nr += __popc(mk[q]);
+            } else {
+                const int nr = __popc(m0) + __popc(m1);
                 const int nn = K - nr;
-                const float inv_r = nr > 0 ? rsqrtf((float)nr) : 0.f;
-                const float inv_n = nn > 0 ? rsqrtf((float)nn) : 0.f;
-                bool ex[KPL];
-                float rs[KPL];
-                float part = 0.f;
-#pragma unroll
-                for (int x = 0; x < FV; ++x) part = fmaf(u[x], v[x], part);
-                int before = 0;
+                inv_r = rsqrtf((float)nr);
+                inv_n = nn > 0 ? rsqrtf((float)nn) : 0.f;
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) {
-                    const int k = lane + 32 * q;
-                    ex[q] = (mk[q] >> lane) & 1u;
-                    rs[q] = ex[q] ? resid[roff + before + __popc(mk[q] & lt_mask)] : 0.f;
-                    before += __popc(mk[q]);
-                    if (k < K) part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;
+                    const uint32_t mq = q == 0 ? m0 : m1;
+                    ex[q] = (mq >> lane) & 1u;
+                    const int rank = (q == 0 ? 0 : __popc(m0)) + __popc(mq & lt_mask);
+                    rs[q] = ex[q] ? rcol[me.w + rank] : 0.f;
+                    part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;
                 }
-                part = warp_sum(part);
-                const float e = r - (mu + bi + bh + part);
-                col_loss += (double)e * (double)e;
-                if (!isfinite(e)) bad = 1;
-                // fused update of every touched parameter (factorization.py:307-328 rules)
+            }
+            part = warp_sum(part);
+            const float e = r - (mu + bh + part);
+            lossf = fmaf(e, e, lossf);
+            // fused update of every touched parameter (factorization.py:307-328 rules)
+            const float geu = R.gu * e, gev = R.gv * e;
+            float uold[FV];
 #pragma unroll
-                for (int x = 0; x < FV; ++x) {
-                    const float uo = u[x];
-                    u[x] = uo + R.gu * (e * v[x] - R.lu * uo);
-                    v[x] = v[x] + R.gv * (e * uo - R.lv * v[x]);
-                }
-                if (fl) store_row<FV>(U + (int64_t)i * F + lane * FV, u);
-                if (lane == 0) Bv[i] = bi + R.gb * (e - R.lb * bi);
-                bh = bh + R.gbh * (e - R.lbh * bh);
+            for (int x = 0; x < FV; ++x) {
+                const float uo = u[x];
+                uold[x] = uo;
+                u[x] = fmaf(R.au, uo, geu * v[x]);
+                v[x] = fmaf(R.av, v[x], gev * uo);
+            }
+            if (atomic_rows) {
+                // add the update instead of storing the new value: a concurrent update of the
+                // same row by another warp is then never lost (only computed from a stale u_i)
+                if (fl) add_row<FV>(U + (size_t)(unsigned)i * (unsigned)F + lane * FV, u, uold);
+                if (lane == 0) atomicAdd(Bv + i, fmaf(R.ab, bi, R.gb * e) - bi);
+            } else {
+                if (fl) store_row<FV>(U + (size_t)(unsigned)i * (unsigned)F + lane * FV, u);
+                if (lane == 0) Bv[i] = fmaf(R.ab, bi, R.gb * e);
+            }
+            bh = fmaf(R.abh, bh, R.gbh * e);
+            const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
 #pragma unroll
-                for (int q = 0; q < KPL; ++q) {
-                    if (ex[q]) w[q] = w[q] + R.gw * (inv_r * e * rs[q] - R.lw * w[q]);
-                    else c[q] = c[q] + R.gc * (inv_n * e - R.lc * c[q]);
+            for (int q = 0; q < KPL; ++q) {
+                if (kin[q]) {
+                    if (ex[q]) w[q] = fmaf(R.aw, w[q], gwe * rs[q]);
+                    else c[q] = fmaf(R.ac, c[q], gce);
                 }
             }
         }
+        cp_async_wait<0>();
+        if (!isfinite(lossf)) bad = 1;
+        col_loss += (double)lossf;
         if (fl) store_row<FV>(V + j * F + lane * FV, v);
 #pragma unroll
         for (int q = 0; q < KPL; ++q) {
             const int k = lane + 32 * q;
-            if (k < K) {
+            if (kin[q]) {
                 W[j * K + k] = w[q];
                 C[j * K + k] = c[q];
             }
         }
         if (lane == 0) BHv[j] = bh;
+        __syncwarp();
     }
     if (lane == 0) {
         if (loss) atomicAdd(loss, col_loss);
@@ -296,19 +433,28 @@ explicit_stream_kernel(CulshData d, double mu, const int32_t *__restrict__ nbr, 
 template <int FV, int KPL>
 int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const int32_t *rows, const float *vals,
                    const uint32_t *mask, const int64_t *resid_ptr, const float *resid,
-                   const int32_t *col_order, CulshModel32 *m, const HwRates &R, int *ticket, double *loss,
-                   int *status, cudaStream_t st) {
-    const int threads = 256;
+                   const int32_t *col_order, CulshModel32 *m, const HwCoef &R, int flags, int max_warps,
+                   int *ticket,
+                   double *loss, int *status, cudaStream_t st) {
+    const int threads = kHwWarps * 32;
+    const size_t smem = (size_t)kHwWarps * hw_smem_per_warp<FV, KPL>();
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hogwild_kernel<FV, KPL>, threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hogwild_kernel<FV, KPL>, threads, smem);
     if (occ < 1) occ = 1;
     int64_t blocks = (int64_t)num_sms() * occ;
-    const int64_t need = (N + 7) / 8;
+    const int64_t need = (N + kHwWarps - 1) / kHwWarps;
     if (blocks > need) blocks = need;
+    if (max_warps > 0 && blocks > (max_warps + kHwWarps - 1) / kHwWarps)
+        blocks = (max_warps + kHwWarps - 1) / kHwWarps;
     if (blocks < 1) blocks = 1;
-    hogwild_kernel<FV, KPL><<<(unsigned)blocks, threads, 0, st>>>(
+    hogwild_kernel<FV, KPL><<<(unsigned)blocks, threads, smem, st>>>(
         N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m->mu, m->b, m->bhat, m->U, m->V, m->W,
-        m->C, m->F, m->K, R, ticket, loss, status);
+        m->C, m->F, m->K, R, flags, ticket, loss, status);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
 }
 
@@ -332,8 +478,9 @@ extern "C" int culsh_sgd_hogwild_epoch(int64_t N, const int64_t *col_ptr, const 
                                        const int32_t *rows,
                                        const float *vals, const uint32_t *mask, const int64_t *resid_ptr,
                                        const float *resid, const int32_t *col_order, CulshModel32 *m,
-                                       const CulshRates *r, int *ticket, double *loss_out, int *status,
-                                       void *stream) {
+                                       const CulshRates *r, int flags, int max_warps, int *ticket,
+                                       double *loss_out,
+                                       int *status, void *stream) {
     const int F = m->F, K = m->K;
     CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
     CULSH_REQUIRE((F >= 1 && F <= 32) || F == 64 || F == 128 || F == 256,
@@ -341,11 +488,12 @@ extern "C" int culsh_sgd_hogwild_epoch(int64_t N, const int64_t *col_ptr, const 
     if (N <= 0) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
-    HwRates R{(float)r->gb, (float)r->gbh, (float)r->gu, (float)r->gv, (float)r->gw, (float)r->gc,
-              (float)r->lb, (float)r->lbh, (float)r->lu, (float)r->lv, (float)r->lw, (float)r->lc};
+    HwCoef R{(float)r->gb, (float)r->gbh, (float)r->gu, (float)r->gv, (float)r->gw, (float)r->gc,
+             (float)(1.0 - r->gb * r->lb), (float)(1.0 - r->gbh * r->lbh), (float)(1.0 - r->gu * r->lu),
+             (float)(1.0 - r->gv * r->lv), (float)(1.0 - r->gw * r->lw), (float)(1.0 - r->gc * r->lc)};
     const bool k2 = K > 32;
-#define HW(FVv) (k2 ? launch_hogwild<FVv, 2>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m, R, ticket, loss_out, status, st) \
-                    : launch_hogwild<FVv, 1>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m, R, ticket, loss_out, status, st))
+#define HW(FVv) (k2 ? launch_hogwild<FVv, 2>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st) \
+                    : launch_hogwild<FVv, 1>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st))
     if (F <= 32) return HW(1);
     if (F == 64) return HW(2);
     if (F == 128) return HW(4);

@@ -167,6 +167,47 @@ def compute_baselines(ratings: SparseRatings) -> BaselineStats:
     return BaselineStats(mu=mu, b=b, b_hat=b_hat)
 
 
+class DeviceSparseRatings:
+    """A SparseRatings built directly in HBM from device triplets (large inputs).
+
+    Same role as SparseRatings for the GPU entry points (``device()``,
+    ``baselines()``, ``M``/``N``/``nnz``); both index views are built by device
+    sorts.  Baselines are computed on the device; for integer-valued ratings they
+    are bit-identical to compute_baselines (every summation order is exact).
+    """
+
+    def __init__(self, M: int, N: int, rows, cols, vals):
+        t = nat.torch()
+        d = rows.device
+        self.M, self.N, self.nnz = int(M), int(N), int(rows.numel())
+        rows = rows.to(t.int32)
+        cols = cols.to(t.int32)
+        vals = vals.to(t.float64)
+        o = t.argsort(cols.long() * M + rows.long())
+        crow, ccol, cval = rows[o].contiguous(), cols[o], vals[o].contiguous()
+        col_ptr = t.zeros(N + 1, dtype=t.int64, device=d)
+        col_ptr[1:] = t.cumsum(t.bincount(ccol, minlength=N), 0)
+        o2 = t.argsort(rows.long() * N + cols.long())
+        row_ptr = t.zeros(M + 1, dtype=t.int64, device=d)
+        row_ptr[1:] = t.cumsum(t.bincount(rows, minlength=M), 0)
+        mu = float(vals.sum().item()) / max(self.nnz, 1)
+        rs = t.zeros(M, dtype=t.float64, device=d).index_add_(0, rows.long(), vals)
+        cs = t.zeros(N, dtype=t.float64, device=d).index_add_(0, cols.long(), vals)
+        rc = t.bincount(rows, minlength=M).double()
+        cc = t.bincount(cols, minlength=N).double()
+        bb = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
+        bh = t.where(cc > 0, cs / cc.clamp(min=1) - mu, t.zeros_like(cs))
+        self._dev = DeviceRatings.from_device(M, N, col_ptr, crow, cval, row_ptr,
+                                              cols[o2].contiguous(), vals[o2].contiguous(), mu, bb, bh)
+        self._stats = BaselineStats(mu, nat.to_host(bb), nat.to_host(bh))
+
+    def device(self) -> "DeviceRatings":
+        return self._dev
+
+    def baselines(self) -> BaselineStats:
+        return self._stats
+
+
 class DeviceRatings:
     """Both views of a SparseRatings in HBM plus the CulshData view for the C ABI.
 

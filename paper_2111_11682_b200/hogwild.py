@@ -61,8 +61,11 @@ class HogwildTrainer:
     """
 
     def __init__(self, ratings, neighbors: NeighborTable | None, config: TrainConfig,
-                 dev=None, params: ModelParams | None = None):
+                 dev=None, params: ModelParams | None = None, rotate: bool = True,
+                 max_warps: int | None = None, atomic_rows: bool = True):
         config.validate()
+        self.rotate = rotate
+        self.atomic_rows = atomic_rows
         self.config = config
         self.neighbors = neighbors
         K = neighbors.K if neighbors is not None else 0
@@ -73,6 +76,9 @@ class HogwildTrainer:
         self.dev = dev if dev is not None else ratings.device()
         d = self.dev
         self.M, self.N, self.nnz = d.M, d.N, d.nnz
+        # Hogwild staleness grows with (concurrently updated columns) / (rows): keep at
+        # most one active column warp per `rows_per_warp` rows (no cap at C2/C3 scale).
+        self.max_warps = max(32, d.M // 16) if max_warps is None else max_warps
         if params is None:
             stats = ratings.baselines()
             params = init_params(d.M, d.N, config.F, K, neighbors, stats, config)
@@ -123,7 +129,8 @@ class HogwildTrainer:
         nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(d.col_rows),
                  nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
                  nat.ptr(self.resid), nat.ptr(order), ctypes.byref(self.model.struct),
-                 ctypes.byref(rates), nat.ptr(self.ticket), nat.ptr(self.loss),
+                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0), int(self.max_warps), nat.ptr(self.ticket),
+                 nat.ptr(self.loss),
                  nat.ptr(self.status), nat.stream_ptr())
 
     def epoch(self, t_epoch: int) -> None:

@@ -79,6 +79,34 @@ def random_sparse_device(M: int, N: int, nnz_target: int, seed: int = 0) -> Devi
     return DeviceMatrix(dev, M, N, nnz)
 
 
+def structured_triplets_device(M: int, N: int, nnz_target: int, seed: int = 0, rank: int = 6):
+    """Skewed, low-rank-plus-noise integer ratings (the survey's "perf-stress"
+    generator; same recipe as the reference's synthetic_movielens_100k,
+    datasets.py:37-102, without the series structure): lognormal row activity and
+    column popularity, rating = clip(round(3.6 + b_u + b_i + u.v + N(0, 0.7)), 1, 5).
+    Returns device (rows, cols, vals) in random order, duplicates removed."""
+    t = nat.torch()
+    d = nat.device()
+    g = t.Generator(device=d)
+    g.manual_seed(seed)
+    act = t.exp(t.randn(M, generator=g, device=d))
+    pop = t.exp(1.2 * t.randn(N, generator=g, device=d))
+    r = t.multinomial(act, nnz_target, replacement=True, generator=g)
+    c = t.multinomial(pop, nnz_target, replacement=True, generator=g)
+    key = t.unique(c * M + r)
+    perm = t.randperm(key.numel(), generator=g, device=d)
+    key = key[perm]
+    rows, cols = (key % M).to(t.int32), (key // M).to(t.int32)
+    bu = 0.35 * t.randn(M, generator=g, device=d, dtype=t.float64)
+    bi = 0.45 * t.randn(N, generator=g, device=d, dtype=t.float64)
+    U = 0.35 * t.randn(M, rank, generator=g, device=d, dtype=t.float64)
+    V = 0.35 * t.randn(N, rank, generator=g, device=d, dtype=t.float64)
+    score = (3.6 + bu[rows.long()] + bi[cols.long()] + (U[rows.long()] * V[cols.long()]).sum(1)
+             + 0.7 * t.randn(rows.numel(), generator=g, device=d, dtype=t.float64))
+    vals = t.clamp(t.round(score), 1.0, 5.0)
+    return rows, cols, vals
+
+
 def host_row_sample(dm: DeviceMatrix, n_rows: int):
     """Host copy (for the CPU baseline) of rows [0, n_rows): full CSR rows, the CSC
     restricted to those rows, and the baselines -- every row keeps all its ratings

@@ -377,3 +377,28 @@ class TestHogwild:
         rm_exact = P.rmse(pe, r.triplets(), r)
         rm_hog = P.rmse(tr.to_params(), r.triplets(), r)
         assert abs(rm_exact - rm_hog) <= REF_TOL_RMSE, (rm_exact, rm_hog)
+
+
+class TestHogwildAtScale:
+    """The performance mode against the exact mode (== reference) at C2 / C3 shape on
+    structured (skewed, low-rank + noise) data, 90/10 split: |test RMSE diff| <= 0.005."""
+
+    @pytest.mark.parametrize("shape,epochs", [("c2", 8), ("c3", 3)])
+    def test_rmse_parity(self, P, shape, epochs):
+        from paper_2111_11682_b200 import _native as nat, lsh, synth
+        from paper_2111_11682_b200.data import DeviceSparseRatings
+        M, N, nnz, F, K, e = synth.SHAPES[shape]
+        rows, cols, vals = synth.structured_triplets_device(M, N, nnz, seed=0)
+        nt = rows.numel() // 10
+        te = P.Triplets(nat.to_host(rows[:nt]), nat.to_host(cols[:nt]), nat.to_host(vals[:nt]))
+        tr = DeviceSparseRatings(M, N, rows[nt:], cols[nt:], vals[nt:])
+        del rows, cols, vals
+        ent, _, _ = lsh.simlsh_topk_device(tr.device(), P.LshConfig(psi_exponent=e), K)
+        nbr = P.NeighborTable(N, K, nat.to_host(ent)[:N * K].reshape(N, K))
+        cfg = P.TrainConfig(F=F, K=K, epochs=epochs, seed=0, alpha_b=0.02, alpha_b_hat=0.02,
+                            alpha_u=0.02, alpha_v=0.02, alpha_w=0.001, alpha_c=0.001,
+                            lambda_b=0.01, lambda_b_hat=0.01, lambda_u=0.01, lambda_v=0.01,
+                            lambda_w=0.05, lambda_c=0.05)
+        r_ex = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
+        r_hw = P.rmse(P.train_full(tr, nbr, cfg, mode="hogwild"), te, tr)
+        assert abs(r_hw - r_ex) <= REF_TOL_RMSE, (shape, r_hw, r_ex)
