@@ -74,6 +74,25 @@ int culsh_hash_accumulate(const int64_t *col_ptr, const int32_t *col_rows, const
                           const uint8_t *table, int q, int p, int G, int e, int into, int int_path,
                           double *acc, uint8_t *sig, uint64_t *keys, int64_t keys_ld, void *stream);
 
+/* Exact-integer bit-counting path for few-valued ratings (e.g. 1..5 stars).
+ * culsh_value_set: per-block sets of distinct values of vals (out n_blocks x 17
+ *   doubles: [count or -1 on overflow, v0..v15]); the caller merges them.
+ * culsh_class_partition: per column, the row indices grouped by value class
+ *   (class c = index of the value in class_vals[0..NC)); class_off (N, NC+1)
+ *   offsets relative to col_ptr[j].
+ * culsh_hash_count: acc/sig/keys for columns [col_begin, col_begin+n_cols) from
+ *   Harley-Seal bit counts: acc = sum_c class_psi[c] * (2*count - n_c), exact, so
+ *   bit-identical to lsh.py:161-183 whenever culsh_psi_int_check passes.
+ *   Needs q*p*ceil(G/8) % 4 == 0 and <= 512. */
+int culsh_value_set(const double *vals, int64_t n, double *out, int n_blocks, void *stream);
+int culsh_class_partition(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                          int64_t N, const double *class_vals, int NC, int32_t *rows_by_class,
+                          int32_t *class_off, void *stream);
+int culsh_hash_count(const int64_t *col_ptr, const int32_t *rows_by_class, const int32_t *class_off,
+                     int NC, const int *class_psi, int64_t col_begin, int64_t n_cols,
+                     const uint8_t *table, int q, int p, int G, double *acc, uint8_t *sig,
+                     uint64_t *keys, int64_t keys_ld, void *stream);
+
 /* Buckets + frequency top-K with seeded supplement for target columns
  * [j_base, j_base+n_cols) of an N_total-column key matrix keys (q, N_total).
  * entries (n_cols, K) i32.  *n_candidates_out (host) = total bucket-mate count.

@@ -186,9 +186,288 @@ __global__ void psi_int_check_kernel(const int64_t *__restrict__ col_ptr,
     if (lane_id() == 0 && (nonint || s >= 2147483647.0)) atomicOr(bad, 1);
 }
 
+// ---------------------------------------------------------------------------
+// Exact-integer fast path by bit counting (Harley-Seal carry-save adders).
+//
+// When the ratings take a few distinct values v (e.g. 1..5 stars) every psi is
+// an integer, and acc[j,g,m,t] = sum_v psi(v) * (2 * n_v[t] - N_v) where n_v[t]
+// counts the column's class-v ratings whose row hash has bit t set and N_v is the
+// class size -- exact integer arithmetic, so the fp64 result equals the
+// reference's ordered sum bit for bit.  Counting is done bit-sliced: a thread
+// owns 32 hash bits (4 consecutive byte slices of the row record), loads one
+// 32-bit word per rating and feeds 16 words at a time through a Harley-Seal CSA
+// tree (15 x 2 LOP3 ops) into a bit-sliced vertical counter -- ~3 ops per 32 bits
+// per rating instead of ~3 ops per bit.  Ratings are pre-partitioned by value
+// class per column (class_partition_kernel) so each class streams contiguously.
+
+constexpr int kHsDepth = 14;         // vertical counter bits: 16*(2^14-1) ratings per flush
+constexpr int kHsMaxClasses = 16;
+constexpr int kHsChunk = 1024;
+
+// Per column: entries grouped by value class (order inside a class is irrelevant to
+// integer counts).  One warp per column, two passes over the column.
+__global__ void class_partition_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ col_rows,
+                                       const double *__restrict__ col_vals, int64_t N,
+                                       const double *__restrict__ class_vals, int NC,
+                                       int32_t *__restrict__ rows_by_class, int32_t *__restrict__ class_off) {
+    __shared__ int s_cnt[8][kHsMaxClasses];
+    const int w = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const int64_t j = blockIdx.x * 8LL + w;
+    if (j >= N) return;
+    const int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
+    if (lane < kHsMaxClasses) s_cnt[w][lane] = 0;
+    __syncwarp();
+    for (int64_t x = lo + lane; x < hi; x += 32) {
+        const double v = col_vals[x];
+        int c = 0;
+        while (c < NC - 1 && class_vals[c] != v) ++c;
+        atomicAdd(&s_cnt[w][c], 1);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int run = 0;
+        for (int c = 0; c < NC; ++c) {
+            const int n = s_cnt[w][c];
+            class_off[j * (NC + 1) + c] = run;
+            s_cnt[w][c] = run;
+            run += n;
+        }
+        class_off[j * (NC + 1) + NC] = run;
+    }
+    __syncwarp();
+    for (int64_t x = lo + lane; x < hi; x += 32) {
+        const double v = col_vals[x];
+        int c = 0;
+        while (c < NC - 1 && class_vals[c] != v) ++c;
+        const int pos = atomicAdd(&s_cnt[w][c], 1);
+        rows_by_class[lo + pos] = col_rows[x];
+    }
+}
+
+// Distinct rating values (up to kHsMaxClasses): per-block sets in shared memory
+// (warp leaders found with __match_any_sync), merged by a one-block pass.
+// out layout per block: [count or -1 on overflow, v0..v15] as doubles.
+__global__ void value_set_kernel(const double *__restrict__ vals, int64_t n, double *__restrict__ out) {
+    __shared__ unsigned long long s_set[kHsMaxClasses];
+    __shared__ int s_n, s_over;
+    if (threadIdx.x == 0) { s_n = 0; s_over = 0; }
+    __syncthreads();
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = base + threadIdx.x;
+        const bool have = x < n;
+        const unsigned long long bits = have ? (unsigned long long)__double_as_longlong(vals[x]) : ~0ULL;
+        const unsigned grp = __match_any_sync(__activemask(), bits);
+        const bool leader = have && ((__ffs(grp) - 1) == (int)lane_id());
+        if (leader && !s_over) {
+            bool found = false;
+            const int cur = atomicAdd(&s_n, 0);
+            for (int k = 0; k < min(cur, kHsMaxClasses); ++k)
+                if (s_set[k] == bits) { found = true; break; }
+            if (!found) {
+                // serialise insertions through the count (rare: only new values get here)
+                for (;;) {
+                    const int m = atomicAdd(&s_n, 0);
+                    bool dup = false;
+                    for (int k = 0; k < min(m, kHsMaxClasses); ++k)
+                        if (atomicAdd(&s_set[k], 0ULL) == bits) { dup = true; break; }
+                    if (dup) break;
+                    if (m >= kHsMaxClasses) { s_over = 1; break; }
+                    if (atomicCAS(&s_n, m, m + 1) == m) {
+                        atomicExch(&s_set[m], bits);
+                        break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (s_over) break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double *o = out + blockIdx.x * (kHsMaxClasses + 1);
+        o[0] = s_over ? -1.0 : (double)s_n;
+        for (int k = 0; k < kHsMaxClasses; ++k) o[1 + k] = k < s_n ? __longlong_as_double((long long)s_set[k]) : 0.0;
+    }
+}
+
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
+    const uint32_t u = a ^ b;
+    h = (a & b) | (u & c);
+    l = u ^ c;
+}
+
+// bit-sliced count of position t: sum_k ((V[k] >> t) & 1) << k
+__device__ __forceinline__ int sliced_count(const uint32_t *V, int D, int t) {
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < kHsDepth; ++k) c |= (int)((V[k] >> t) & 1u) << k;
+    (void)D;
+    return c;
+}
+
+__global__ void __launch_bounds__(128)
+hash_count_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows_by_class,
+                  const int32_t *__restrict__ class_off, int NC, const int *__restrict__ class_psi,
+                  int64_t col_begin, const uint32_t *__restrict__ table32, int W4, int qp, int p, int G,
+                  int ns, double *__restrict__ acc, uint8_t *__restrict__ sig,
+                  uint64_t *__restrict__ keys, int64_t keys_ld) {
+    __shared__ int32_t s_rows[kHsChunk];
+    extern __shared__ uint8_t s_sigbyte[];
+    const int64_t j = col_begin + blockIdx.x;
+    const int lw = threadIdx.x;              // word lane: slices 4*lw .. 4*lw+3
+    const bool active = lw < W4;
+    const int64_t lo = col_ptr[j];
+    const int32_t *coff = class_off + j * (NC + 1);
+
+    int a32[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) a32[t] = 0;
+    for (int c = 0; c < NC; ++c) {
+        const int c_lo = coff[c], c_hi = coff[c + 1];
+        if (c_hi <= c_lo) continue;          // uniform across the CTA
+        const int psi = class_psi[c];
+        uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
+        uint32_t V[kHsDepth];
+#pragma unroll
+        for (int k = 0; k < kHsDepth; ++k) V[k] = 0;
+        int groups = 0;
+        int n_class = c_hi - c_lo;
+        auto flush = [&](int n_done) {
+            // class-v contribution psi * (2 * count - n_done), count from the sliced state
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const int cnt = 16 * sliced_count(V, kHsDepth, t) + 8 * (int)((eights >> t) & 1u) +
+                                4 * (int)((fours >> t) & 1u) + 2 * (int)((twos >> t) & 1u) +
+                                (int)((ones >> t) & 1u);
+                a32[t] += psi * (2 * cnt - n_done);
+            }
+            ones = twos = fours = eights = 0;
+#pragma unroll
+            for (int k = 0; k < kHsDepth; ++k) V[k] = 0;
+        };
+        int done_since_flush = 0;
+        for (int c0 = c_lo; c0 < c_hi; c0 += kHsChunk) {
+            const int n = min(kHsChunk, c_hi - c0);
+            __syncthreads();
+            for (int x = threadIdx.x; x < n; x += blockDim.x) s_rows[x] = rows_by_class[lo + c0 + x];
+            __syncthreads();
+            if (active) {
+                for (int g0 = 0; g0 < n; g0 += 16) {
+                    uint32_t w[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        w[q] = (g0 + q < n) ? __ldg(table32 + (int64_t)s_rows[g0 + q] * W4 + lw) : 0u;
+                    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+                    csa(twosA, ones, ones, w[0], w[1]);
+                    csa(twosB, ones, ones, w[2], w[3]);
+                    csa(foursA, twos, twos, twosA, twosB);
+                    csa(twosA, ones, ones, w[4], w[5]);
+                    csa(twosB, ones, ones, w[6], w[7]);
+                    csa(foursB, twos, twos, twosA, twosB);
+                    csa(eightsA, fours, fours, foursA, foursB);
+                    csa(twosA, ones, ones, w[8], w[9]);
+                    csa(twosB, ones, ones, w[10], w[11]);
+                    csa(foursA, twos, twos, twosA, twosB);
+                    csa(twosA, ones, ones, w[12], w[13]);
+                    csa(twosB, ones, ones, w[14], w[15]);
+                    csa(foursB, twos, twos, twosA, twosB);
+                    csa(eightsB, fours, fours, foursA, foursB);
+                    csa(sixteens, eights, eights, eightsA, eightsB);
+                    uint32_t carry = sixteens;
+#pragma unroll
+                    for (int k = 0; k < kHsDepth; ++k) {
+                        const uint32_t t2 = V[k] & carry;
+                        V[k] ^= carry;
+                        carry = t2;
+                    }
+                    ++groups;
+                    const int ng = min(16, n - g0);
+                    done_since_flush += ng;
+                    if (groups == (1 << kHsDepth) - 1) {   // counter full: fold into a32
+                        flush(done_since_flush);
+                        groups = 0;
+                        done_since_flush = 0;
+                    }
+                }
+            }
+        }
+        if (active) flush(done_since_flush);
+        (void)n_class;
+    }
+    if (active) {
+        const int64_t accW = (int64_t)qp * G;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int s = 4 * lw + b;
+            if (s >= qp * ns) break;
+            const int gm = s / ns, sl = s % ns;
+            const int nbits = min(8, G - 8 * sl);
+            double *a_out = acc + j * accW + (int64_t)gm * G + 8 * sl;
+            uint32_t sb = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const double v = (double)a32[8 * b + t];
+                if (t < nbits) {
+                    a_out[t] = v;
+                    sb |= (v >= 0.0 ? 1u : 0u) << t;
+                }
+            }
+            if (sig) {
+                uint8_t *sg = sig + j * accW + (int64_t)gm * G + 8 * sl;
+                for (int t = 0; t < nbits; ++t) sg[t] = (sb >> t) & 1u;
+            }
+            s_sigbyte[s] = (uint8_t)sb;
+        }
+    }
+    if (keys) {
+        __syncthreads();
+        const int q = qp / p;
+        for (int g = threadIdx.x; g < q; g += blockDim.x) {
+            uint64_t k = 0;
+            for (int m = 0; m < p; ++m)
+                for (int sl = 0; sl < ns; ++sl)
+                    k |= (uint64_t)s_sigbyte[(g * p + m) * ns + sl] << (m * G + 8 * sl);
+            keys[(int64_t)g * keys_ld + j] = k;
+        }
+    }
+}
+
 }  // namespace culsh
 
 using namespace culsh;
+
+extern "C" int culsh_class_partition(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                                     int64_t N, const double *class_vals, int NC, int32_t *rows_by_class,
+                                     int32_t *class_off, void *stream) {
+    CULSH_REQUIRE(NC >= 1 && NC <= kHsMaxClasses, "1..16 value classes supported");
+    if (N <= 0) return CULSH_OK;
+    class_partition_kernel<<<(unsigned)((N + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+        col_ptr, col_rows, col_vals, N, class_vals, NC, rows_by_class, class_off);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_hash_count(const int64_t *col_ptr, const int32_t *rows_by_class, const int32_t *class_off,
+                                int NC, const int *class_psi, int64_t col_begin, int64_t n_cols,
+                                const uint8_t *table, int q, int p, int G, double *acc, uint8_t *sig,
+                                uint64_t *keys, int64_t keys_ld, void *stream) {
+    CULSH_REQUIRE(q >= 1 && p >= 1 && G >= 1 && G <= 64 && p * G <= 64, "bad LSH config");
+    CULSH_REQUIRE(NC >= 1 && NC <= kHsMaxClasses, "1..16 value classes supported");
+    const int ns = (G + 7) / 8;
+    const int W8 = q * p * ns;
+    CULSH_REQUIRE(W8 % 4 == 0, "bit-count path needs q*p*ceil(G/8) divisible by 4");
+    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(table) & 3) == 0, "row-hash table must be 4-byte aligned");
+    if (n_cols <= 0) return CULSH_OK;
+    const int W4 = W8 / 4;
+    int threads = ((W4 + 31) / 32) * 32;
+    CULSH_REQUIRE(threads <= 128, "q*p*ceil(G/8) > 512 bytes: use culsh_hash_accumulate");
+    hash_count_kernel<<<(unsigned)n_cols, threads, (size_t)W8, (cudaStream_t)stream>>>(
+        col_ptr, rows_by_class, class_off, NC, class_psi, col_begin,
+        reinterpret_cast<const uint32_t *>(table), W4, q * p, p, G, ns, acc, sig, keys, keys_ld);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
 
 extern "C" int culsh_row_hash_table(uint64_t seed, int q, int p, int G, int64_t row_lo, int64_t row_hi,
                                     uint8_t *table, void *stream) {
@@ -267,6 +546,15 @@ extern "C" int culsh_hash_accumulate(const int64_t *col_ptr, const int32_t *col_
         hash_accumulate_kernel<double><<<(unsigned)n_cols, threads, smem, st>>>(
             col_ptr, col_rows, col_vals, col_begin, n_cols, col_list, table, q * p, p, G, ns, e, into,
             acc, sig, keys, keys_ld);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+// Per-block distinct-value sets of `vals` (out: n_blocks x 17 doubles, see
+// value_set_kernel); the caller merges them.  n_blocks <= 4096.
+extern "C" int culsh_value_set(const double *vals, int64_t n, double *out, int n_blocks, void *stream) {
+    CULSH_REQUIRE(n_blocks >= 1 && n_blocks <= 4096, "n_blocks must be in [1, 4096]");
+    value_set_kernel<<<n_blocks, 256, 0, (cudaStream_t)stream>>>(vals, n, out);
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }

@@ -240,9 +240,72 @@ def _int_path_ok(dev, col_begin: int, n_cols: int, col_list, e: int) -> bool:
     return int(bad.item()) == 0
 
 
+_MAX_CLASSES = 16
+
+
+def _value_classes(dev):
+    """Distinct rating values of the matrix if there are at most 16 (cached per
+    DeviceRatings; the ratings are immutable), else None."""
+    if hasattr(dev, "_value_classes"):
+        return dev._value_classes
+    nb = 256
+    out = nat.empty((nb * (_MAX_CLASSES + 1),), "float64")
+    nat.call("culsh_value_set", nat.ptr(dev.col_vals), dev.nnz, nat.ptr(out), nb, nat.stream_ptr())
+    o = nat.to_host(out).reshape(nb, _MAX_CLASSES + 1)
+    if (o[:, 0] < 0).any():
+        classes = None
+    else:
+        vals = np.unique(np.concatenate([o[b, 1:1 + int(o[b, 0])] for b in range(nb)]))
+        classes = vals if len(vals) <= _MAX_CLASSES else None
+    dev._value_classes = classes
+    return classes
+
+
+def _class_partition(dev, classes: np.ndarray):
+    """Row indices of every column grouped by value class (cached per DeviceRatings)."""
+    if getattr(dev, "_class_part", None) is None:
+        NC = len(classes)
+        cv = nat.to_dev(np.asarray(classes, np.float64))
+        rows_bc = nat.empty((max(dev.nnz, 1),), "int32")
+        off = nat.empty(((NC + 1) * max(dev.N, 1),), "int32")
+        nat.call("culsh_class_partition", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
+                 nat.ptr(dev.col_vals), dev.N, nat.ptr(cv), NC, nat.ptr(rows_bc), nat.ptr(off),
+                 nat.stream_ptr())
+        dev._class_part = (rows_bc, off)
+    return dev._class_part
+
+
+def _psi_int(v: float, e: int):
+    p = v if e == 1 else (v * v if e == 2 else (v * v) * (v * v))
+    return int(p) if float(p).is_integer() and abs(p) < 2 ** 20 else None
+
+
+def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, keys_ld) -> bool:
+    """Harley-Seal bit-count kernel (exact integers) when the data allow it."""
+    W8 = c.q * c.p * _ns(c.G)
+    if W8 % 4 or W8 > 512 or dev.nnz == 0:
+        return False
+    classes = _value_classes(dev)
+    if classes is None:
+        return False
+    psi = [_psi_int(float(v), c.psi_exponent) for v in classes]
+    if any(x is None for x in psi):
+        return False
+    rows_bc, off = _class_partition(dev, classes)
+    cpsi = nat.to_dev(np.asarray(psi, np.int32))
+    nat.call("culsh_hash_count", nat.ptr(dev.col_ptr), nat.ptr(rows_bc), nat.ptr(off), len(classes),
+             nat.ptr(cpsi), col_begin, n_cols, nat.ptr(table), c.q, c.p, c.G, nat.ptr(acc),
+             nat.ptr(sig), nat.ptr(keys), dev.N if keys_ld is None else keys_ld, nat.stream_ptr())
+    return True
+
+
 def _accumulate(dev, table, c: LshConfig, acc, sig, keys, col_begin: int, n_cols: int,
-                col_list=None, into: bool = False, keys_ld: int | None = None) -> None:
+                col_list=None, into: bool = False, keys_ld: int | None = None,
+                allow_count: bool = True) -> None:
     int_path = (not into) and _int_path_ok(dev, col_begin, n_cols, col_list, c.psi_exponent)
+    if int_path and col_list is None and allow_count:
+        if _count_path(dev, table, c, acc, sig, keys, col_begin, n_cols, keys_ld):
+            return
     nat.call("culsh_hash_accumulate", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
              nat.ptr(dev.col_vals), col_begin, n_cols, nat.ptr(col_list), nat.ptr(table), c.q, c.p,
              c.G, c.psi_exponent, int(into), int(int_path), nat.ptr(acc), nat.ptr(sig),

@@ -402,3 +402,44 @@ class TestHogwildAtScale:
         r_ex = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
         r_hw = P.rmse(P.train_full(tr, nbr, cfg, mode="hogwild"), te, tr)
         assert abs(r_hw - r_ex) <= REF_TOL_RMSE, (shape, r_hw, r_ex)
+
+
+class TestBitCountPath:
+    """The Harley-Seal bit-count kernel (integer ratings, <= 16 distinct values) must
+    equal the ordered-fp64 kernel byte for byte, including the counter-overflow fold."""
+
+    def _fp64(self, P, r, c):
+        from paper_2111_11682_b200 import _native as nat
+        dev = r.device()
+        h = P.assign_row_hashes(r.M, c)
+        acc = nat.zeros((r.N * c.q * c.p * c.G,), "float64")
+        nat.call("culsh_hash_accumulate", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
+                 nat.ptr(dev.col_vals), 0, r.N, None, nat.ptr(h.table()), c.q, c.p, c.G,
+                 c.psi_exponent, 0, 0, nat.ptr(acc), None, None, r.N, nat.stream_ptr())
+        return nat.to_host(acc)
+
+    @pytest.mark.parametrize("G,p,q,e,nvals", [(8, 3, 100, 2, 5), (5, 2, 4, 4, 16), (16, 2, 6, 1, 9),
+                                                (4, 4, 10, 2, 17)])
+    def test_matches_fp64(self, P, G, p, q, e, nvals):
+        from paper_2111_11682_b200 import lsh as L
+        rng = np.random.default_rng(G * 100 + nvals)
+        M, N = 700, 90
+        mask = rng.random((M, N)) < 0.2
+        rows, cols = np.nonzero(mask)
+        vals = rng.integers(1, nvals + 1, len(rows)).astype(float) - (nvals // 3)
+        r = P.SparseRatings(M, N, rows, cols, vals)
+        c = P.LshConfig(G=G, p=p, q=q, psi_exponent=e, seed=3)
+        st = P.compute_hash_state(r, c)
+        uses_count = (nvals <= 16) and ((q * p * ((G + 7) // 8)) % 4 == 0)
+        assert (L._value_classes(r.device()) is not None) == (nvals <= 16)
+        assert st.acc.tobytes() == self._fp64(P, r, c).tobytes(), uses_count
+
+    def test_counter_fold_long_column(self, P):
+        M = 300_000                   # one class > 16*(2^14-1) ratings in column 0
+        rows = np.concatenate([np.arange(M), np.arange(0, M, 7)])
+        cols = np.concatenate([np.zeros(M, np.int64), np.ones(len(rows) - M, np.int64)])
+        vals = np.concatenate([np.full(M, 3.0), np.full(len(rows) - M, 5.0)])
+        vals[::1000] = 1.0
+        r = P.SparseRatings(M, 2, rows, cols, vals)
+        c = P.LshConfig(G=8, p=2, q=2, psi_exponent=2, seed=0)
+        assert P.compute_hash_state(r, c).acc.tobytes() == self._fp64(P, r, c).tobytes()
