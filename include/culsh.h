@@ -83,13 +83,19 @@ int culsh_hash_accumulate(const int64_t *col_ptr, const int32_t *col_rows, const
  * culsh_hash_count: acc/sig/keys for columns [col_begin, col_begin+n_cols) from
  *   Harley-Seal bit counts: acc = sum_c class_psi[c] * (2*count - n_c), exact, so
  *   bit-identical to lsh.py:161-183 whenever culsh_psi_int_check passes.
+ *   The table must hold M+1 rows, row M all zeros (padding).  max_slice_mb > 0
+ *   splits the work into row-range passes whose table slice stays L2-resident;
+ *   acc carries the exact partial sums between passes (class segments are
+ *   row-sorted).  variant 0: row records staged by the bulk-copy engine
+ *   (cp.async.bulk + mbarrier); 1: register double-buffered loads.
  *   Needs q*p*ceil(G/8) % 4 == 0 and <= 512. */
 int culsh_value_set(const double *vals, int64_t n, double *out, int n_blocks, void *stream);
 int culsh_class_partition(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
                           int64_t N, const double *class_vals, int NC, int32_t *rows_by_class,
                           int32_t *class_off, void *stream);
 int culsh_hash_count(const int64_t *col_ptr, const int32_t *rows_by_class, const int32_t *class_off,
-                     int NC, const int *class_psi, int64_t col_begin, int64_t n_cols,
+                     int NC, const int *class_psi, int64_t M, int max_slice_mb, int variant,
+                     int64_t col_begin, int64_t n_cols,
                      const uint8_t *table, int q, int p, int G, double *acc, uint8_t *sig,
                      uint64_t *keys, int64_t keys_ld, void *stream);
 

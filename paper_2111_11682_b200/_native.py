@@ -73,8 +73,8 @@ _SIGS = {
                               _i32, _vp, _vp, _vp, _i64, _vp],
     "culsh_value_set": [_vp, _i64, _vp, _i32, _vp],
     "culsh_class_partition": [_vp, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp],
-    "culsh_hash_count": [_vp, _vp, _vp, _i32, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp,
-                         _i64, _vp],
+    "culsh_hash_count": [_vp, _vp, _vp, _i32, _vp, _i64, _i32, _i32, _i64, _i64, _vp, _i32, _i32, _i32, _vp,
+                         _vp, _vp, _i64, _vp],
     "culsh_topk": [_vp, _i32, _i64, _i32, _i64, _i64, _i32, _u64, _vp, _P(_i64), _vp],
     "culsh_pass_plan": [_vp, _vp, _i64, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32, _i32, _vp,
                         _vp, _vp],

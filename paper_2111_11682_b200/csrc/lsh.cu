@@ -17,6 +17,11 @@
 
 namespace culsh {
 
+// Row record of the packed table: q*p*ceil(G/8) bytes padded to 16 (bulk-copy unit).
+__host__ __device__ __forceinline__ int64_t table_stride(int qp, int ns) {
+    return ((int64_t)qp * ns + 15) & ~15LL;
+}
+
 __global__ void map_keys_kernel(uint64_t seed, int q, int p, uint64_t *keys) {
     int gm = blockIdx.x * blockDim.x + threadIdx.x;
     if (gm < q * p) keys[gm] = map_key(seed, gm / p, gm % p);
@@ -25,7 +30,7 @@ __global__ void map_keys_kernel(uint64_t seed, int q, int p, uint64_t *keys) {
 // table[i][g][m][s] = byte s of the low G bits of splitmix64(key(g,m) ^ i)
 __global__ void row_hash_kernel(const uint64_t *__restrict__ keys, int qp, int G, int ns,
                                 int64_t row_lo, int64_t row_hi, uint8_t *__restrict__ table) {
-    const int64_t rec = (int64_t)qp * ns;
+    const int64_t rec = table_stride(qp, ns);
     const int64_t total = (row_hi - row_lo) * (int64_t)qp;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
          x += (int64_t)gridDim.x * blockDim.x) {
@@ -50,7 +55,8 @@ __global__ void pack_bits_kernel(const uint8_t *__restrict__ bits, int64_t M, in
         const int nb = min(8, G - 8 * s);
         uint8_t v = 0;
         for (int t = 0; t < nb; ++t) v |= (uint8_t)((src[t] != 0) << t);
-        table[x] = v;
+        const int64_t i = igm / qp;
+        table[i * table_stride(qp, ns) + (igm % qp) * ns + s] = v;
     }
 }
 
@@ -61,7 +67,8 @@ __global__ void unpack_bits_kernel(const uint8_t *__restrict__ table, int64_t M,
          x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t igm = x / G;
         const int t = (int)(x % G);
-        bits[x] = (table[igm * ns + t / 8] >> (t % 8)) & 1;
+        const int64_t i = igm / qp;
+        bits[x] = (table[i * table_stride(qp, ns) + (igm % qp) * ns + t / 8] >> (t % 8)) & 1;
     }
 }
 
@@ -85,7 +92,7 @@ hash_accumulate_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__res
 
     const int64_t j = col_list ? (int64_t)col_list[blockIdx.x] : col_begin + blockIdx.x;
     const int W8 = qp * ns;
-    const int64_t rec = (int64_t)W8;
+    const int64_t rec = table_stride(qp, ns);
     const int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
     const int64_t accW = (int64_t)qp * G;
 
@@ -202,7 +209,7 @@ __global__ void psi_int_check_kernel(const int64_t *__restrict__ col_ptr,
 
 constexpr int kHsDepth = 14;         // vertical counter bits: 16*(2^14-1) ratings per flush
 constexpr int kHsMaxClasses = 16;
-constexpr int kHsChunk = 1024;
+constexpr int kHsChunk = 1024;   // multiple of 16
 
 // Per column: entries grouped by value class (order inside a class is irrelevant to
 // integer counts).  One warp per column, two passes over the column.
@@ -236,58 +243,74 @@ __global__ void class_partition_kernel(const int64_t *__restrict__ col_ptr, cons
         class_off[j * (NC + 1) + NC] = run;
     }
     __syncwarp();
-    for (int64_t x = lo + lane; x < hi; x += 32) {
-        const double v = col_vals[x];
-        int c = 0;
-        while (c < NC - 1 && class_vals[c] != v) ++c;
-        const int pos = atomicAdd(&s_cnt[w][c], 1);
-        rows_by_class[lo + pos] = col_rows[x];
+    // stable within each class (rows stay ascending): per 32-entry step, lanes of
+    // class c take consecutive slots in lane order
+    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int64_t x = b0 + lane;
+        const bool have = x < hi;
+        int c = -1;
+        if (have) {
+            const double v = col_vals[x];
+            c = 0;
+            while (c < NC - 1 && class_vals[c] != v) ++c;
+        }
+        for (int cc = 0; cc < NC; ++cc) {
+            const unsigned bal = __ballot_sync(0xffffffffu, c == cc);
+            if (!bal) continue;
+            const int base = s_cnt[w][cc];
+            if (c == cc) rows_by_class[lo + base + __popc(bal & ((1u << lane) - 1u))] = col_rows[x];
+            __syncwarp();
+            if (lane == 0) s_cnt[w][cc] = base + __popc(bal);
+            __syncwarp();
+        }
     }
 }
 
 // Distinct rating values (up to kHsMaxClasses): per-block sets in shared memory
 // (warp leaders found with __match_any_sync), merged by a one-block pass.
 // out layout per block: [count or -1 on overflow, v0..v15] as doubles.
+// Lock-free set of up to kHsMaxClasses distinct values per block: slots start
+// EMPTY (a NaN payload; ratings are finite) and are claimed with atomicCAS, so a
+// value can never be inserted twice.  Each thread loads 4 values up front.
 __global__ void value_set_kernel(const double *__restrict__ vals, int64_t n, double *__restrict__ out) {
+    constexpr unsigned long long EMPTY = 0x7FF4DEADBEEF0001ULL;
     __shared__ unsigned long long s_set[kHsMaxClasses];
-    __shared__ int s_n, s_over;
-    if (threadIdx.x == 0) { s_n = 0; s_over = 0; }
+    __shared__ int s_over;
+    if (threadIdx.x < kHsMaxClasses) s_set[threadIdx.x] = EMPTY;
+    if (threadIdx.x == 0) s_over = 0;
     __syncthreads();
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = base + threadIdx.x;
-        const bool have = x < n;
-        const unsigned long long bits = have ? (unsigned long long)__double_as_longlong(vals[x]) : ~0ULL;
-        const unsigned grp = __match_any_sync(__activemask(), bits);
-        const bool leader = have && ((__ffs(grp) - 1) == (int)lane_id());
-        if (leader && !s_over) {
-            bool found = false;
-            const int cur = atomicAdd(&s_n, 0);
-            for (int k = 0; k < min(cur, kHsMaxClasses); ++k)
-                if (s_set[k] == bits) { found = true; break; }
-            if (!found) {
-                // serialise insertions through the count (rare: only new values get here)
-                for (;;) {
-                    const int m = atomicAdd(&s_n, 0);
-                    bool dup = false;
-                    for (int k = 0; k < min(m, kHsMaxClasses); ++k)
-                        if (atomicAdd(&s_set[k], 0ULL) == bits) { dup = true; break; }
-                    if (dup) break;
-                    if (m >= kHsMaxClasses) { s_over = 1; break; }
-                    if (atomicCAS(&s_n, m, m + 1) == m) {
-                        atomicExch(&s_set[m], bits);
-                        break;
-                    }
-                }
-            }
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += 4 * step) {
+        unsigned long long v4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t x = base + u * step + threadIdx.x;
+            v4[u] = x < n ? (unsigned long long)__double_as_longlong(vals[x]) : EMPTY;
         }
-        __syncthreads();
-        if (s_over) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned long long v = v4[u];
+            if (v == EMPTY) continue;
+            bool found = false;
+            for (int k = 0; k < kHsMaxClasses && !found; ++k)
+                found = ((volatile unsigned long long *)s_set)[k] == v;
+            if (found) continue;
+            int k = 0;
+            for (; k < kHsMaxClasses; ++k) {
+                const unsigned long long old = atomicCAS(&s_set[k], EMPTY, v);
+                if (old == EMPTY || old == v) break;
+            }
+            if (k == kHsMaxClasses) s_over = 1;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double *o = out + blockIdx.x * (kHsMaxClasses + 1);
-        o[0] = s_over ? -1.0 : (double)s_n;
-        for (int k = 0; k < kHsMaxClasses; ++k) o[1 + k] = k < s_n ? __longlong_as_double((long long)s_set[k]) : 0.0;
+        int cnt = 0;
+        for (int k = 0; k < kHsMaxClasses; ++k)
+            if (s_set[k] != EMPTY) o[1 + cnt++] = __longlong_as_double((long long)s_set[k]);
+        for (int k = cnt; k < kHsMaxClasses; ++k) o[1 + k] = 0.0;
+        o[0] = s_over ? -1.0 : (double)cnt;
     }
 }
 
@@ -306,58 +329,159 @@ __device__ __forceinline__ int sliced_count(const uint32_t *V, int D, int t) {
     return c;
 }
 
+// mbarrier / bulk-copy helpers (TMA engine, non-tensor form)
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                 "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+constexpr int kHsRing = 4;        // 16-row groups in flight per CTA (64 row records)
+
+// CTA per column.  Thread 0 gathers whole row records (stride bytes, 16-aligned) of
+// the next groups into a shared-memory ring with the bulk-copy engine
+// (cp.async.bulk + mbarrier transaction counts); every thread then reads its own
+// 32-bit word of each record from shared memory and runs the CSA tree.
+template <bool kTma>
 __global__ void __launch_bounds__(128)
 hash_count_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows_by_class,
                   const int32_t *__restrict__ class_off, int NC, const int *__restrict__ class_psi,
-                  int64_t col_begin, const uint32_t *__restrict__ table32, int W4, int qp, int p, int G,
-                  int ns, double *__restrict__ acc, uint8_t *__restrict__ sig,
-                  uint64_t *__restrict__ keys, int64_t keys_ld) {
+                  int64_t col_begin, const uint8_t *__restrict__ table, int stride, int W4, int qp, int p,
+                  int G, int ns, int pad_row, int row_lo, int row_hi, int first, int last,
+                  double *__restrict__ acc, uint8_t *__restrict__ sig, uint64_t *__restrict__ keys,
+                  int64_t keys_ld) {
     __shared__ int32_t s_rows[kHsChunk];
-    extern __shared__ uint8_t s_sigbyte[];
+    __shared__ __align__(8) uint64_t s_bar[kHsRing];
+    extern __shared__ __align__(16) uint8_t s_dyn[];
+    uint8_t *s_ring = s_dyn;                                        // kHsRing * 16 * stride (TMA)
+    uint8_t *s_sigbyte = s_dyn + (kTma ? (size_t)kHsRing * 16 * stride : 0);   // W4*4 bytes (padded)
+    int *a32 = reinterpret_cast<int *>(s_sigbyte + ((W4 * 4 + 15) & ~15)) + threadIdx.x;
+    const int astr = blockDim.x;
     const int64_t j = col_begin + blockIdx.x;
     const int lw = threadIdx.x;              // word lane: slices 4*lw .. 4*lw+3
     const bool active = lw < W4;
     const int64_t lo = col_ptr[j];
     const int32_t *coff = class_off + j * (NC + 1);
+    const int64_t accW = (int64_t)qp * G;
+    const unsigned gbytes = 16u * (unsigned)stride;
 
-    int a32[32];
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kHsRing; ++k) mbar_init(&s_bar[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // running sums of earlier row-range passes come back from acc (exact integers)
 #pragma unroll
-    for (int t = 0; t < 32; ++t) a32[t] = 0;
+    for (int b = 0; b < 4; ++b) {
+        const int s = 4 * lw + b;
+        const bool ok = active && s < qp * ns;
+        const int gm = ok ? s / ns : 0, sl = ok ? s % ns : 0;
+        const int nbits = ok ? min(8, G - 8 * sl) : 0;
+        const double *a_in = acc + j * accW + (int64_t)gm * G + 8 * sl;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a32[(8 * b + t) * astr] = (!first && t < nbits) ? (int)a_in[t] : 0;
+    }
+    __syncthreads();
+    unsigned issued = 0, consumed = 0;   // group counters (identical in every thread)
+
     for (int c = 0; c < NC; ++c) {
-        const int c_lo = coff[c], c_hi = coff[c + 1];
+        int c_lo = coff[c], c_hi = coff[c + 1];
         if (c_hi <= c_lo) continue;          // uniform across the CTA
+        {   // this pass's rows [row_lo, row_hi): the class segment is row-sorted
+            const int32_t *seg = rows_by_class + lo;
+            int l = c_lo, h = c_hi;
+            while (l < h) { const int m = (l + h) >> 1; if (seg[m] < row_lo) l = m + 1; else h = m; }
+            const int a = l;
+            h = c_hi;
+            while (l < h) { const int m = (l + h) >> 1; if (seg[m] < row_hi) l = m + 1; else h = m; }
+            c_lo = a;
+            c_hi = l;
+        }
+        if (c_hi <= c_lo) continue;
         const int psi = class_psi[c];
         uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
         uint32_t V[kHsDepth];
 #pragma unroll
         for (int k = 0; k < kHsDepth; ++k) V[k] = 0;
-        int groups = 0;
-        int n_class = c_hi - c_lo;
+        int groups = 0, done_since_flush = 0;
         auto flush = [&](int n_done) {
-            // class-v contribution psi * (2 * count - n_done), count from the sliced state
+            // class contribution psi * (2 * count - n_done), count from the sliced state
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
                 const int cnt = 16 * sliced_count(V, kHsDepth, t) + 8 * (int)((eights >> t) & 1u) +
                                 4 * (int)((fours >> t) & 1u) + 2 * (int)((twos >> t) & 1u) +
                                 (int)((ones >> t) & 1u);
-                a32[t] += psi * (2 * cnt - n_done);
+                a32[t * astr] += psi * (2 * cnt - n_done);
             }
             ones = twos = fours = eights = 0;
 #pragma unroll
             for (int k = 0; k < kHsDepth; ++k) V[k] = 0;
         };
-        int done_since_flush = 0;
         for (int c0 = c_lo; c0 < c_hi; c0 += kHsChunk) {
             const int n = min(kHsChunk, c_hi - c0);
+            const int n16 = (n + 15) & ~15;   // tail padded with the all-zero row
+            __syncthreads();                  // previous chunk fully consumed
+            for (int x = threadIdx.x; x < n16; x += blockDim.x)
+                s_rows[x] = x < n ? rows_by_class[lo + c0 + x] : pad_row;
             __syncthreads();
-            for (int x = threadIdx.x; x < n; x += blockDim.x) s_rows[x] = rows_by_class[lo + c0 + x];
-            __syncthreads();
-            if (active) {
-                for (int g0 = 0; g0 < n; g0 += 16) {
-                    uint32_t w[16];
+            const int ng = n16 / 16;
+            // lanes 0..15 of warp 0 each gather one row record of the group
+            auto issue = [&](int g) {
+                const unsigned slot = issued % kHsRing;
+                uint64_t *bar = &s_bar[slot];
+                if (threadIdx.x == 0) mbar_expect_tx(bar, gbytes);
+                __syncwarp();
+                if (threadIdx.x < 16) {
+                    uint8_t *dst = s_ring + (size_t)slot * gbytes + threadIdx.x * stride;
+                    bulk_g2s(dst, table + (int64_t)s_rows[16 * g + threadIdx.x] * stride, stride, bar);
+                }
+            };
+            if (kTma && threadIdx.x < 32) {
+                for (int g = 0; g < min(kHsRing, ng); ++g) { issue(g); ++issued; }
+            } else {
+                issued += min(kHsRing, ng);
+            }
+            const uint32_t *tab32 = reinterpret_cast<const uint32_t *>(table) + lw;
+            const int sw = stride >> 2;
+            uint32_t wn[16];
+            if (!kTma && active) {
 #pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        w[q] = (g0 + q < n) ? __ldg(table32 + (int64_t)s_rows[g0 + q] * W4 + lw) : 0u;
+                for (int q = 0; q < 16; ++q) wn[q] = __ldg(tab32 + (int64_t)s_rows[q] * sw);
+            }
+            for (int g = 0; g < ng; ++g) {
+                const unsigned slot = consumed % kHsRing;
+                if (kTma) mbar_wait(&s_bar[slot], (consumed / kHsRing) & 1u);
+                if (active) {
+                    uint32_t w[16];
+                    if (kTma) {
+                        const uint32_t *src = reinterpret_cast<const uint32_t *>(s_ring + (size_t)slot * gbytes) + lw;
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) w[q] = src[q * sw];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) w[q] = wn[q];
+                        if (g + 1 < ng) {   // next group's loads in flight during this group's CSA tree
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) wn[q] = __ldg(tab32 + (int64_t)s_rows[16 * (g + 1) + q] * sw);
+                        }
+                    }
                     uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
                     csa(twosA, ones, ones, w[0], w[1]);
                     csa(twosB, ones, ones, w[2], w[3]);
@@ -382,21 +506,38 @@ hash_count_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict
                         carry = t2;
                     }
                     ++groups;
-                    const int ng = min(16, n - g0);
-                    done_since_flush += ng;
+                    done_since_flush += min(16, n - 16 * g);
                     if (groups == (1 << kHsDepth) - 1) {   // counter full: fold into a32
                         flush(done_since_flush);
                         groups = 0;
                         done_since_flush = 0;
                     }
                 }
+                ++consumed;
+                if (kTma) {
+                    __syncthreads();               // slot free for the producer
+                    if (g + kHsRing < ng) {
+                        if (threadIdx.x < 32) issue(g + kHsRing);
+                        ++issued;
+                    }
+                }
             }
         }
         if (active) flush(done_since_flush);
-        (void)n_class;
     }
+    if (active && !last) {   // park the partial sums for the next pass
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int s = 4 * lw + b;
+            if (s >= qp * ns) break;
+            const int gm = s / ns, sl = s % ns;
+            const int nbits = min(8, G - 8 * sl);
+            double *a_out = acc + j * accW + (int64_t)gm * G + 8 * sl;
+            for (int t = 0; t < nbits; ++t) a_out[t] = (double)a32[(8 * b + t) * astr];
+        }
+    }
+    if (!last) return;
     if (active) {
-        const int64_t accW = (int64_t)qp * G;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int s = 4 * lw + b;
@@ -407,7 +548,7 @@ hash_count_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict
             uint32_t sb = 0;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
-                const double v = (double)a32[8 * b + t];
+                const double v = (double)a32[(8 * b + t) * astr];
                 if (t < nbits) {
                     a_out[t] = v;
                     sb |= (v >= 0.0 ? 1u : 0u) << t;
@@ -449,23 +590,50 @@ extern "C" int culsh_class_partition(const int64_t *col_ptr, const int32_t *col_
 }
 
 extern "C" int culsh_hash_count(const int64_t *col_ptr, const int32_t *rows_by_class, const int32_t *class_off,
-                                int NC, const int *class_psi, int64_t col_begin, int64_t n_cols,
-                                const uint8_t *table, int q, int p, int G, double *acc, uint8_t *sig,
-                                uint64_t *keys, int64_t keys_ld, void *stream) {
+                                int NC, const int *class_psi, int64_t M, int max_slice_mb, int variant,
+                                int64_t col_begin, int64_t n_cols, const uint8_t *table, int q, int p, int G,
+                                double *acc, uint8_t *sig, uint64_t *keys, int64_t keys_ld, void *stream) {
     CULSH_REQUIRE(q >= 1 && p >= 1 && G >= 1 && G <= 64 && p * G <= 64, "bad LSH config");
     CULSH_REQUIRE(NC >= 1 && NC <= kHsMaxClasses, "1..16 value classes supported");
     const int ns = (G + 7) / 8;
     const int W8 = q * p * ns;
     CULSH_REQUIRE(W8 % 4 == 0, "bit-count path needs q*p*ceil(G/8) divisible by 4");
-    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(table) & 3) == 0, "row-hash table must be 4-byte aligned");
+    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(table) & 15) == 0, "row-hash table must be 16-byte aligned");
     if (n_cols <= 0) return CULSH_OK;
     const int W4 = W8 / 4;
+    const int stride = (int)table_stride(q * p, ns);
     int threads = ((W4 + 31) / 32) * 32;
     CULSH_REQUIRE(threads <= 128, "q*p*ceil(G/8) > 512 bytes: use culsh_hash_accumulate");
-    hash_count_kernel<<<(unsigned)n_cols, threads, (size_t)W8, (cudaStream_t)stream>>>(
-        col_ptr, rows_by_class, class_off, NC, class_psi, col_begin,
-        reinterpret_cast<const uint32_t *>(table), W4, q * p, p, G, ns, acc, sig, keys, keys_ld);
-    CULSH_LAUNCH_CHECK();
+    const size_t smem = (size_t)kHsRing * 16 * stride + (size_t)((W4 * 4 + 15) & ~15) +
+                        sizeof(int) * 32 * threads;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(hash_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(hash_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        attr = true;
+    }
+    const bool use_tma = variant == 0;
+    const size_t smem_k = use_tma ? smem : smem - (size_t)kHsRing * 16 * stride;
+    CULSH_REQUIRE(smem <= 96 * 1024, "row record too large for the staging ring");
+    int passes = 1;
+    if (max_slice_mb > 0) {
+        const int64_t slice_bytes = (int64_t)max_slice_mb << 20;
+        passes = (int)((M * (int64_t)stride + slice_bytes - 1) / slice_bytes);
+        if (passes < 1) passes = 1;
+        if (passes > 64) passes = 64;
+    }
+    for (int ps = 0; ps < passes; ++ps) {
+        const int r0 = (int)((M * ps) / passes), r1 = (int)((M * (ps + 1)) / passes);
+        if (use_tma)
+            hash_count_kernel<true><<<(unsigned)n_cols, threads, smem_k, (cudaStream_t)stream>>>(
+                col_ptr, rows_by_class, class_off, NC, class_psi, col_begin, table, stride, W4, q * p, p, G,
+                ns, (int)M, r0, r1, ps == 0, ps == passes - 1, acc, sig, keys, keys_ld);
+        else
+            hash_count_kernel<false><<<(unsigned)n_cols, threads, smem_k, (cudaStream_t)stream>>>(
+                col_ptr, rows_by_class, class_off, NC, class_psi, col_begin, table, stride, W4, q * p, p, G,
+                ns, (int)M, r0, r1, ps == 0, ps == passes - 1, acc, sig, keys, keys_ld);
+        CULSH_LAUNCH_CHECK();
+    }
     return CULSH_OK;
 }
 

@@ -90,7 +90,7 @@ class RowHashes:
         if self._table is None:
             M, q, p, G = self._shape
             src = nat.to_dev(self._bits.reshape(-1) if self._bits.size else np.zeros(1, np.uint8))
-            t = nat.empty((max(M * q * p * _ns(G), 1),), "uint8")
+            t = _table_alloc(M, q, p, G)
             nat.call("culsh_pack_bits", nat.ptr(src), M, q, p, G, nat.ptr(t), nat.stream_ptr())
             self._table = t
         return self._table
@@ -102,8 +102,17 @@ class RowHashes:
         return _device_row_hashes(M_new, q, p, G, self.seed)
 
 
+def _table_alloc(M: int, q: int, p: int, G: int):
+    """Packed table storage: M rows + one all-zero padding row (read by the
+    bit-count kernel for group tails)."""
+    rec = (q * p * _ns(G) + 15) // 16 * 16   # row record padded to the 16-byte bulk-copy unit
+    t = nat.empty(((M + 1) * rec,), "uint8")
+    t[M * rec:].zero_()
+    return t
+
+
 def _device_row_hashes(M: int, q: int, p: int, G: int, seed: int) -> RowHashes:
-    t = nat.empty((max(M * q * p * _ns(G), 1),), "uint8")
+    t = _table_alloc(M, q, p, G)
     nat.call("culsh_row_hash_table", ctypes.c_uint64(seed), q, p, G, 0, M, nat.ptr(t),
              nat.stream_ptr())
     return RowHashes(None, seed, _table=t, _shape=(M, q, p, G))
@@ -241,6 +250,8 @@ def _int_path_ok(dev, col_begin: int, n_cols: int, col_list, e: int) -> bool:
 
 
 _MAX_CLASSES = 16
+_SLICE_MB = int(__import__("os").environ.get("CULSH_HASH_SLICE_MB", "0"))   # 0 = one pass
+_COUNT_VARIANT = 1   # 0: bulk-copy (TMA engine) staging, 1: register double buffering (faster)
 
 
 def _value_classes(dev):
@@ -248,14 +259,15 @@ def _value_classes(dev):
     DeviceRatings; the ratings are immutable), else None."""
     if hasattr(dev, "_value_classes"):
         return dev._value_classes
-    nb = 256
+    nb = 1184   # 148 SMs x 8: enough loads in flight to stream the values at HBM speed
     out = nat.empty((nb * (_MAX_CLASSES + 1),), "float64")
     nat.call("culsh_value_set", nat.ptr(dev.col_vals), dev.nnz, nat.ptr(out), nb, nat.stream_ptr())
     o = nat.to_host(out).reshape(nb, _MAX_CLASSES + 1)
     if (o[:, 0] < 0).any():
         classes = None
     else:
-        vals = np.unique(np.concatenate([o[b, 1:1 + int(o[b, 0])] for b in range(nb)]))
+        have = np.arange(_MAX_CLASSES)[None, :] < o[:, :1]
+        vals = np.unique(o[:, 1:][have])
         classes = vals if len(vals) <= _MAX_CLASSES else None
     dev._value_classes = classes
     return classes
@@ -294,7 +306,9 @@ def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, key
     rows_bc, off = _class_partition(dev, classes)
     cpsi = nat.to_dev(np.asarray(psi, np.int32))
     nat.call("culsh_hash_count", nat.ptr(dev.col_ptr), nat.ptr(rows_bc), nat.ptr(off), len(classes),
-             nat.ptr(cpsi), col_begin, n_cols, nat.ptr(table), c.q, c.p, c.G, nat.ptr(acc),
+             nat.ptr(cpsi), dev.M, int(_SLICE_MB), int(_COUNT_VARIANT), col_begin, n_cols, nat.ptr(table),
+             c.q, c.p, c.G,
+             nat.ptr(acc),
              nat.ptr(sig), nat.ptr(keys), dev.N if keys_ld is None else keys_ld, nat.stream_ptr())
     return True
 

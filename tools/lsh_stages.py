@@ -53,7 +53,14 @@ _, t_vs = timed(lambda: (clear(), lsh._value_classes(dev)))
 print(f"value classes         {t_vs:8.3f} ms  -> {dev._value_classes}")
 _, t_cp = timed(lambda: (setattr(dev, "_class_part", None), lsh._class_partition(dev, dev._value_classes)))
 print(f"class partition       {t_cp:8.3f} ms")
-_, t_cnt = timed(lambda: lsh._count_path(dev, h.table(), c, acc, sig, keys, 0, N, None))
+for var in (0, 1):
+    for mb in (0, 96, 48):
+        lsh._SLICE_MB = mb
+        lsh._COUNT_VARIANT = var
+        _, t_cnt = timed(lambda: lsh._count_path(dev, h.table(), c, acc, sig, keys, 0, N, None))
+        print(f"hash_count variant={var} slice={mb:3d}MB {t_cnt:8.3f} ms")
+lsh._SLICE_MB = 0
+lsh._COUNT_VARIANT = 1
 print(f"hash_count kernel     {t_cnt:8.3f} ms  ({nnz * W / t_cnt / 1e9:.1f} G signed adds/ms equiv.)")
 _, t_acc = timed(lambda: lsh._accumulate(dev, h.table(), c, acc, sig, keys, 0, N, allow_count=False))
 print(f"int accumulate kernel {t_acc:8.3f} ms (previous path, for comparison)")
