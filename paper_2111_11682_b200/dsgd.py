@@ -61,6 +61,12 @@ class RingPlan:
         return slice(int(self.col_bounds[cb]), int(self.col_bounds[cb + 1]))
 
 
+def _host_staging() -> bool:
+    """Gloo has no CUDA send/recv: stage device tensors through host memory."""
+    import torch.distributed as dist
+    return dist.get_backend() == "gloo"
+
+
 def ring_shift(plan: RingPlan, rank: int, stage: int, tensors, group=None) -> None:
     """After stage `stage`: send the row block just trained to rank-1 and receive the
     next stage's row block from rank+1, in place, for every (M, ...) tensor given."""
@@ -70,13 +76,19 @@ def ring_shift(plan: RingPlan, rank: int, stage: int, tensors, group=None) -> No
     send_rb = plan.row_block(rank, stage)
     recv_rb = plan.row_block(rank, stage + 1)
     dst, src = plan.send_peer(rank), plan.recv_peer(rank)
+    stage_host = _host_staging()
     ops = []
     for t in tensors:
-        ops.append(dist.P2POp(dist.isend, t[plan.rows(send_rb)].contiguous(), dst, group))
+        out = t[plan.rows(send_rb)].contiguous()
+        if stage_host and out.is_cuda:
+            out = out.cpu()
+        ops.append(dist.P2POp(dist.isend, out, dst, group))
     recv_bufs = []
     for t in tensors:
         buf = t[plan.rows(recv_rb)]
-        if not buf.is_contiguous():
+        if stage_host and buf.is_cuda:
+            buf = buf.cpu()
+        elif not buf.is_contiguous():
             buf = buf.contiguous()
         recv_bufs.append(buf)
         ops.append(dist.P2POp(dist.irecv, buf, src, group))
@@ -108,11 +120,13 @@ def allgather_blocks(t, bounds: np.ndarray, rank: int, D: int, group=None):
     send = torch.zeros((mx,) + tail, dtype=t.dtype, device=t.device)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     send[:hi - lo] = t[lo:hi]
+    if _host_staging() and send.is_cuda:
+        send = send.cpu()
     outs = [torch.empty_like(send) for _ in range(D)]
     dist.all_gather(outs, send, group=group)
     for d in range(D):
         a, b = int(bounds[d]), int(bounds[d + 1])
-        t[a:b] = outs[d][:b - a]
+        t[a:b] = outs[d][:b - a].to(t.device)
     return t
 
 
@@ -155,6 +169,16 @@ def simlsh_topk_sharded(dev, config, K: int, rank: int, D: int, group=None):
 
 # --------------------------------------------------------------- the bench ---
 
+def _max_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def bench_main(args, metric, workload, rates):
     """Multi-GPU DSGD benchmark (launched by torchrun, one rank per GPU)."""
     import json
@@ -170,9 +194,17 @@ def bench_main(args, metric, workload, rates):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CULSH_DIST_BACKEND=gloo + CULSH_SHARE_GPU=1 lets a 1-GPU box run the N-rank
+    # orchestration end to end (ranks time-share cuda:0, exchanges staged via host)
+    backend = os.environ.get("CULSH_DIST_BACKEND", "nccl")
+    if os.environ.get("CULSH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     D = world
     M, N, nnz_t, F, K, e = synth.SHAPES[args.config]
     dm = synth.random_sparse_device(M, N, nnz_t, seed=0)   # same seed: identical matrix on every rank
@@ -186,8 +218,7 @@ def bench_main(args, metric, workload, rates):
     ent, _ = simlsh_topk_sharded(dm.dev, lcfg, K, rank, D)
     ev1.record()
     torch.cuda.synchronize()
-    lsh_s = torch.tensor([ev0.elapsed_time(ev1) / 1e3], device="cuda")
-    dist.all_reduce(lsh_s, op=dist.ReduceOp.MAX)
+    lsh_s = _max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
     nbr = NeighborTable(N, K, nat.to_host(ent)[:N * K].reshape(N, K).astype(np.int32))
 
     cfg = TrainConfig(F=F, K=K, epochs=args.warmup + args.steps, seed=0, **rates)
@@ -234,9 +265,7 @@ def bench_main(args, metric, workload, rates):
     t1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    el = torch.tensor([t0.elapsed_time(t1) / 1e3], device="cuda")
-    dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    total = float(el.item())
+    total = _max_over_ranks(t0.elapsed_time(t1) / 1e3)
     ups = nnz * args.steps / total
     if rank == 0:
         line = {"metric": metric, "value": ups, "unit": "updates/s", "n_gpus": D, "steps": args.steps,
@@ -245,7 +274,7 @@ def bench_main(args, metric, workload, rates):
                 "data": "synthetic (random_sparse distribution generated in HBM)",
                 "config": {"workload": workload[args.config], "parallelism": f"dsgd{D}",
                            "exchange": "NCCL send/recv ring shift of u/b row blocks per stage"},
-                "lsh_build_s": float(lsh_s.item()),
+                "lsh_build_s": lsh_s,
                 "gpu_launches": args.steps * D,
                 "e2e": None}
         print(json.dumps(line), flush=True)
