@@ -224,7 +224,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     t_prep = time.perf_counter()
     tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params, rotate=bool(args.rotate),
-                        atomic_rows=bool(args.atomic))
+                        atomic_rows=bool(args.atomic), subwarp=args.kernel == "subwarp")
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t_prep
     del params
@@ -275,14 +275,14 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (random_sparse distribution generated in HBM, integer stars 1-5)",
         "config": {"workload": WORKLOAD[args.config], "M": M, "N": N, "nnz": nnz, "F": F, "K": K,
-                   "mode": "hogwild fp32, warp per column", "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic),
+                   "mode": "hogwild fp32, warp per column", "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic), "kernel": args.kernel,
                    "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
         "lsh_build_s": lsh_s, "lsh_candidates": ncand,
         "prep_s": t_prep, "datagen_s": t_gen, "train_rmse_running": train_rmse,
         "epoch_ms": [p * 1e3 for p in per],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_update": b_upd, "kernel": "hogwild_kernel<4,1>"},
+                     "bytes_per_update": b_upd, "kernel": "hogwild_sg_kernel<16,8,2,1>" if args.kernel == "subwarp" else "hogwild_kernel<4,1>"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,
@@ -324,8 +324,10 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--rotate", type=int, default=1, help="per-column rotated visiting order")
+    ap.add_argument("--rotate", type=int, default=0, help="per-column rotated visiting order")
     ap.add_argument("--atomic", type=int, default=1, help="row updates as atomic adds")
+    ap.add_argument("--kernel", default="warp", choices=["warp", "subwarp"],
+                    help="Hogwild kernel: a warp per column (default) or 16 lanes per column")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -192,7 +192,8 @@ int culsh_explicit_stream(const CulshData *d, double mu, const int32_t *nbr, int
  * block otherwise, see culsh_pass_plan).  rows/vals: CSC row index and fp32
  * value.  flags bit 0: start each column at a per-column hashed offset (warps
  * sweep rows out of phase: fewer concurrent writes to one u_i); bit 1: apply
- * row updates as vector atomic adds of the delta (no lost updates); max_warps > 0
+ * row updates as vector atomic adds of the delta (no lost updates); bit 2: the
+ * sub-warp kernel (16 lanes per column) instead of warp-per-column; max_warps > 0
  * caps the number of concurrently active column warps (Hogwild staleness on
  * small matrices), 0 = every resident warp.  loss_out
  * (device double, optional) accumulates sum e^2; *status |= 1 on a non-finite

@@ -259,24 +259,60 @@ def bench_main(args, metric, workload, rates):
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for s in range(args.steps):
-        run_epoch(plan, rank, stage(args.warmup + s), [U, b])
-    t1.record()
-    torch.cuda.synchronize()
+    from bench import Clocks   # noqa: E402  (repo root is on sys.path under bench.py)
+    clk = Clocks(f"/tmp/culsh_clocks_rank{rank}.csv")
+    with clk:
+        t0.record()
+        for s in range(args.steps):
+            run_epoch(plan, rank, stage(args.warmup + s), [U, b])
+        t1.record()
+        torch.cuda.synchronize()
     dist.barrier()
     total = _max_over_ranks(t0.elapsed_time(t1) / 1e3)
     ups = nnz * args.steps / total
+    b_upd = tr.bytes_per_update()
+
+    # e2e: every step each rank copies ITS column block's rating stream (rows,
+    # values, masks) from pinned host memory, runs the epoch, reads the loss back
+    lo_e, hi_e = int(d.col_ptr[cs.start].item()), int(d.col_ptr[cs.stop].item())
+    host = {"rows": d.col_rows[lo_e:hi_e].cpu().pin_memory(),
+            "vals": tr.vals32[lo_e:hi_e].cpu().pin_memory(),
+            "mask": tr.mask[lo_e * tr.MW:hi_e * tr.MW].cpu().pin_memory()}
+    e_steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    dist.barrier()
+    w0 = time.perf_counter()
+    for s in range(e_steps):
+        d.col_rows[lo_e:hi_e].copy_(host["rows"], non_blocking=True)
+        tr.vals32[lo_e:hi_e].copy_(host["vals"], non_blocking=True)
+        tr.mask[lo_e * tr.MW:hi_e * tr.MW].copy_(host["mask"], non_blocking=True)
+        tr.loss.zero_()
+        run_epoch(plan, rank, stage(args.warmup + args.steps + s), [U, b])
+        float(tr.loss.item())
+    torch.cuda.synchronize()
+    e_dt = _max_over_ranks(time.perf_counter() - w0)
+    h2d = sum(int(v.numel() * v.element_size()) for v in host.values())
+    peak = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]) if os.path.exists(os.path.join(
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6650.0
+    ach = b_upd * nnz / D / (total / args.steps) / 1e9
     if rank == 0:
         line = {"metric": metric, "value": ups, "unit": "updates/s", "n_gpus": D, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
                 "data": "synthetic (random_sparse distribution generated in HBM)",
                 "config": {"workload": workload[args.config], "parallelism": f"dsgd{D}",
-                           "exchange": "NCCL send/recv ring shift of u/b row blocks per stage"},
+                           "exchange": "NCCL send/recv ring shift of u/b row blocks per stage",
+                           "l2": "inputs larger than L2, no flush"},
                 "lsh_build_s": lsh_s,
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                             "frac": ach / peak, "traffic": None,
+                             "note": "per GPU: B_upd x nnz/D per epoch / epoch time (incl. ring shifts)"},
                 "gpu_launches": args.steps * D,
-                "e2e": None}
+                "e2e": {"value": nnz * e_steps / e_dt, "unit": "updates/s",
+                        "h2d_bytes_per_step": h2d * D, "d2h_bytes_per_step": 8 * D,
+                        "api": "per-rank pinned column-block stream -> DSGD epoch -> loss"},
+                "clocks": clk.summary(local)}
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -61,11 +61,12 @@ class HogwildTrainer:
     """
 
     def __init__(self, ratings, neighbors: NeighborTable | None, config: TrainConfig,
-                 dev=None, params: ModelParams | None = None, rotate: bool = True,
-                 max_warps: int | None = None, atomic_rows: bool = True):
+                 dev=None, params: ModelParams | None = None, rotate: bool = False,
+                 max_warps: int | None = None, atomic_rows: bool = True, subwarp: bool = False):
         config.validate()
         self.rotate = rotate
         self.atomic_rows = atomic_rows
+        self.subwarp = subwarp   # 16-lanes-per-column kernel instead of warp per column
         self.config = config
         self.neighbors = neighbors
         K = neighbors.K if neighbors is not None else 0
@@ -129,7 +130,8 @@ class HogwildTrainer:
         nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(d.col_rows),
                  nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
                  nat.ptr(self.resid), nat.ptr(order), ctypes.byref(self.model.struct),
-                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0), int(self.max_warps), nat.ptr(self.ticket),
+                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0),
+                 int(self.max_warps), nat.ptr(self.ticket),
                  nat.ptr(self.loss),
                  nat.ptr(self.status), nat.stream_ptr())
 
