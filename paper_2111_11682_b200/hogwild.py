@@ -161,6 +161,55 @@ class HogwildTrainer:
         h2d = sum(int(v.numel() * v.element_size()) for v in host.values())
         return loss, h2d, 8 + 4
 
+    def train_from_host(self, host: dict, t_start: int, n_epochs: int):
+        """Epochs whose rating stream comes from pinned host memory every epoch, with
+        the H2D copy of epoch e+1 (copy stream, double buffer) overlapping the
+        kernel of epoch e, and each epoch's loss copied back (D2H) as it finishes.
+        Returns (per-epoch sum of e^2, h2d bytes per epoch, d2h bytes per epoch)."""
+        t = nat.torch()
+        comp = t.cuda.current_stream()
+        cstream = t.cuda.Stream()
+        bufs = [(self.dev.col_rows, self.vals32, self.mask),
+                (t.empty_like(self.dev.col_rows), t.empty_like(self.vals32), t.empty_like(self.mask))]
+        src = (host["rows"], host["vals"], host["mask"])
+        copied = [t.cuda.Event(), t.cuda.Event()]
+        used = [t.cuda.Event(), t.cuda.Event()]
+        loss_dev = t.zeros(n_epochs, dtype=t.float64, device=self.loss.device)
+        loss_host = t.zeros(n_epochs, dtype=t.float64).pin_memory()
+
+        def fill(b):
+            with t.cuda.stream(cstream):
+                cstream.wait_event(used[b])
+                for dst, s_ in zip(bufs[b], src):
+                    dst.copy_(s_, non_blocking=True)
+                copied[b].record(cstream)
+
+        for b in (0, 1):
+            used[b].record(comp)
+        fill(0)
+        for e in range(n_epochs):
+            b = e % 2
+            comp.wait_event(copied[b])
+            if e + 1 < n_epochs:
+                fill(1 - b)
+            rows_b, vals_b, mask_b = bufs[b]
+            c = self.config
+            rates = _rates_struct(c.rates_at(t_start + e), c.regs)
+            d = self.dev
+            nat.call("culsh_sgd_hogwild_epoch", d.N, nat.ptr(d.col_ptr), None, nat.ptr(rows_b),
+                     nat.ptr(vals_b), nat.ptr(mask_b), nat.ptr(self.resid_ptr), nat.ptr(self.resid),
+                     nat.ptr(self.col_order), ctypes.byref(self.model.struct), ctypes.byref(rates),
+                     int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0),
+                     int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss_dev[e:]),
+                     nat.ptr(self.status), nat.stream_ptr())
+            used[b].record(comp)
+            loss_host[e:e + 1].copy_(loss_dev[e:e + 1], non_blocking=True)
+        comp.synchronize()
+        if int(self.status.item()):
+            raise TrainingDivergedError(epoch=t_start + n_epochs - 1)
+        h2d = sum(int(v.numel() * v.element_size()) for v in src)
+        return loss_host.numpy().copy(), h2d, 8
+
     def to_params(self) -> ModelParams:
         return self.model.to_params(self.neighbors, self.M, self.N)
 
