@@ -130,8 +130,8 @@ constexpr int hw_smem_per_warp() {
 // cp.async fills kHwDepth-1 updates ahead, so the HBM/L2 latency of the row
 // gather is off the update's critical path.  Each lane copies and later reads
 // only its own FV floats of every row, so the ring needs no warp barrier.
-template <int FV, int KPL>
-__global__ void __launch_bounds__(kHwWarps * 32)
+template <int FV, int KPL, bool ATOMIC>
+__global__ void __launch_bounds__(kHwWarps * 32, 4)
 hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__restrict__ seg,
                const int32_t *__restrict__ rows, const float *__restrict__ vals,
                const uint32_t *__restrict__ mask, const int64_t *__restrict__ resid_ptr,
@@ -144,7 +144,6 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
     constexpr int P = kHwDepth;
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;
-    const bool atomic_rows = (flags & 2) != 0;
     unsigned char *wbase = s_raw + (size_t)warp * hw_smem_per_warp<FV, KPL>();
     int4 *s_meta = reinterpret_cast<int4 *>(wbase);                           // 64 x 16 B
     uint32_t *s_m1 = reinterpret_cast<uint32_t *>(wbase + 64 * 16);           // KPL == 2
@@ -257,85 +256,109 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             cp_async_commit();
         }
         float lossf = 0.f;
-        for (int tt = 0; tt < n; ++tt) {
-            if ((tt & 31) == 0 && tt > 0) {
+        const float ngu = -R.gu * (1.f - R.au) / R.gu;   // = -(gu*lu): delta_u = ngu*u + gu*e*v
+        for (int base = 0; base < n; base += 32) {
+            if (base > 0) {
                 __syncwarp();   // every lane is done with the half being refilled
-                if (tt + 32 < n) load_chunk((tt >> 5) + 1);
+                if (base + 32 < n) load_chunk((base >> 5) + 1);
                 __syncwarp();
             }
-            if (tt + P - 1 < n) issue(tt + P - 1);
-            cp_async_commit();
-            cp_async_wait<P - 1>();
-            const int4 me = s_meta[tt & 63];
-            const int i = me.x;
-            const float r = __int_as_float(me.y);
-            const uint32_t m0 = (uint32_t)me.z;
-            const uint32_t m1 = KPL == 2 ? s_m1[tt & 63] : 0u;
-            float u[FV];
-            load_row<FV>(my_ring + (tt % P) * 32 * FV, u);
-            float part = 0.f;
+            const int cnt = min(32, n - base);
+            for (int k = 0; k < cnt; ++k) {
+                const int tt = base + k;
+                // prefetch P-1 ahead; past the end, re-fetch the last row into an unused slot
+                {
+                    const int tp = tt + P - 1;
+                    const int ip = s_meta[min(tp, n - 1) & 63].x;
+                    float *dst = my_ring + (tp % P) * 32 * FV;
+                    if (fl) cp_async_row<FV>(dst, Ulane + (size_t)(unsigned)ip * (unsigned)F);
+                    if (lane == 0) cp_async_bytes4(s_bring + (tp % P), Bv + ip);
+                }
+                cp_async_commit();
+                cp_async_wait<P - 1>();
+                const int4 me = s_meta[tt & 63];
+                const int i = me.x;
+                const float r = __int_as_float(me.y);
+                const uint32_t m0 = (uint32_t)me.z;
+                const uint32_t m1 = KPL == 2 ? s_m1[tt & 63] : 0u;
+                float u[FV];
+                load_row<FV>(my_ring + (tt % P) * 32 * FV, u);
+                const float bi = lane == 0 ? s_bring[tt % P] : 0.f;
+                float part = bi;
 #pragma unroll
-            for (int x = 0; x < FV; ++x) part = fmaf(u[x], v[x], part);
-            if (!fl) part = 0.f;
-            float bi = 0.f;
-            if (lane == 0) {
-                bi = s_bring[tt % P];
-                part += bi;
-            }
-            const bool anyex = (m0 | m1) != 0u;   // warp-uniform
-            float inv_r = 0.f, inv_n = invK;
-            float rs[KPL];
-            bool ex[KPL];
-            if (!anyex) {
+                for (int x = 0; x < FV; ++x) part = fmaf(u[x], fl ? v[x] : 0.f, part);
+                const bool anyex = (m0 | m1) != 0u;   // warp-uniform
+                float inv_r = 0.f, inv_n = invK;
+                float rs[KPL];
+                bool ex[KPL];
+                if (!anyex) {
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        ex[q] = false;
+                        rs[q] = 0.f;
+                        part = fmaf(c[q], invK, part);
+                    }
+                } else {
+                    const int nr = __popc(m0) + __popc(m1);
+                    const int nn = K - nr;
+                    inv_r = rsqrtf((float)nr);
+                    inv_n = nn > 0 ? rsqrtf((float)nn) : 0.f;
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        const uint32_t mq = q == 0 ? m0 : m1;
+                        ex[q] = (mq >> lane) & 1u;
+                        const int rank = (q == 0 ? 0 : __popc(m0)) + __popc(mq & lt_mask);
+                        rs[q] = ex[q] ? rcol[me.w + rank] : 0.f;
+                        part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;
+                    }
+                }
+                part = warp_sum(part);
+                const float e = r - (mu + bh + part);
+                lossf = fmaf(e, e, lossf);
+                // fused update of every touched parameter (factorization.py:307-328 rules)
+                const float geu = R.gu * e, gev = R.gv * e;
+                float* urow = U + (size_t)(unsigned)i * (unsigned)F + lane * FV;
+                if constexpr (ATOMIC) {
+                    // add the update instead of storing the new value: a concurrent update of the
+                    // same row by another warp is then never lost (only computed from a stale u_i)
+                    float dlt[FV];
+#pragma unroll
+                    for (int x = 0; x < FV; ++x) {
+                        const float uo = u[x];
+                        dlt[x] = fmaf(ngu, uo, geu * v[x]);
+                        v[x] = fmaf(R.av, v[x], gev * uo);
+                    }
+                    if (fl) {
+                        if constexpr (FV % 4 == 0) {
+#pragma unroll
+                            for (int x = 0; x < FV; x += 4)
+                                atomicAdd(reinterpret_cast<float4 *>(urow + x),
+                                          make_float4(dlt[x], dlt[x + 1], dlt[x + 2], dlt[x + 3]));
+                        } else if constexpr (FV == 2) {
+                            atomicAdd(reinterpret_cast<float2 *>(urow), make_float2(dlt[0], dlt[1]));
+                        } else {
+                            atomicAdd(urow, dlt[0]);
+                        }
+                    }
+                    if (lane == 0) atomicAdd(Bv + i, fmaf(R.ab - 1.f, bi, R.gb * e));
+                } else {
+#pragma unroll
+                    for (int x = 0; x < FV; ++x) {
+                        const float uo = u[x];
+                        u[x] = fmaf(R.au, uo, geu * v[x]);
+                        v[x] = fmaf(R.av, v[x], gev * uo);
+                    }
+                    if (fl) store_row<FV>(urow, u);
+                    if (lane == 0) Bv[i] = fmaf(R.ab, bi, R.gb * e);
+                }
+                bh = fmaf(R.abh, bh, R.gbh * e);
+                const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) {
-                    ex[q] = false;
-                    rs[q] = 0.f;
-                    part = fmaf(c[q], invK, part);
-                }
-            } else {
-                const int nr = __popc(m0) + __popc(m1);
-                const int nn = K - nr;
-                inv_r = rsqrtf((float)nr);
-                inv_n = nn > 0 ? rsqrtf((float)nn) : 0.f;
-#pragma unroll
-                for (int q = 0; q < KPL; ++q) {
-                    const uint32_t mq = q == 0 ? m0 : m1;
-                    ex[q] = (mq >> lane) & 1u;
-                    const int rank = (q == 0 ? 0 : __popc(m0)) + __popc(mq & lt_mask);
-                    rs[q] = ex[q] ? rcol[me.w + rank] : 0.f;
-                    part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;
-                }
-            }
-            part = warp_sum(part);
-            const float e = r - (mu + bh + part);
-            lossf = fmaf(e, e, lossf);
-            // fused update of every touched parameter (factorization.py:307-328 rules)
-            const float geu = R.gu * e, gev = R.gv * e;
-            float uold[FV];
-#pragma unroll
-            for (int x = 0; x < FV; ++x) {
-                const float uo = u[x];
-                uold[x] = uo;
-                u[x] = fmaf(R.au, uo, geu * v[x]);
-                v[x] = fmaf(R.av, v[x], gev * uo);
-            }
-            if (atomic_rows) {
-                // add the update instead of storing the new value: a concurrent update of the
-                // same row by another warp is then never lost (only computed from a stale u_i)
-                if (fl) add_row<FV>(U + (size_t)(unsigned)i * (unsigned)F + lane * FV, u, uold);
-                if (lane == 0) atomicAdd(Bv + i, fmaf(R.ab, bi, R.gb * e) - bi);
-            } else {
-                if (fl) store_row<FV>(U + (size_t)(unsigned)i * (unsigned)F + lane * FV, u);
-                if (lane == 0) Bv[i] = fmaf(R.ab, bi, R.gb * e);
-            }
-            bh = fmaf(R.abh, bh, R.gbh * e);
-            const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
-#pragma unroll
-            for (int q = 0; q < KPL; ++q) {
-                if (kin[q]) {
-                    if (ex[q]) w[q] = fmaf(R.aw, w[q], gwe * rs[q]);
-                    else c[q] = fmaf(R.ac, c[q], gce);
+                    const float wn = fmaf(R.aw, w[q], gwe * rs[q]);
+                    const float cn = fmaf(R.ac, c[q], gce);
+                    w[q] = (kin[q] && ex[q]) ? wn : w[q];
+                    c[q] = (kin[q] && !ex[q]) ? cn : c[q];
                 }
             }
         }
@@ -772,11 +795,13 @@ int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const 
     const size_t smem = (size_t)kHwWarps * hw_smem_per_warp<FV, KPL>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(hogwild_kernel<FV, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hogwild_kernel<FV, KPL>, threads, smem);
+    auto kern = (flags & 2) ? hogwild_kernel<FV, KPL, true> : hogwild_kernel<FV, KPL, false>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     if (occ < 1) occ = 1;
     int64_t blocks = (int64_t)num_sms() * occ;
     const int64_t need = (N + kHwWarps - 1) / kHwWarps;
@@ -784,7 +809,7 @@ int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const 
     if (max_warps > 0 && blocks > (max_warps + kHwWarps - 1) / kHwWarps)
         blocks = (max_warps + kHwWarps - 1) / kHwWarps;
     if (blocks < 1) blocks = 1;
-    hogwild_kernel<FV, KPL><<<(unsigned)blocks, threads, smem, st>>>(
+    kern<<<(unsigned)blocks, threads, smem, st>>>(
         N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m->mu, m->b, m->bhat, m->U, m->V, m->W,
         m->C, m->F, m->K, R, flags, ticket, loss, status);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
