@@ -108,6 +108,21 @@ int culsh_topk(const uint64_t *keys, int q, int64_t N_total, int key_bits, int64
                int64_t n_cols, int K, uint64_t seed, int32_t *entries,
                int64_t *n_candidates_out_host, void *stream);
 
+/* Stage APIs of the same pipeline (lsh.py:290-305 coarse_candidates, 377-398 fine_topk):
+ * culsh_pack_keys: keys (q, N) from a signature tensor sig (N, q, p, G) u8.
+ * culsh_candidates: per target column the bucket mates over all q groups, each
+ *   column's list sorted ascending.  Call with cand == NULL to get offsets
+ *   (n_cols+1, device int64) and *n_candidates_out; then with a buffer of that size.
+ * culsh_select_topk: frequency top-K + seeded supplement from caller-supplied
+ *   candidate lists (cand, offsets; unsorted is fine). */
+int culsh_pack_keys(const uint8_t *sig, int64_t N, int q, int p, int G, uint64_t *keys, void *stream);
+int culsh_candidates(const uint64_t *keys, int q, int64_t N_total, int key_bits, int64_t j_base,
+                     int64_t n_cols, int64_t *offsets, int32_t *cand, int64_t cand_capacity,
+                     int64_t *n_candidates_out_host, void *stream);
+int culsh_select_topk(const int32_t *cand, const int64_t *offsets, int64_t total, int64_t j_base,
+                      int64_t n_cols, int K, uint64_t seed, int64_t N_total, int32_t *entries,
+                      void *stream);
+
 /* ---------------------------------------------------------------- SGD --- */
 
 /* Learning rates and regularisers of one epoch (factorization.py:84-95). */

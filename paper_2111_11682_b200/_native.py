@@ -75,6 +75,9 @@ _SIGS = {
     "culsh_class_partition": [_vp, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp],
     "culsh_hash_count": [_vp, _vp, _vp, _i32, _vp, _i64, _i32, _i32, _i64, _i64, _vp, _i32, _i32, _i32, _vp,
                          _vp, _vp, _i64, _vp],
+    "culsh_pack_keys": [_vp, _i64, _i32, _i32, _i32, _vp, _vp],
+    "culsh_candidates": [_vp, _i32, _i64, _i32, _i64, _i64, _vp, _vp, _i64, _P(_i64), _vp],
+    "culsh_select_topk": [_vp, _vp, _i64, _i64, _i64, _i32, _u64, _i64, _vp, _vp],
     "culsh_topk": [_vp, _i32, _i64, _i32, _i64, _i64, _i32, _u64, _vp, _P(_i64), _vp],
     "culsh_pass_plan": [_vp, _vp, _i64, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _i32, _i32, _vp,
                         _vp, _vp],

@@ -726,3 +726,29 @@ extern "C" int culsh_value_set(const double *vals, int64_t n, double *out, int n
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }
+
+// lsh.py:246-260 _pack_group_keys for a given signature tensor sig (N, q, p, G) u8:
+// keys[g, j] bit (m*G + t) = sig[j, g, m, t] != 0.
+__global__ void pack_keys_kernel(const uint8_t *__restrict__ sig, int64_t N, int q, int p, int G,
+                                 uint64_t *__restrict__ keys) {
+    const int64_t total = N * (int64_t)q;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = x / q;
+        const int g = (int)(x % q);
+        const uint8_t *s = sig + (j * q + g) * (int64_t)p * G;
+        uint64_t k = 0;
+        for (int b = 0; b < p * G; ++b) k |= (uint64_t)(s[b] != 0) << b;
+        keys[(int64_t)g * N + j] = k;
+    }
+}
+
+extern "C" int culsh_pack_keys(const uint8_t *sig, int64_t N, int q, int p, int G, uint64_t *keys, void *stream) {
+    CULSH_REQUIRE(q >= 1 && p >= 1 && G >= 1 && p * G <= 64, "p*G exceeds the 64-bit bucket key");
+    if (N <= 0) return CULSH_OK;
+    const int64_t total = N * (int64_t)q;
+    const int blocks = (int)min64((total + 255) / 256, (int64_t)num_sms() * 8);
+    pack_keys_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sig, N, q, p, G, keys);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}

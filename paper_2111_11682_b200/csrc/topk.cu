@@ -156,9 +156,118 @@ struct DevBuf {
     template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
 };
 
+// ---- host-side stages -------------------------------------------------------
+
+// Buckets of every group: per (g, column) the [start, end) of its run of equal keys
+// in the group's key-sorted order (scols).  rs/re/scols are (q, N_total) int32.
+static int build_runs(const uint64_t *keys, int q, int64_t N_total, int key_bits, DevBuf &scols, DevBuf &rs,
+                      DevBuf &re, cudaStream_t st) {
+    const int64_t QN = (int64_t)q * N_total;
+    const int grid = (int)min64((QN + 255) / 256, (int64_t)num_sms() * 8);
+    DevBuf skeys(st), vals_in(st), seg(st), tmp(st);
+    CULSH_CHECK(skeys.alloc(sizeof(uint64_t) * QN));
+    CULSH_CHECK(vals_in.alloc(sizeof(int32_t) * QN));
+    CULSH_CHECK(scols.alloc(sizeof(int32_t) * QN));
+    CULSH_CHECK(seg.alloc(sizeof(int) * (q + 1)));
+    iota_cols_kernel<<<grid, 256, 0, st>>>(vals_in.as<int32_t>(), q, N_total, seg.as<int>());
+    CULSH_LAUNCH_CHECK();
+    size_t tb = 0;
+    CULSH_CHECK(cub::DeviceSegmentedRadixSort::SortPairs(
+        nullptr, tb, keys, skeys.as<uint64_t>(), vals_in.as<int32_t>(), scols.as<int32_t>(), (int)QN, q,
+        seg.as<int>(), seg.as<int>() + 1, 0, key_bits, st));
+    CULSH_CHECK(tmp.alloc(tb));
+    CULSH_CHECK(cub::DeviceSegmentedRadixSort::SortPairs(
+        tmp.p, tb, keys, skeys.as<uint64_t>(), vals_in.as<int32_t>(), scols.as<int32_t>(), (int)QN, q,
+        seg.as<int>(), seg.as<int>() + 1, 0, key_bits, st));
+    CULSH_CHECK(rs.alloc(sizeof(int32_t) * QN));
+    CULSH_CHECK(re.alloc(sizeof(int32_t) * QN));
+    runs_kernel<<<grid, 256, 0, st>>>(skeys.as<uint64_t>(), scols.as<int32_t>(), q, N_total, rs.as<int32_t>(),
+                                      re.as<int32_t>());
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+// offsets (n_cols+1, device int64) = exclusive prefix of per-target candidate counts;
+// returns the total through *total_host (one small D2H).
+static int candidate_offsets(const DevBuf &rs, const DevBuf &re, int q, int64_t N_total, int64_t j_base,
+                             int64_t n_cols, int64_t *offsets, int64_t *total_host, cudaStream_t st) {
+    DevBuf counts(st), tmp(st);
+    CULSH_CHECK(counts.alloc(sizeof(int64_t) * (n_cols + 1)));
+    const int gridc = (int)min64((n_cols + 127) / 128, (int64_t)num_sms() * 8);
+    cand_count_kernel<<<gridc, 128, 0, st>>>(rs.as<int32_t>(), re.as<int32_t>(), q, N_total, j_base, n_cols,
+                                             counts.as<int64_t>());
+    CULSH_LAUNCH_CHECK();
+    size_t tb = 0;
+    CULSH_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.as<int64_t>(), offsets, (int)(n_cols + 1), st));
+    CULSH_CHECK(tmp.alloc(tb));
+    CULSH_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.as<int64_t>(), offsets, (int)(n_cols + 1), st));
+    CULSH_CHECK(cudaMemcpyAsync(total_host, offsets + n_cols, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CULSH_CHECK(cudaStreamSynchronize(st));
+    return CULSH_OK;
+}
+
+static int sort_segments(const int32_t *in, int32_t *out, int64_t total, int64_t n_cols, const int64_t *offsets,
+                         cudaStream_t st) {
+    if (total <= 0) return CULSH_OK;
+    size_t tb = 0;
+    CULSH_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, in, out, (int)total, (int)n_cols, offsets,
+                                                   offsets + 1, st));
+    DevBuf tmp(st);
+    CULSH_CHECK(tmp.alloc(tb));
+    CULSH_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp.p, tb, in, out, (int)total, (int)n_cols, offsets,
+                                                   offsets + 1, st));
+    return CULSH_OK;
+}
+
 }  // namespace culsh
 
 using namespace culsh;
+
+extern "C" int culsh_candidates(const uint64_t *keys, int q, int64_t N_total, int key_bits, int64_t j_base,
+                                int64_t n_cols, int64_t *offsets, int32_t *cand, int64_t cand_capacity,
+                                int64_t *n_candidates_out, void *stream) {
+    CULSH_REQUIRE(q >= 1 && N_total >= 1, "empty key matrix");
+    CULSH_REQUIRE((int64_t)q * N_total < (1LL << 31), "q*N too large for one sort");
+    CULSH_REQUIRE(j_base >= 0 && j_base + n_cols <= N_total, "target columns out of range");
+    if (key_bits <= 0 || key_bits > 64) key_bits = 64;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf scols(st), rs(st), re(st);
+    int r = build_runs(keys, q, N_total, key_bits, scols, rs, re, st);
+    if (r != CULSH_OK) return r;
+    int64_t total = 0;
+    if (n_cols > 0) {
+        r = candidate_offsets(rs, re, q, N_total, j_base, n_cols, offsets, &total, st);
+        if (r != CULSH_OK) return r;
+    }
+    if (n_candidates_out) *n_candidates_out = total;
+    if (!cand || total == 0) return CULSH_OK;
+    CULSH_REQUIRE(cand_capacity >= total, "candidate buffer too small");
+    CULSH_REQUIRE(total < (1LL << 31), "candidate list exceeds 2^31 entries");
+    DevBuf raw(st);
+    CULSH_CHECK(raw.alloc(sizeof(int32_t) * total));
+    const int gridc = (int)min64((n_cols + 127) / 128, (int64_t)num_sms() * 8);
+    cand_fill_kernel<<<gridc, 128, 0, st>>>(scols.as<int32_t>(), rs.as<int32_t>(), re.as<int32_t>(), q, N_total,
+                                            j_base, n_cols, offsets, raw.as<int32_t>());
+    CULSH_LAUNCH_CHECK();
+    return sort_segments(raw.as<int32_t>(), cand, total, n_cols, offsets, st);
+}
+
+extern "C" int culsh_select_topk(const int32_t *cand, const int64_t *offsets, int64_t total, int64_t j_base,
+                                 int64_t n_cols, int K, uint64_t seed, int64_t N_total, int32_t *entries,
+                                 void *stream) {
+    CULSH_REQUIRE(K >= 0 && K <= kMaxK, "K out of supported range [0, 128]");
+    CULSH_REQUIRE(K <= N_total - 1 || n_cols == 0, "K exceeds N-1");
+    if (n_cols <= 0 || K == 0) return CULSH_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf sorted(st);
+    CULSH_CHECK(sorted.alloc(sizeof(int32_t) * (total > 0 ? total : 1)));
+    int r = sort_segments(cand, sorted.as<int32_t>(), total, n_cols, offsets, st);
+    if (r != CULSH_OK) return r;
+    const int gridc = (int)min64((n_cols + 127) / 128, (int64_t)num_sms() * 8);
+    select_kernel<<<gridc, 128, 0, st>>>(sorted.as<int32_t>(), offsets, j_base, n_cols, K, seed, N_total, entries);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
 
 extern "C" int culsh_topk(const uint64_t *keys, int q, int64_t N_total, int key_bits, int64_t j_base,
                           int64_t n_cols, int K, uint64_t seed, int32_t *entries,
@@ -170,76 +279,32 @@ extern "C" int culsh_topk(const uint64_t *keys, int q, int64_t N_total, int key_
     CULSH_REQUIRE(j_base >= 0 && j_base + n_cols <= N_total, "target columns out of range");
     if (key_bits <= 0 || key_bits > 64) key_bits = 64;
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t QN = (int64_t)q * N_total;
-    const int grid = (int)min64((QN + 255) / 256, (int64_t)num_sms() * 8);
-
-    DevBuf skeys(st), vals_in(st), scols(st), seg(st), rs(st), re(st), counts(st), offsets(st),
-        cand(st), cand_sorted(st), tmp(st), tmp2(st);
-    CULSH_CHECK(skeys.alloc(sizeof(uint64_t) * QN));
-    CULSH_CHECK(vals_in.alloc(sizeof(int32_t) * QN));
-    CULSH_CHECK(scols.alloc(sizeof(int32_t) * QN));
-    CULSH_CHECK(seg.alloc(sizeof(int) * (q + 1)));
-    iota_cols_kernel<<<grid, 256, 0, st>>>(vals_in.as<int32_t>(), q, N_total, seg.as<int>());
-    CULSH_LAUNCH_CHECK();
-
-    size_t tb = 0;
-    CULSH_CHECK(cub::DeviceSegmentedRadixSort::SortPairs(
-        nullptr, tb, keys, skeys.as<uint64_t>(), vals_in.as<int32_t>(), scols.as<int32_t>(), (int)QN, q,
-        seg.as<int>(), seg.as<int>() + 1, 0, key_bits, st));
-    CULSH_CHECK(tmp.alloc(tb));
-    CULSH_CHECK(cub::DeviceSegmentedRadixSort::SortPairs(
-        tmp.p, tb, keys, skeys.as<uint64_t>(), vals_in.as<int32_t>(), scols.as<int32_t>(), (int)QN, q,
-        seg.as<int>(), seg.as<int>() + 1, 0, key_bits, st));
-
-    CULSH_CHECK(rs.alloc(sizeof(int32_t) * QN));
-    CULSH_CHECK(re.alloc(sizeof(int32_t) * QN));
-    runs_kernel<<<grid, 256, 0, st>>>(skeys.as<uint64_t>(), scols.as<int32_t>(), q, N_total,
-                                      rs.as<int32_t>(), re.as<int32_t>());
-    CULSH_LAUNCH_CHECK();
-
+    DevBuf scols(st), rs(st), re(st), offsets(st), cand(st), cand_sorted(st);
+    int r = build_runs(keys, q, N_total, key_bits, scols, rs, re, st);
+    if (r != CULSH_OK) return r;
     if (n_cols == 0) {
         if (n_candidates_out) *n_candidates_out = 0;
         return CULSH_OK;
     }
-    CULSH_CHECK(counts.alloc(sizeof(int64_t) * (n_cols + 1)));
     CULSH_CHECK(offsets.alloc(sizeof(int64_t) * (n_cols + 1)));
-    const int gridc = (int)min64((n_cols + 127) / 128, (int64_t)num_sms() * 8);
-    cand_count_kernel<<<gridc, 128, 0, st>>>(rs.as<int32_t>(), re.as<int32_t>(), q, N_total, j_base,
-                                             n_cols, counts.as<int64_t>());
-    CULSH_LAUNCH_CHECK();
-    size_t tb2 = 0;
-    CULSH_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, counts.as<int64_t>(), offsets.as<int64_t>(),
-                                              (int)(n_cols + 1), st));
-    CULSH_CHECK(tmp2.alloc(tb2));
-    CULSH_CHECK(cub::DeviceScan::ExclusiveSum(tmp2.p, tb2, counts.as<int64_t>(), offsets.as<int64_t>(),
-                                              (int)(n_cols + 1), st));
     int64_t total = 0;
-    CULSH_CHECK(cudaMemcpyAsync(&total, offsets.as<int64_t>() + n_cols, sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, st));
-    CULSH_CHECK(cudaStreamSynchronize(st));
+    r = candidate_offsets(rs, re, q, N_total, j_base, n_cols, offsets.as<int64_t>(), &total, st);
+    if (r != CULSH_OK) return r;
     if (n_candidates_out) *n_candidates_out = total;
     CULSH_REQUIRE(total < (1LL << 31), "candidate list exceeds 2^31 entries");
-
     CULSH_CHECK(cand.alloc(sizeof(int32_t) * total));
     CULSH_CHECK(cand_sorted.alloc(sizeof(int32_t) * total));
+    const int gridc = (int)min64((n_cols + 127) / 128, (int64_t)num_sms() * 8);
     if (total > 0) {
-        cand_fill_kernel<<<gridc, 128, 0, st>>>(scols.as<int32_t>(), rs.as<int32_t>(), re.as<int32_t>(),
-                                                q, N_total, j_base, n_cols, offsets.as<int64_t>(),
-                                                cand.as<int32_t>());
+        cand_fill_kernel<<<gridc, 128, 0, st>>>(scols.as<int32_t>(), rs.as<int32_t>(), re.as<int32_t>(), q,
+                                                N_total, j_base, n_cols, offsets.as<int64_t>(), cand.as<int32_t>());
         CULSH_LAUNCH_CHECK();
-        size_t tb3 = 0;
-        CULSH_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb3, cand.as<int32_t>(),
-                                                       cand_sorted.as<int32_t>(), (int)total, (int)n_cols,
-                                                       offsets.as<int64_t>(), offsets.as<int64_t>() + 1, st));
-        DevBuf tmp3(st);
-        CULSH_CHECK(tmp3.alloc(tb3));
-        CULSH_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp3.p, tb3, cand.as<int32_t>(),
-                                                       cand_sorted.as<int32_t>(), (int)total, (int)n_cols,
-                                                       offsets.as<int64_t>(), offsets.as<int64_t>() + 1, st));
+        r = sort_segments(cand.as<int32_t>(), cand_sorted.as<int32_t>(), total, n_cols, offsets.as<int64_t>(), st);
+        if (r != CULSH_OK) return r;
     }
     if (K > 0) {
-        select_kernel<<<gridc, 128, 0, st>>>(cand_sorted.as<int32_t>(), offsets.as<int64_t>(), j_base,
-                                             n_cols, K, seed, N_total, entries);
+        select_kernel<<<gridc, 128, 0, st>>>(cand_sorted.as<int32_t>(), offsets.as<int64_t>(), j_base, n_cols, K,
+                                             seed, N_total, entries);
         CULSH_LAUNCH_CHECK();
     }
     return CULSH_OK;

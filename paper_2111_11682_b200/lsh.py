@@ -386,6 +386,57 @@ def _topk_device(keys, q: int, N_total: int, key_bits: int, j_base: int, n_cols:
     return entries, int(ncand.value)
 
 
+def coarse_candidates(signatures) -> list[np.ndarray]:
+    """Bucket columns that agree on all p maps of one group (lsh.py:290-305).
+
+    ``signatures`` is a sequence of p arrays of shape (N, G); returns, per column,
+    the sorted int32 array of the other columns sharing its bucket key.
+    """
+    sig_group = np.stack([np.asarray(s, dtype=np.uint8) for s in signatures], axis=1)
+    N, p, G = sig_group.shape
+    if p * G > 64:
+        raise ValueError("p*G exceeds the 64-bit bucket key")
+    if N == 0:
+        return []
+    sig = nat.to_dev(np.ascontiguousarray(sig_group.reshape(N, 1, p, G)).reshape(-1))
+    keys = nat.empty((N,), "uint64")
+    nat.call("culsh_pack_keys", nat.ptr(sig), N, 1, p, G, nat.ptr(keys), nat.stream_ptr())
+    offsets = nat.empty((N + 1,), "int64")
+    total = ctypes.c_int64(0)
+    nat.call("culsh_candidates", nat.ptr(keys), 1, N, p * G, 0, N, nat.ptr(offsets), None, 0,
+             ctypes.byref(total), nat.stream_ptr())
+    cand = nat.empty((max(total.value, 1),), "int32")
+    nat.call("culsh_candidates", nat.ptr(keys), 1, N, p * G, 0, N, nat.ptr(offsets), nat.ptr(cand),
+             max(total.value, 1), ctypes.byref(total), nat.stream_ptr())
+    off = nat.to_host(offsets)
+    c = nat.to_host(cand)[:total.value]
+    return [c[off[j]:off[j + 1]].astype(np.int32) for j in range(N)]
+
+
+def fine_topk(candidate_sets, K: int, N: int, seed: int) -> NeighborTable:
+    """Top-K by occurrence frequency across the q groups, seeded supplement
+    (lsh.py:377-398); ``candidate_sets`` is q per-group lists of per-column arrays."""
+    if K > N - 1:
+        raise ValueError(f"K={K} exceeds N-1={N - 1}")
+    counts = np.zeros(N + 1, dtype=np.int64)
+    for group in candidate_sets:
+        for j in range(N):
+            counts[j + 1] += len(group[j])
+    offsets = np.cumsum(counts)
+    cand = np.empty(max(int(offsets[N]), 1), dtype=np.int32)
+    fill = offsets[:N].copy()
+    for group in candidate_sets:
+        for j in range(N):
+            k = len(group[j])
+            cand[fill[j]:fill[j] + k] = group[j]
+            fill[j] += k
+    entries = nat.empty((max(N * K, 1),), "int32")
+    cand_d, off_d = nat.to_dev(cand), nat.to_dev(offsets)   # keep alive across the call
+    nat.call("culsh_select_topk", nat.ptr(cand_d), nat.ptr(off_d), int(offsets[N]), 0, N, K,
+             ctypes.c_uint64(seed), N, nat.ptr(entries), nat.stream_ptr())
+    return NeighborTable(N=N, K=K, entries=nat.to_host(entries)[:N * K].reshape(N, K).copy())
+
+
 def simlsh_topk(ratings: SparseRatings, config: LshConfig, K: int):
     """Approximate Top-K neighbours of every column (lsh.py:426-438).
 

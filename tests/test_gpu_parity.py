@@ -443,3 +443,52 @@ class TestBitCountPath:
         r = P.SparseRatings(M, 2, rows, cols, vals)
         c = P.LshConfig(G=8, p=2, q=2, psi_exponent=2, seed=0)
         assert P.compute_hash_state(r, c).acc.tobytes() == self._fp64(P, r, c).tobytes()
+
+
+class TestStageApis:
+    """coarse_candidates / fine_topk (lsh.py:290-305, 377-398) as in test_lsh.py:111-257."""
+
+    def test_equal_signatures_bucket_together(self, P):
+        sig = np.zeros((3, 4), dtype=np.uint8)
+        sig[2, 1] = 1
+        out = P.coarse_candidates([sig])
+        assert list(out[0]) == [1] and list(out[1]) == [0] and list(out[2]) == []
+
+    def test_any_differing_bit_separates(self, P):
+        s1 = np.zeros((2, 4), dtype=np.uint8)
+        s2 = np.zeros((2, 4), dtype=np.uint8)
+        s2[1, 3] = 1
+        out = P.coarse_candidates([s1, s2])
+        assert list(out[0]) == [] and list(out[1]) == []
+
+    def test_fine_topk_rules(self, P):
+        groups = [[np.array([5, 2]), *[np.array([], int)] * 9],
+                  [np.array([5, 2, 7]), *[np.array([], int)] * 9],
+                  [np.array([5]), *[np.array([], int)] * 9]]
+        assert list(P.fine_topk(groups, K=2, N=10, seed=0).entries[0]) == [5, 2]
+        assert P.fine_topk([[np.array([7, 3]), *[np.array([], int)] * 9]], K=1, N=10, seed=0).entries[0, 0] == 3
+        t = P.fine_topk([[np.array([4]), *[np.array([], int)] * 4]], K=3, N=5, seed=1)
+        assert t.entries[0, 0] == 4 and len(set(t.entries[0])) == 3 and 0 not in t.entries[0]
+        P.fine_topk([[np.array([], int)] * 6], K=3, N=6, seed=2).validate()
+        with pytest.raises(ValueError):
+            P.fine_topk([[np.array([], int)] * 3], K=3, N=3, seed=0)
+
+    def test_pipeline_equals_composition(self, P):
+        # test_lsh.py:233-257: one call == per-map signatures -> per-group buckets -> top-K
+        rng = np.random.default_rng(42)
+        mask = rng.random((12, 9)) < 0.5
+        rows, cols = np.nonzero(mask)
+        r = P.SparseRatings(12, 9, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+        cfg = P.LshConfig(G=5, p=2, q=3, psi_exponent=2, seed=8)
+        table, state = P.simlsh_topk(r, cfg, K=3)
+        hashes = P.assign_row_hashes(r.M, cfg)
+        groups = []
+        for g in range(cfg.q):
+            sigs = []
+            for m in range(cfg.p):
+                H = hashes.map_bits(g, m)
+                sigs.append(np.stack([P.simlsh_signature(j, r, H, cfg.psi_exponent)[1]
+                                      for j in range(r.N)]))
+            groups.append(P.coarse_candidates(sigs))
+        composed = P.fine_topk(groups, K=3, N=r.N, seed=cfg.seed)
+        np.testing.assert_array_equal(composed.entries, table.entries)
