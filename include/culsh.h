@@ -172,11 +172,13 @@ int culsh_block_pointers(const int64_t *col_ptr, const int32_t *col_rows, int64_
  * are scratch; *status (device int) is OR-ed with 1 on a non-finite error.
  * Replaces factorization.py:332-363 _full_pass_block, parallel.py:110-128
  * _stage_pass (all D blocks of a stage in one launch) and online.py:253-271
- * _online_col_pass. */
+ * _online_col_pass.  variant 0: the full model; variant 3: the row-major basic-MF
+ * pass (factorization.py:366-391 _basic_pass, K = 0) run on the TRANSPOSED data
+ * (CulshData with rows and columns swapped, csc2csr = the CSR->CSC map). */
 int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
                             const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
-                            int64_t col_hi, int row_mode, int64_t M_old, int *row_last,
-                            int *ticket, int *status, void *stream);
+                            int64_t col_hi, int row_mode, int64_t M_old, int variant,
+                            int *row_last, int *ticket, int *status, void *stream);
 
 /* online.py:230-250 _online_row_pass (rows [row_lo,row_hi), columns < N_old). */
 int culsh_sgd_exact_rowpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,

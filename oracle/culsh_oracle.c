@@ -542,3 +542,32 @@ double orc_predict(int64_t i, int64_t j, const int64_t *row_ptr, const int32_t *
                   (double *)V, (double *)W, (double *)C, nbr, F, K, base_b, base_bhat};
     return predict_one(&md, i, j);
 }
+
+/* factorization.py:366-391 _basic_pass: row-major basic MF over rows_subset (in that
+ * order); pred = (use_biases ? mu + b_i + b_hat_j : 0) with the products added one by
+ * one; returns 1 on the first non-finite error (before its update). */
+int orc_basic_pass(const int64_t *rows_subset, int64_t n_rows, const int64_t *row_ptr,
+                   const int32_t *row_cols, const double *row_vals, double mu, double *b, double *bhat,
+                   double *U, double *V, int F, int use_biases, const orc_rates_t *rt) {
+    for (int64_t ii = 0; ii < n_rows; ++ii) {
+        const int64_t i = rows_subset[ii];
+        for (int64_t idx = row_ptr[i]; idx < row_ptr[i + 1]; ++idx) {
+            const int64_t j = row_cols[idx];
+            double pred = 0.0;
+            if (use_biases) pred = mu + b[i] + bhat[j];
+            for (int f = 0; f < F; ++f) pred += U[i * F + f] * V[j * F + f];
+            const double e = row_vals[idx] - pred;
+            if (!isfinite(e)) return 1;
+            if (use_biases) {
+                b[i] += rt->gb * (e - rt->lb * b[i]);
+                bhat[j] += rt->gbh * (e - rt->lbh * bhat[j]);
+            }
+            for (int f = 0; f < F; ++f) {
+                const double uf = U[i * F + f], vf = V[j * F + f];
+                U[i * F + f] = uf + rt->gu * (e * vf - rt->lu * uf);
+                V[j * F + f] = vf + rt->gv * (e * uf - rt->lv * vf);
+            }
+        }
+    }
+    return 0;
+}

@@ -408,3 +408,29 @@ def stage_pass(d: Csr, m: Model, rates: Rates, col_lo: int, col_hi: int, rb: int
     return lib().orc_stage_pass(ctypes.c_int64(col_lo), ctypes.c_int64(col_hi), rb,
                                 _p(block_ptr), nb, _p(d.col_rows), _p(d.col_vals),
                                 *_model_args(d, m), ctypes.byref(rates))
+
+
+def train_basic(d: Csr, mu_data, F, epochs, seed, rates_fn, regs, with_biases=False,
+                sort_rows_by_count=False, init_scale=None) -> Model:
+    """factorization.py:476-527 train_basic, serial (racy_workers=0)."""
+    rng = np.random.default_rng(seed)
+    scale = init_scale if init_scale is not None else 1.0 / np.sqrt(F)
+    U = rng.uniform(0.0, scale, size=(d.M, F))
+    V = rng.uniform(0.0, scale, size=(d.N, F))
+    if with_biases:
+        mu, b, bh = mu_data, d.base_b.copy(), d.base_bhat.copy()
+    else:
+        mu, b, bh = 0.0, np.zeros(d.M), np.zeros(d.N)
+    if sort_rows_by_count:
+        order = np.argsort(-np.diff(d.row_ptr), kind="stable").astype(np.int64)
+    else:
+        order = np.arange(d.M, dtype=np.int64)
+    lib().orc_basic_pass.restype = ctypes.c_int
+    for t in range(epochs):
+        rt = make_rates(rates_fn(t), regs)
+        bad = lib().orc_basic_pass(_p(order), ctypes.c_int64(d.M), _p(d.row_ptr), _p(d.row_cols),
+                                   _p(d.row_vals), ctypes.c_double(mu), _p(b), _p(bh), _p(U), _p(V), F,
+                                   int(with_biases), ctypes.byref(rt))
+        if bad:
+            raise FloatingPointError(f"diverged at epoch {t}")
+    return Model(mu, b, bh, U, V, np.zeros((d.N, 0)), np.zeros((d.N, 0)), np.zeros((d.N, 0), np.int32))

@@ -55,18 +55,27 @@ struct Scalars {
     double e, inv_r, inv_n;
 };
 
+// variant bit 0: basic-MF summation (factorization.py:375-379: pred starts at the
+//   bias sum and the products are added to it one by one, no separate dot);
+// variant bit 1: the pass runs on the transposed matrix (rows as columns, for the
+//   row-major basic pass) -- the reference's bias sum is (mu + b_i) + b_hat_j with
+//   b_i then being the register-resident side.
 __device__ __forceinline__ Scalars exact_error(const double *buf, int F, int K, const uint32_t *emask,
-                                               double mu, double bi, double bhj, double r) {
-    double dot = 0.0;
-    for (int f = 0; f < F; ++f) dot = dot + buf[f];
+                                               double mu, double bi, double bhj, double r, int variant) {
+    double pred = (variant & 2) ? mu + bhj + bi : mu + bi + bhj;
+    if (variant & 1) {
+        for (int f = 0; f < F; ++f) pred = pred + buf[f];
+    } else {
+        double dot = 0.0;
+        for (int f = 0; f < F; ++f) dot = dot + buf[f];
+        pred = pred + dot;
+    }
     int nr = 0, nn = 0;
     double sw = 0.0, sc = 0.0;
     for (int k = 0; k < K; ++k) {
         if ((emask[k >> 5] >> (k & 31)) & 1u) { ++nr; sw = sw + buf[F + k]; }
         else { ++nn; sc = sc + buf[F + k]; }
     }
-    double pred = mu + bi + bhj;
-    pred = pred + dot;
     if (nr > 0) pred = pred + sw / sqrt((double)nr);
     if (nn > 0) pred = pred + sc / sqrt((double)nn);
     Scalars s;
@@ -80,7 +89,7 @@ template <int FPL, int KPL>
 __global__ void __launch_bounds__(256)
 exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                  const int32_t *__restrict__ chain_lo, int64_t col_lo, int64_t col_hi, int row_mode,
-                 int64_t M_old, int *__restrict__ row_last, int *__restrict__ ticket,
+                 int64_t M_old, int variant, int *__restrict__ row_last, int *__restrict__ ticket,
                  int *__restrict__ status) {
     extern __shared__ double s_buf[];
     const int warp = threadIdx.x >> 5;
@@ -166,7 +175,7 @@ exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                 if (k < K) buf[F + k] = expl[q] ? resid[q] * w[q] : c[q];
             }
             __syncwarp();
-            const Scalars s = exact_error(buf, F, K, emask, mu, bi, bhj, r);
+            const Scalars s = exact_error(buf, F, K, emask, mu, bi, bhj, r, variant);
             const double e = s.e;
             if (!isfinite(e)) {
                 if (lane == 0) atomicOr(status, 1);
@@ -275,7 +284,7 @@ exact_row_kernel(ExactModel P, CulshRates R, int64_t row_lo, int64_t row_hi, int
                 if (k < K) buf[F + k] = expl[q] ? resid[q] * w[q] : c[q];
             }
             __syncwarp();
-            const Scalars s = exact_error(buf, F, K, emask, mu, bi, P.bhat[j], r);
+            const Scalars s = exact_error(buf, F, K, emask, mu, bi, P.bhat[j], r, 0);
             const double e = s.e;
             if (!isfinite(e)) {
                 if (lane == 0) atomicOr(status, 1);
@@ -355,8 +364,8 @@ __global__ void block_pointers_kernel(const int64_t *__restrict__ col_ptr, const
 
 template <int FPL, int KPL>
 int launch_col(const ExactModel &P, const CulshRates &R, const int64_t *seg, const int32_t *chain_lo,
-               int64_t col_lo, int64_t col_hi, int row_mode, int64_t M_old, int *row_last, int *ticket,
-               int *status, cudaStream_t st) {
+               int64_t col_lo, int64_t col_hi, int row_mode, int64_t M_old, int variant, int *row_last,
+               int *ticket, int *status, cudaStream_t st) {
     const int threads = 128;
     const size_t smem = (size_t)(threads / 32) * (P.F + P.K) * sizeof(double);
     int occ = 0;
@@ -368,7 +377,7 @@ int launch_col(const ExactModel &P, const CulshRates &R, const int64_t *seg, con
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
     exact_col_kernel<FPL, KPL><<<(unsigned)blocks, threads, smem, st>>>(
-        P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, row_last, ticket, status);
+        P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
 }
 
@@ -453,8 +462,8 @@ extern "C" int culsh_pass_plan(const int64_t *col_ptr, const int32_t *col_rows, 
 
 extern "C" int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
                                        const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
-                                       int64_t col_hi, int row_mode, int64_t M_old, int *row_last,
-                                       int *ticket, int *status, void *stream) {
+                                       int64_t col_hi, int row_mode, int64_t M_old, int variant,
+                                       int *row_last, int *ticket, int *status, void *stream) {
     CULSH_REQUIRE(m->F >= 1 && m->F <= 256, "F must be in [1, 256]");
     CULSH_REQUIRE(m->K >= 0 && m->K <= 64, "K must be in [0, 64]");
     if (col_hi <= col_lo) return CULSH_OK;
@@ -463,7 +472,7 @@ extern "C" int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, cons
     CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     const ExactModel P = make_model(d, m);
     const CulshRates R = *r;
-#define CALL_COL(a, b) launch_col<a, b>(P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, row_last, ticket, status, st)
+#define CALL_COL(a, b) launch_col<a, b>(P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status, st)
     CULSH_DISPATCH_FK(m->F, m->K, CALL_COL);
 #undef CALL_COL
 }

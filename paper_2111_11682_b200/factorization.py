@@ -257,10 +257,11 @@ def _plan_full(dev, sc: _Scratch, col_lo, col_hi, row_lo, row_hi) -> None:
 
 
 def _colpass(dev, dm: DeviceModel64, sc: _Scratch, rates: nat.CulshRates, col_lo, col_hi,
-             row_mode: int, M_old: int = 0) -> None:
+             row_mode: int, M_old: int = 0, variant: int = 0) -> None:
     nat.call("culsh_sgd_exact_colpass", ctypes.byref(dev.struct), ctypes.byref(dm.struct),
              ctypes.byref(rates), nat.ptr(sc.seg), nat.ptr(sc.chain), col_lo, col_hi, row_mode,
-             M_old, nat.ptr(sc.row_last), nat.ptr(sc.ticket), nat.ptr(sc.status), nat.stream_ptr())
+             M_old, variant, nat.ptr(sc.row_last), nat.ptr(sc.ticket), nat.ptr(sc.status),
+             nat.stream_ptr())
 
 
 def _check_model_dims(F: int, K: int) -> None:
@@ -338,6 +339,108 @@ def sgd_update(i: int, j: int, params: ModelParams, rates: tuple, regs: tuple,
     if not np.isfinite(e) or sc.status_value():
         raise TrainingDivergedError(epoch=0)
     return float(e)
+
+
+def _transposed_device(r: SparseRatings):
+    """The ratings with rows and columns swapped, in HBM (row-major passes run the
+    column-pass kernels on it)."""
+    from .data import DeviceRatings
+    dev = r.device()
+    return DeviceRatings.from_device(r.N, r.M, dev.row_ptr, dev.row_cols, dev.row_vals, dev.col_ptr,
+                                     dev.col_rows, dev.col_vals, 0.0, nat.zeros((max(r.N, 1),), "float64"),
+                                     nat.zeros((max(r.M, 1),), "float64"))
+
+
+def train_basic(ratings: SparseRatings, config: TrainConfig, with_biases: bool = False,
+                sort_rows_by_count: bool = False, racy_workers: int = 0,
+                epoch_callback=None) -> ModelParams:
+    """Basic MF (U, V, optional biases), row-major SGD (factorization.py:476-527; the
+    paper's CUSGD++, Alg. 2).
+
+    racy_workers == 0: the exact serial row-major order, bit-identical to the
+    reference, run by the exact kernel on the transposed matrix (rows take the role
+    of columns; the wavefront waits on the previous updater of each column).
+    racy_workers > 0: lock-free (Hogwild on V) fp32 on the GPU, like the reference's
+    racy mode nondeterministic; the worker count itself is not meaningful here.
+    """
+    config.validate()
+    M, N = ratings.M, ratings.N
+    rng = np.random.default_rng(config.seed)
+    scale = config.effective_init_scale
+    U = rng.uniform(0.0, scale, size=(M, config.F))
+    V = rng.uniform(0.0, scale, size=(N, config.F))
+    if with_biases:
+        stats = ratings.baselines()
+        mu, b, bhat = stats.mu, stats.b.copy(), stats.b_hat.copy()
+    else:
+        mu, b, bhat = 0.0, np.zeros(M), np.zeros(N)
+    params = ModelParams(mu=mu, b=b, b_hat=bhat, U=U, V=V, W=np.zeros((N, 0)), C=np.zeros((N, 0)),
+                         neighbors=None)
+    if config.epochs == 0 or ratings.nnz == 0:
+        return params
+    _check_model_dims(config.F, 0)
+    if sort_rows_by_count:   # process rows in that order == relabel rows by rank
+        counts = np.diff(ratings.row_ptr)
+        order = np.argsort(-counts, kind="stable").astype(np.int64)
+    else:
+        order = np.arange(M, dtype=np.int64)
+    rank = np.empty(M, dtype=np.int64)
+    rank[order] = np.arange(M)
+    work = ratings if not sort_rows_by_count else SparseRatings(
+        M, N, rank[ratings.entry_rows], ratings.entry_cols, ratings.entry_values)
+    # transposed model: the kernel's (row side, column side) = (columns, rows) of the data
+    tp = ModelParams(mu=mu, b=params.b_hat, b_hat=params.b[order], U=params.V, V=params.U[order],
+                     W=np.zeros((M, 0)), C=np.zeros((M, 0)), neighbors=None)
+    if racy_workers > 0:
+        from .hogwild import HogwildTrainer
+        tdev = _transposed_device(work)
+        tcfg = replace(config, K=0, alpha_b=config.alpha_b_hat, alpha_b_hat=config.alpha_b,
+                       alpha_u=config.alpha_v, alpha_v=config.alpha_u,
+                       lambda_b=config.lambda_b_hat, lambda_b_hat=config.lambda_b,
+                       lambda_u=config.lambda_v, lambda_v=config.lambda_u)
+        tr = HogwildTrainer(None, None, tcfg, dev=tdev, params=tp)
+        if not with_biases:   # biases stay 0: zero rates
+            tr.config = replace(tcfg, alpha_b=1e-300, alpha_b_hat=1e-300)
+        for t in range(config.epochs):
+            tr.epoch(t)
+            if epoch_callback is not None:
+                _basic_from_transposed(tr.to_params(), params, order)
+                epoch_callback(t, params)
+        _basic_from_transposed(tr.to_params(), params, order)
+        return params
+    tdev = _transposed_device(work)
+    dm = DeviceModel64(tp)
+    sc = _Scratch(N, M)
+    _plan_full(tdev, sc, 0, M, 0, N)
+    for t in range(config.epochs):
+        gb, gbh, gu, gv, _, _ = config.rates_at(t)
+        if not with_biases:
+            gb = gbh = 0.0
+        rates = _rates_struct((gbh, gb, gv, gu, 0.0, 0.0),
+                              (config.lambda_b_hat, config.lambda_b, config.lambda_v, config.lambda_u,
+                               0.0, 0.0))
+        _colpass(tdev, dm, sc, rates, 0, M, 1, 0, variant=3)
+        if sc.status_value():
+            dm.download(tp)
+            _basic_from_transposed(tp, params, order)
+            raise TrainingDivergedError(epoch=t)
+        if epoch_callback is not None:
+            dm.download(tp)
+            _basic_from_transposed(tp, params, order)
+            epoch_callback(t, params)
+            tp = ModelParams(mu=mu, b=params.b_hat, b_hat=params.b[order], U=params.V,
+                             V=params.U[order], W=np.zeros((M, 0)), C=np.zeros((M, 0)))
+            dm = DeviceModel64(tp)
+    dm.download(tp)
+    _basic_from_transposed(tp, params, order)
+    return params
+
+
+def _basic_from_transposed(tp: ModelParams, params: ModelParams, order: np.ndarray) -> None:
+    params.b_hat[...] = tp.b
+    params.V[...] = tp.U
+    params.b[order] = tp.b_hat
+    params.U[order] = tp.V
 
 
 def train_full(ratings: SparseRatings, neighbors: NeighborTable | None,

@@ -197,15 +197,38 @@ def online_c1(train):
     return out
 
 
+def basic():
+    """train_basic (factorization.py:476-527): serial row-major, +/- biases, sorted rows."""
+    from lshmf.factorization import train_basic
+    out = {}
+    cases = [(0, True, 4, 5, False, False), (1, False, 3, 4, True, False), (2, True, 8, 3, False, True),
+             (3, False, 2, 6, True, True)]
+    for s, (seed, integer, F, epochs, wb, srt) in enumerate(cases):
+        r = random_sparse(50, 35, 0.3, seed=seed, integer_values=integer)
+        cfg = TrainConfig(F=F, K=0, epochs=epochs, seed=seed, alpha_u=0.04, alpha_v=0.04,
+                          lambda_u=0.035, lambda_v=0.035)
+        p = train_basic(r, cfg, with_biases=wb, sort_rows_by_count=srt)
+        out.update(triplets_of(r, f"b{s}_"))
+        out[f"b{s}_cfg"] = np.array([F, epochs, seed, int(wb), int(srt)], np.int64)
+        out.update(params_of(p, f"b{s}_", True))
+    out["n_cases"] = len(cases)
+    np.savez_compressed(os.path.join(OUT, "basic.npz"), **out)
+
+
 def main():
     np.set_printoptions(precision=17)
     print("lshmf", lshmf.__version__, "numpy", np.__version__)
+    if "--only-basic" in sys.argv:
+        basic()
+        return
     lsh_small()
     print("lsh_small done")
     sgd_small()
     print("sgd_small done")
     online_small()
     print("online_small done")
+    basic()
+    print("basic done")
     train, test = c1_data()
     c1 = {"train_M": train.M, "train_N": train.N,
           "train_rows": train.entry_rows.astype(np.int16), "train_cols": train.entry_cols.astype(np.int16),

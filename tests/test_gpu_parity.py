@@ -492,3 +492,28 @@ class TestStageApis:
             groups.append(P.coarse_candidates(sigs))
         composed = P.fine_topk(groups, K=3, N=r.N, seed=cfg.seed)
         np.testing.assert_array_equal(composed.entries, table.entries)
+
+
+class TestTrainBasic:
+    """train_basic (CUSGD++ basic MF, factorization.py:476-527): the serial mode must
+    equal the reference bit for bit; the racy (Hogwild) mode must train comparably."""
+
+    def test_serial_bit_exact(self, P):
+        z = load_golden("basic.npz")
+        for s in range(int(z["n_cases"])):
+            pre = f"b{s}_"
+            F, epochs, seed, wb, srt = (int(x) for x in z[pre + "cfg"])
+            r = ratings_of(P, z, pre)
+            cfg = P.TrainConfig(F=F, K=0, epochs=epochs, seed=seed, alpha_u=0.04, alpha_v=0.04,
+                                lambda_u=0.035, lambda_v=0.035)
+            p = P.train_basic(r, cfg, with_biases=bool(wb), sort_rows_by_count=bool(srt))
+            for n in ("b", "b_hat", "U", "V"):
+                assert getattr(p, n).tobytes() == z[f"{pre}{n}"].tobytes(), (s, n)
+
+    def test_racy_mode_trains(self, P, c1):
+        z, tr, te = c1
+        cfg = P.TrainConfig(F=32, K=0, alpha_u=0.04, alpha_v=0.04, lambda_u=0.035, lambda_v=0.035,
+                            epochs=20, seed=0)
+        exact = P.rmse(P.train_basic(tr, cfg, with_biases=True), te, tr)
+        racy = P.rmse(P.train_basic(tr, cfg, with_biases=True, racy_workers=4), te, tr)
+        assert abs(racy - exact) <= REF_TOL_RMSE, (racy, exact)

@@ -213,3 +213,16 @@ class TestOnlineGolden:
         for n, a in (("b", me.b), ("b_hat", me.bhat), ("U", me.U), ("V", me.V), ("W", me.W),
                      ("C", me.C)):
             assert sha(a) == str(z[f"online_ext_{n}_sha"]), n
+
+
+class TestBasicGolden:
+    def test_train_basic(self, orc):
+        z = load_golden("basic.npz")
+        for s in range(int(z["n_cases"])):
+            pre = f"b{s}_"
+            F, epochs, seed, wb, srt = (int(x) for x in z[pre + "cfg"])
+            d, mu = _csr(orc, z, pre)
+            m = orc.train_basic(d, mu, F, epochs, seed, _rates((0.035, 0.035, 0.04, 0.04, 0.002, 0.002)),
+                                (0.02, 0.02, 0.035, 0.035, 0.002, 0.002), bool(wb), bool(srt))
+            for n, a in (("b", m.b), ("b_hat", m.bhat), ("U", m.U), ("V", m.V)):
+                assert a.tobytes() == z[f"{pre}{n}"].tobytes(), (s, n)
