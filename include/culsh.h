@@ -247,6 +247,15 @@ int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows
 /* csc2csr[idx] for every CSC entry (binary search of column j in row i). */
 int culsh_csc_to_csr_map(const CulshData *d, int32_t *csc2csr, void *stream);
 
+/* Online append (replaces the full rebuild of online.py:84-93 extend_ratings):
+ * out segment s = old segment s (s < n_old) followed by add segment s, for
+ * s < n_total; out_ptr (n_total+1).  Applied to the CSC (segments = columns, the
+ * increment's rows sort after the old ones) and to the CSR (segments = rows). */
+int culsh_append_segments(int64_t n_old, int64_t n_total, const int64_t *old_ptr, const int32_t *old_idx,
+                          const double *old_val, const int64_t *add_ptr, const int32_t *add_idx,
+                          const double *add_val, int64_t *out_ptr, int32_t *out_idx, double *out_val,
+                          void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,7 @@ _SIGS = {
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "culsh_predict": [_P(CulshData), _P(CulshModel64), _vp, _vp, _i64, _vp, _vp],
     "culsh_csc_to_csr_map": [_P(CulshData), _vp, _vp],
+    "culsh_append_segments": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {"culsh_last_error": ctypes.c_char_p, "culsh_version": ctypes.c_char_p}
 

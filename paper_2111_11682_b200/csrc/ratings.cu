@@ -31,3 +31,50 @@ extern "C" int culsh_csc_to_csr_map(const CulshData *d, int32_t *csc2csr, void *
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }
+
+namespace culsh {
+
+// out segment s = old segment s (s < n_old) followed by add segment s; out_ptr is
+// (n_total+1).  One warp per segment, coalesced copies.  Used to append an online
+// increment to both index views (new rows / columns sort after the old ones, so
+// every merged segment stays sorted; online.py:84-93 rebuilds instead).
+__global__ void append_segments_kernel(int64_t n_old, int64_t n_total, const int64_t *__restrict__ old_ptr,
+                                       const int32_t *__restrict__ old_idx, const double *__restrict__ old_val,
+                                       const int64_t *__restrict__ add_ptr, const int32_t *__restrict__ add_idx,
+                                       const double *__restrict__ add_val, int64_t *__restrict__ out_ptr,
+                                       int32_t *__restrict__ out_idx, double *__restrict__ out_val) {
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned lane = lane_id();
+    for (int64_t s = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); s <= n_total; s += warps) {
+        const int64_t o_lo = old_ptr[min64(s, n_old)];
+        const int64_t base = o_lo + add_ptr[s];
+        if (lane == 0) out_ptr[s] = base;
+        if (s == n_total) continue;
+        const int64_t o_hi = s < n_old ? old_ptr[s + 1] : o_lo;
+        const int64_t a_lo = add_ptr[s], a_hi = add_ptr[s + 1];
+        for (int64_t x = lane; x < o_hi - o_lo; x += 32) {
+            out_idx[base + x] = old_idx[o_lo + x];
+            out_val[base + x] = old_val[o_lo + x];
+        }
+        const int64_t b2 = base + (o_hi - o_lo);
+        for (int64_t x = lane; x < a_hi - a_lo; x += 32) {
+            out_idx[b2 + x] = add_idx[a_lo + x];
+            out_val[b2 + x] = add_val[a_lo + x];
+        }
+    }
+}
+
+}  // namespace culsh
+
+extern "C" int culsh_append_segments(int64_t n_old, int64_t n_total, const int64_t *old_ptr,
+                                     const int32_t *old_idx, const double *old_val, const int64_t *add_ptr,
+                                     const int32_t *add_idx, const double *add_val, int64_t *out_ptr,
+                                     int32_t *out_idx, double *out_val, void *stream) {
+    CULSH_REQUIRE(n_old >= 0 && n_total >= n_old, "bad segment counts");
+    const int blocks = (int)min64((n_total + 1 + 7) / 8, (int64_t)num_sms() * 16);
+    append_segments_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_old, n_total, old_ptr, old_idx, old_val,
+                                                                      add_ptr, add_idx, add_val, out_ptr,
+                                                                      out_idx, out_val);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}

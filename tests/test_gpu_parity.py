@@ -517,3 +517,33 @@ class TestTrainBasic:
         exact = P.rmse(P.train_basic(tr, cfg, with_biases=True), te, tr)
         racy = P.rmse(P.train_basic(tr, cfg, with_biases=True, racy_workers=4), te, tr)
         assert abs(racy - exact) <= REF_TOL_RMSE, (racy, exact)
+
+
+class TestOnlineSession:
+    """Device-resident online session (append instead of rebuild) == the reference's
+    absorb_increment, bit for bit, on integer-valued data (golden fixtures)."""
+
+    @pytest.mark.parametrize("s", [0, 2])
+    def test_matches_reference(self, P, s):
+        from paper_2111_11682_b200.online_device import OnlineSession
+        from paper_2111_11682_b200 import lsh as L
+        z = load_golden("online_small.npz")
+        pre = f"o{s}_"
+        G, p_, q, e, lseed = (int(x) for x in z[pre + "lsh"])
+        F, K, epochs, seed = (int(x) for x in z[pre + "cfg"])
+        orig = ratings_of(P, z, pre)
+        lc = P.LshConfig(G=G, p=p_, q=q, psi_exponent=e, seed=lseed)
+        cfg = P.TrainConfig(F=F, K=K, epochs=epochs, seed=seed)
+        ent, state, _ = L.simlsh_topk_device(orig.device(), lc, K)
+        tbl = P.NeighborTable(orig.N, K, P._native.to_host(ent)[:orig.N * K].reshape(orig.N, K))
+        params = P.train_full(orig, tbl, cfg)
+        sess = OnlineSession(orig.device(), state, ent, K, params, cfg)
+        bM, bN, nr_, nc_ = (int(x) for x in z[pre + "b_shape"])
+        batch = P.IncrementBatch(bM, bN, nr_, nc_, z[pre + "b_rows"], z[pre + "b_cols"], z[pre + "b_vals"])
+        tm = sess.absorb(batch)
+        assert tm["total"] > 0
+        assert sess.state.acc.tobytes() == z[pre + "ext_acc"].tobytes()
+        pe = sess.to_params()
+        assert pe.neighbors.entries.tobytes() == z[pre + "ext_entries"].tobytes()
+        for n in ("b", "b_hat", "U", "V", "W", "C"):
+            assert getattr(pe, n).tobytes() == z[f"{pre}ext_{n}"].tobytes(), n
