@@ -29,16 +29,8 @@ from . import _native as nat
 from .data import DeviceRatings
 from .factorization import (DeviceModel64, ModelParams, TrainConfig, TrainingDivergedError,
                             _Scratch, _colpass, _plan_full, _rates_struct)
-from .lsh import HashState, LshConfig, _device_row_hashes, _topk_device
-from .online import IncrementBatch
-
-
-def _segments(n_seg: int, seg_of: np.ndarray, idx: np.ndarray, val: np.ndarray):
-    """Host CSR-style grouping of a (small) batch: ptr, idx sorted within segment."""
-    order = np.lexsort((idx, seg_of))
-    ptr = np.zeros(n_seg + 1, np.int64)
-    np.cumsum(np.bincount(seg_of, minlength=n_seg), out=ptr[1:])
-    return ptr, idx[order].astype(np.int32), val[order].astype(np.float64)
+from .lsh import HashState, LshConfig, RowHashes, _ns, _table_alloc, _topk_device
+from .online import IncrementBatch, device_segments
 
 
 def _device_baselines(M: int, N: int, col_ptr, col_rows, col_vals):
@@ -70,6 +62,21 @@ class OnlineSession:
         self.model = DeviceModel64(params)
         self.M, self.N = dev.M, dev.N
 
+    def _extend_row_hashes(self, M_hat: int) -> RowHashes:
+        c = self.lsh
+        rec = (c.q * c.p * _ns(c.G) + 15) // 16 * 16
+        table = _table_alloc(M_hat, c.q, c.p, c.G)
+        old = getattr(self, "_table", None)
+        if old is not None and self._table_rows <= M_hat:
+            table[:self._table_rows * rec] = old[:self._table_rows * rec]
+            lo = self._table_rows
+        else:
+            lo = 0
+        nat.call("culsh_row_hash_table", ctypes.c_uint64(c.seed), c.q, c.p, c.G, lo, M_hat,
+                 nat.ptr(table), nat.stream_ptr())
+        self._table, self._table_rows = table, M_hat
+        return RowHashes(None, c.seed, _table=table, _shape=(M_hat, c.q, c.p, c.G))
+
     def absorb(self, batch: IncrementBatch) -> dict:
         t = nat.torch()
         if batch.base_M != self.M or batch.base_N != self.N:
@@ -86,8 +93,8 @@ class OnlineSession:
         t.cuda.synchronize()
         t0 = time.perf_counter()
         M_hat, N_hat, N_old, M_old = batch.M_hat, batch.N_hat, self.N, self.M
-        # (1) row hashes for the extended row space
-        hashes = _device_row_hashes(M_hat, c.q, c.p, c.G, c.seed)
+        # (1) row hashes for the extended row space: old rows copied, new rows hashed
+        hashes = self._extend_row_hashes(M_hat)
         t0 = mark("row_hashes", t0)
         # (2) incremental hash state (online.py:120-149)
         from .online import update_hashes_incremental
@@ -105,8 +112,11 @@ class OnlineSession:
         t0 = mark("topk_new", t0)
         # (4) extend both index views in HBM (online.py:84-93)
         d = self.dev
-        cptr, crow, cval = _segments(N_hat, batch.cols, batch.rows, batch.values)
-        rptr, rcol, rval = _segments(M_hat, batch.rows, batch.cols, batch.values)
+        br = nat.to_dev(np.asarray(batch.rows, np.int32))
+        bcl = nat.to_dev(np.asarray(batch.cols, np.int32))
+        bv = nat.to_dev(np.asarray(batch.values, np.float64))
+        cptr_d, crow_d, cval_d = device_segments(N_hat, bcl, br, bv)
+        rptr_d, rcol_d, rval_d = device_segments(M_hat, br, bcl, bv)
         nnz_hat = d.nnz + len(batch.rows)
         new_col_ptr = nat.empty((N_hat + 1,), "int64")
         new_col_rows = nat.empty((max(nnz_hat, 1),), "int32")
@@ -114,8 +124,6 @@ class OnlineSession:
         new_row_ptr = nat.empty((M_hat + 1,), "int64")
         new_row_cols = nat.empty((max(nnz_hat, 1),), "int32")
         new_row_vals = nat.empty((max(nnz_hat, 1),), "float64")
-        cptr_d, crow_d, cval_d = nat.to_dev(cptr), nat.to_dev(crow), nat.to_dev(cval)
-        rptr_d, rcol_d, rval_d = nat.to_dev(rptr), nat.to_dev(rcol), nat.to_dev(rval)
         nat.call("culsh_append_segments", N_old, N_hat, nat.ptr(d.col_ptr), nat.ptr(d.col_rows),
                  nat.ptr(d.col_vals), nat.ptr(cptr_d), nat.ptr(crow_d), nat.ptr(cval_d),
                  nat.ptr(new_col_ptr), nat.ptr(new_col_rows), nat.ptr(new_col_vals), nat.stream_ptr())
