@@ -214,6 +214,10 @@ def run_online(args):
     sess = OnlineSession(base.device(), state, ent, K, params, cfg)
     times = []
     Mb, Nb = M0, N0
+    import gc
+    gc.collect()
+    if os.environ.get("CULSH_GC_OFF"):
+        gc.disable()
     for b in range(10):
         sel = bidx == b
         nr_ = dM if b < 9 else M - (M0 + 9 * dM)
@@ -221,6 +225,10 @@ def run_online(args):
         batch = IncrementBatch(Mb, Nb, nr_, nc_, nat.to_host(row[sel]), nat.to_host(col[sel]),
                                nat.to_host(d.col_vals[sel]))
         tm = sess.absorb(batch)
+        ms = torch.cuda.memory_stats()
+        print("batch", b, json.dumps({k: round(v, 4) for k, v in tm.items()}),
+              "retries", ms.get("num_alloc_retries"), "alloc_GB", round(ms.get("allocated_bytes.all.current", 0) / 1e9, 2),
+              "reserved_GB", round(ms.get("reserved_bytes.all.current", 0) / 1e9, 2), file=sys.stderr, flush=True)
         times.append(tm)
         Mb, Nb = Mb + nr_, Nb + nc_
     keys = [k for k in times[0] if k not in ("batch_ratings",)]
@@ -231,6 +239,7 @@ def run_online(args):
             "data": "synthetic (random_sparse distribution generated in HBM, integer stars 1-5)",
             "config": {"workload": "C4 Netflix-shape online: fit on 90% rows x 90% cols, 10 increments of "
                                    "1% new rows + 1% new cols, 1 incremental epoch each (exact fp64)"},
+            "median_s_per_batch": float(np.median([t["total"] for t in times[1:]])),
             "stage_mean_s": mean, "batch_ratings": [t["batch_ratings"] for t in times],
             "reference_measured_s_per_batch": 104.0,
             "reference_note": "SURVEY.md §6 C4: reference absorb_increment on an 8-core Xeon, one 1% batch"}

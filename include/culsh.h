@@ -256,6 +256,17 @@ int culsh_append_segments(int64_t n_old, int64_t n_total, const int64_t *old_ptr
                           const double *add_val, int64_t *out_ptr, int32_t *out_idx, double *out_val,
                           void *stream);
 
+/* csc2csr of the merged views after the two appends above, without a full
+ * rebuild: kept entries shift by add_row_ptr[i], added entries are searched.
+ * d describes the merged ratings; old_col_ptr/old_map the pre-append CSC. */
+int culsh_append_csc2csr(const CulshData *d, int64_t n_old_cols, const int64_t *old_col_ptr,
+                         const int32_t *old_map, const int64_t *add_row_ptr, int64_t M_old,
+                         int32_t *csc2csr, void *stream);
+
+/* out[s] = sum of val[ptr[s]..ptr[s+1]) for s < n (baseline sums, data.py:289-309;
+ * exact, hence order-independent, for integer-valued ratings). */
+int culsh_segment_sums(int64_t n, const int64_t *ptr, const double *val, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

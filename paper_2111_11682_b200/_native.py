@@ -95,6 +95,8 @@ _SIGS = {
     "culsh_predict": [_P(CulshData), _P(CulshModel64), _vp, _vp, _i64, _vp, _vp],
     "culsh_csc_to_csr_map": [_P(CulshData), _vp, _vp],
     "culsh_append_segments": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "culsh_append_csc2csr": [_P(CulshData), _i64, _vp, _vp, _vp, _i64, _vp, _vp],
+    "culsh_segment_sums": [_i64, _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {"culsh_last_error": ctypes.c_char_p, "culsh_version": ctypes.c_char_p}
 

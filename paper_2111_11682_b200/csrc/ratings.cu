@@ -78,3 +78,76 @@ extern "C" int culsh_append_segments(int64_t n_old, int64_t n_total, const int64
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }
+
+namespace culsh {
+
+// After appending an increment to both views: an old CSC entry (i, j) keeps its
+// place inside row i (new entries of row i have columns >= n_old_cols > j) and
+// shifts by the add entries of the rows before i, i.e. by add_row_ptr[i]; the
+// added entries are located by binary search in the merged row view.
+__global__ void append_map_kernel(CulshData d, int64_t n_old_cols, const int64_t *__restrict__ old_col_ptr,
+                                  const int32_t *__restrict__ old_map, const int64_t *__restrict__ add_row_ptr,
+                                  int64_t M_old, int32_t *__restrict__ out) {
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned lane = lane_id();
+    for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < d.N; j += warps) {
+        const int64_t lo = d.col_ptr[j], hi = d.col_ptr[j + 1];
+        int64_t n_keep = 0, o_lo = 0;
+        if (j < n_old_cols) {
+            o_lo = old_col_ptr[j];
+            n_keep = old_col_ptr[j + 1] - o_lo;
+        }
+        for (int64_t x = lane; x < hi - lo; x += 32) {
+            const int32_t i = d.col_rows[lo + x];
+            int64_t pos;
+            if (x < n_keep && i < M_old) {
+                pos = (int64_t)old_map[o_lo + x] + add_row_ptr[i];
+            } else {
+                int64_t a = d.row_ptr[i], b = d.row_ptr[i + 1];
+                while (a < b) {
+                    const int64_t m = (a + b) >> 1;
+                    if (d.row_cols[m] < j) a = m + 1; else b = m;
+                }
+                pos = a;
+            }
+            out[lo + x] = (int32_t)pos;
+        }
+    }
+}
+
+// out[s] = sum of val[ptr[s] .. ptr[s+1]) (warp per segment; exact for integer data).
+__global__ void segment_sums_kernel(int64_t n, const int64_t *__restrict__ ptr, const double *__restrict__ val,
+                                    double *__restrict__ out) {
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned lane = lane_id();
+    for (int64_t s = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); s < n; s += warps) {
+        double acc = 0.0;
+        for (int64_t x = ptr[s] + lane; x < ptr[s + 1]; x += 32) acc += val[x];
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[s] = acc;
+    }
+}
+
+}  // namespace culsh
+
+extern "C" int culsh_append_csc2csr(const CulshData *d, int64_t n_old_cols, const int64_t *old_col_ptr,
+                                    const int32_t *old_map, const int64_t *add_row_ptr, int64_t M_old,
+                                    int32_t *csc2csr, void *stream) {
+    CULSH_REQUIRE(d->nnz < (1LL << 31), "nnz must be < 2^31");
+    CULSH_REQUIRE(n_old_cols >= 0 && n_old_cols <= d->N && M_old >= 0 && M_old <= d->M, "bad old shape");
+    if (d->N <= 0 || d->nnz == 0) return CULSH_OK;
+    const int blocks = (int)min64((d->N + 7) / 8, (int64_t)num_sms() * 16);
+    append_map_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*d, n_old_cols, old_col_ptr, old_map,
+                                                                 add_row_ptr, M_old, csc2csr);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_segment_sums(int64_t n, const int64_t *ptr, const double *val, double *out, void *stream) {
+    CULSH_REQUIRE(n >= 0, "bad segment count");
+    if (n == 0) return CULSH_OK;
+    const int blocks = (int)min64((n + 7) / 8, (int64_t)num_sms() * 16);
+    segment_sums_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n, ptr, val, out);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}

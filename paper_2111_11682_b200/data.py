@@ -218,17 +218,23 @@ class DeviceRatings:
 
     @classmethod
     def from_device(cls, M: int, N: int, col_ptr, col_rows, col_vals, row_ptr, row_cols, row_vals,
-                    mu: float, base_b, base_bhat) -> "DeviceRatings":
-        """Wrap index arrays that already live in HBM (e.g. built by synth.py)."""
+                    mu: float, base_b, base_bhat, csc2csr=None, map_out=None) -> "DeviceRatings":
+        """Wrap index arrays that already live in HBM (e.g. built by synth.py).
+
+        csc2csr: a callable(DeviceRatings) that fills self.csc2csr, default the
+        full binary-search map; map_out: preallocated int32 storage (>= nnz) for it."""
         self = cls.__new__(cls)
         self.M, self.N, self.nnz = int(M), int(N), int(col_rows.numel())
         self.col_ptr, self.col_rows, self.col_vals = col_ptr, col_rows, col_vals
         self.row_ptr, self.row_cols, self.row_vals = row_ptr, row_cols, row_vals
         self.mu, self.base_b, self.base_bhat = float(mu), base_b, base_bhat
-        self.csc2csr = nat.empty((max(self.nnz, 1),), "int32")
+        self.csc2csr = map_out if map_out is not None else nat.empty((max(self.nnz, 1),), "int32")
         self.struct = self._make_struct()
-        nat.call("culsh_csc_to_csr_map", ctypes.byref(self.struct), nat.ptr(self.csc2csr),
-                 nat.stream_ptr())
+        if csc2csr is not None:
+            csc2csr(self)
+        else:
+            nat.call("culsh_csc_to_csr_map", ctypes.byref(self.struct), nat.ptr(self.csc2csr),
+                     nat.stream_ptr())
         return self
 
     def __init__(self, r: SparseRatings, with_baselines: bool = True):

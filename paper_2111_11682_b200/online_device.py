@@ -33,25 +33,55 @@ from .lsh import HashState, LshConfig, RowHashes, _ns, _table_alloc, _topk_devic
 from .online import IncrementBatch, device_segments
 
 
-def _device_baselines(M: int, N: int, col_ptr, col_rows, col_vals):
+def _device_baselines(M: int, N: int, col_ptr, col_vals, row_ptr, row_vals, nnz: int):
+    """compute_baselines (data.py:289-309) from the two views' segment sums."""
     t = nat.torch()
-    nnz = col_rows.numel()
-    mu = float(col_vals.sum().item()) / max(nnz, 1)
+    cs = nat.empty((max(N, 1),), "float64")
+    rs = nat.empty((max(M, 1),), "float64")
+    nat.call("culsh_segment_sums", N, nat.ptr(col_ptr), nat.ptr(col_vals), nat.ptr(cs), nat.stream_ptr())
+    nat.call("culsh_segment_sums", M, nat.ptr(row_ptr), nat.ptr(row_vals), nat.ptr(rs), nat.stream_ptr())
+    cs, rs = cs[:N], rs[:M]
+    mu = float(cs.sum().item()) / max(nnz, 1)
     cnt_c = (col_ptr[1:] - col_ptr[:-1]).to(t.float64)
-    col_of = t.repeat_interleave(t.arange(N, device=col_rows.device), col_ptr[1:] - col_ptr[:-1])
-    cs = t.zeros(N, dtype=t.float64, device=col_rows.device).index_add_(0, col_of, col_vals)
-    rs = t.zeros(M, dtype=t.float64, device=col_rows.device).index_add_(0, col_rows.long(), col_vals)
-    rc = t.bincount(col_rows, minlength=M).to(t.float64)
+    rc = (row_ptr[1:] - row_ptr[:-1]).to(t.float64)
     bb = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
     bh = t.where(cnt_c > 0, cs / cnt_c.clamp(min=1) - mu, t.zeros_like(cs))
     return mu, bb, bh
 
 
+class _Reserve:
+    """A 1-D HBM buffer with spare capacity: view(n) returns its first n elements,
+    regrowing by `grow` (keeping the first `keep` elements) only when n exceeds it,
+    so a stream of increments does not hit cudaMalloc on every batch."""
+
+    def __init__(self, dtype: str, grow: float):
+        self.dtype, self.grow, self.buf = dtype, grow, None
+
+    def view(self, n: int, keep: int = 0):
+        n = max(int(n), 1)
+        if self.buf is None or self.buf.numel() < n:
+            nb = nat.empty((int(n * self.grow) + 1,), self.dtype)
+            if keep and self.buf is not None:
+                nb[:keep] = self.buf[:keep]
+            self.buf = nb
+        return self.buf[:n]
+
+
+_VIEW_FIELDS = (("col_ptr", "int64", "N1"), ("col_rows", "int32", "nnz"), ("col_vals", "float64", "nnz"),
+                ("row_ptr", "int64", "M1"), ("row_cols", "int32", "nnz"), ("row_vals", "float64", "nnz"),
+                ("csc2csr", "int32", "nnz"))
+
+
 class OnlineSession:
-    """HBM-resident state for a stream of increments (paper Alg. 4)."""
+    """HBM-resident state for a stream of increments (paper Alg. 4).
+
+    Memory: the two index views live in a ping-pong pair of reserved buffer sets
+    (the append reads set s and writes set 1-s); the row-hash table and the model
+    arrays grow in place inside reserved buffers.  `reserve` is the headroom factor
+    (default 1.25: ~25% growth before the first reallocation)."""
 
     def __init__(self, dev: DeviceRatings, state: HashState, entries, K: int, params: ModelParams,
-                 config: TrainConfig):
+                 config: TrainConfig, reserve: float = 1.25):
         self.dev = dev
         self.state = state
         self.lsh: LshConfig = state.config
@@ -61,21 +91,37 @@ class OnlineSession:
         self.mu = float(params.mu)
         self.model = DeviceModel64(params)
         self.M, self.N = dev.M, dev.N
+        self.reserve = float(reserve)
+        self._sets = [{f: _Reserve(dt, self.reserve) for f, dt, _ in _VIEW_FIELDS} for _ in range(2)]
+        self._cur = 1                     # the next append writes set 0
+        self._table = _Reserve("uint8", self.reserve)
+        self._table_rows = 0
+        m = self.model
+        self._model = {k: _Reserve(dt, self.reserve) for k, dt in
+                       (("b", "float64"), ("bhat", "float64"), ("U", "float64"), ("V", "float64"),
+                        ("W", "float64"), ("C", "float64"), ("nbr", "int32"))}
+        for k, r in self._model.items():
+            src = getattr(m, k)
+            r.view(src.numel())[:] = src
+            setattr(m, k, r.buf[:src.numel()])
 
     def _extend_row_hashes(self, M_hat: int) -> RowHashes:
         c = self.lsh
         rec = (c.q * c.p * _ns(c.G) + 15) // 16 * 16
-        table = _table_alloc(M_hat, c.q, c.p, c.G)
-        old = getattr(self, "_table", None)
-        if old is not None and self._table_rows <= M_hat:
-            table[:self._table_rows * rec] = old[:self._table_rows * rec]
-            lo = self._table_rows
-        else:
-            lo = 0
+        lo = self._table_rows if self._table_rows <= M_hat else 0
+        table = self._table.view((M_hat + 1) * rec, keep=lo * rec)
+        table[M_hat * rec:].zero_()      # the all-zero padding row
         nat.call("culsh_row_hash_table", ctypes.c_uint64(c.seed), c.q, c.p, c.G, lo, M_hat,
                  nat.ptr(table), nat.stream_ptr())
-        self._table, self._table_rows = table, M_hat
+        self._table_rows = M_hat
         return RowHashes(None, c.seed, _table=table, _shape=(M_hat, c.q, c.p, c.G))
+
+    def _grow_model(self, name: str, n_keep: int, new):
+        r = self._model[name]
+        v = r.view(n_keep + new.numel(), keep=n_keep)
+        if new.numel():
+            v[n_keep:] = new
+        return v
 
     def absorb(self, batch: IncrementBatch) -> dict:
         t = nat.torch()
@@ -102,8 +148,9 @@ class OnlineSession:
         t0 = mark("hash_update", t0)
         # (3) top-K for the new columns (online.py:152-184)
         n_new = N_hat - N_old
-        ent = nat.empty((N_hat * self.K,), "int32")
-        ent[:N_old * self.K] = self.entries[:N_old * self.K]
+        if self.entries.data_ptr() != self._model["nbr"].buf.data_ptr():
+            self._model["nbr"].view(N_old * self.K)[:] = self.entries[:N_old * self.K]
+        ent = self._model["nbr"].view(N_hat * self.K, keep=N_old * self.K)
         if n_new > 0:
             e_new, _ = _topk_device(self.state.device_keys(), c.q, N_hat, c.p * c.G, N_old, n_new,
                                     self.K, c.seed)
@@ -118,23 +165,28 @@ class OnlineSession:
         cptr_d, crow_d, cval_d = device_segments(N_hat, bcl, br, bv)
         rptr_d, rcol_d, rval_d = device_segments(M_hat, br, bcl, bv)
         nnz_hat = d.nnz + len(batch.rows)
-        new_col_ptr = nat.empty((N_hat + 1,), "int64")
-        new_col_rows = nat.empty((max(nnz_hat, 1),), "int32")
-        new_col_vals = nat.empty((max(nnz_hat, 1),), "float64")
-        new_row_ptr = nat.empty((M_hat + 1,), "int64")
-        new_row_cols = nat.empty((max(nnz_hat, 1),), "int32")
-        new_row_vals = nat.empty((max(nnz_hat, 1),), "float64")
+        self._cur ^= 1
+        sizes = {"N1": N_hat + 1, "M1": M_hat + 1, "nnz": nnz_hat}
+        out = {f: self._sets[self._cur][f].view(sizes[k]) for f, _, k in _VIEW_FIELDS}
+        new_col_ptr, new_col_rows, new_col_vals = out["col_ptr"], out["col_rows"], out["col_vals"]
+        new_row_ptr, new_row_cols, new_row_vals = out["row_ptr"], out["row_cols"], out["row_vals"]
         nat.call("culsh_append_segments", N_old, N_hat, nat.ptr(d.col_ptr), nat.ptr(d.col_rows),
                  nat.ptr(d.col_vals), nat.ptr(cptr_d), nat.ptr(crow_d), nat.ptr(cval_d),
                  nat.ptr(new_col_ptr), nat.ptr(new_col_rows), nat.ptr(new_col_vals), nat.stream_ptr())
         nat.call("culsh_append_segments", M_old, M_hat, nat.ptr(d.row_ptr), nat.ptr(d.row_cols),
                  nat.ptr(d.row_vals), nat.ptr(rptr_d), nat.ptr(rcol_d), nat.ptr(rval_d),
                  nat.ptr(new_row_ptr), nat.ptr(new_row_cols), nat.ptr(new_row_vals), nat.stream_ptr())
-        mu_x, bb, bh = _device_baselines(M_hat, N_hat, new_col_ptr, new_col_rows[:nnz_hat],
-                                         new_col_vals[:nnz_hat])
+        mu_x, bb, bh = _device_baselines(M_hat, N_hat, new_col_ptr, new_col_vals, new_row_ptr,
+                                         new_row_vals, nnz_hat)
+
+        def merged_map(nd):
+            nat.call("culsh_append_csc2csr", ctypes.byref(nd.struct), N_old, nat.ptr(d.col_ptr),
+                     nat.ptr(d.csc2csr), nat.ptr(rptr_d), M_old, nat.ptr(nd.csc2csr), nat.stream_ptr())
+
         self.dev = DeviceRatings.from_device(M_hat, N_hat, new_col_ptr, new_col_rows[:nnz_hat],
                                              new_col_vals[:nnz_hat], new_row_ptr, new_row_cols[:nnz_hat],
-                                             new_row_vals[:nnz_hat], mu_x, bb, bh)
+                                             new_row_vals[:nnz_hat], mu_x, bb, bh, csc2csr=merged_map,
+                                             map_out=out["csc2csr"])
         t0 = mark("extend_ratings", t0)
         # (5) extend the model (online.py:187-227), same PCG64 stream as the reference
         cfg = self.config
@@ -146,27 +198,29 @@ class OnlineSession:
         b_new = np.zeros(batch.new_row_count)
         bh_new = np.zeros(batch.new_col_count)
         if len(batch.rows):
-            rs = np.zeros(M_hat)
-            rc = np.zeros(M_hat)
-            np.add.at(rs, batch.rows, batch.values)
-            np.add.at(rc, batch.rows, 1.0)
-            sel = rc[M_old:] > 0
-            b_new[sel] = rs[M_old:][sel] / rc[M_old:][sel] - self.mu
-            cs = np.zeros(N_hat)
-            cc = np.zeros(N_hat)
-            np.add.at(cs, batch.cols, batch.values)
-            np.add.at(cc, batch.cols, 1.0)
-            sel = cc[N_old:] > 0
-            bh_new[sel] = cs[N_old:][sel] / cc[N_old:][sel] - self.mu
+            # bincount sums in entry order, as np.add.at does (online.py:205-215), over
+            # the entries of new rows / new columns only
+            sel_r = batch.rows >= M_old
+            r_new = batch.rows[sel_r] - M_old
+            rs = np.bincount(r_new, weights=batch.values[sel_r], minlength=batch.new_row_count)
+            rc = np.bincount(r_new, minlength=batch.new_row_count).astype(np.float64)
+            sel = rc > 0
+            b_new[sel] = rs[sel] / rc[sel] - self.mu
+            sel_c = batch.cols >= N_old
+            c_new = batch.cols[sel_c] - N_old
+            cs = np.bincount(c_new, weights=batch.values[sel_c], minlength=batch.new_col_count)
+            cc = np.bincount(c_new, minlength=batch.new_col_count).astype(np.float64)
+            sel = cc > 0
+            bh_new[sel] = cs[sel] / cc[sel] - self.mu
         m = self.model
         K = self.K
-        m.b = t.cat([m.b[:M_old], nat.to_dev(b_new)])
-        m.bhat = t.cat([m.bhat[:N_old], nat.to_dev(bh_new)])
-        m.U = t.cat([m.U[:M_old * F], nat.to_dev(U_new.reshape(-1))])
-        m.V = t.cat([m.V[:N_old * F], nat.to_dev(V_new.reshape(-1))])
+        m.b = self._grow_model("b", M_old, nat.to_dev(b_new))
+        m.bhat = self._grow_model("bhat", N_old, nat.to_dev(bh_new))
+        m.U = self._grow_model("U", M_old * F, nat.to_dev(U_new.reshape(-1)))
+        m.V = self._grow_model("V", N_old * F, nat.to_dev(V_new.reshape(-1)))
         if K:
-            m.W = t.cat([m.W[:N_old * K], nat.zeros((n_new * K,), "float64")])
-            m.C = t.cat([m.C[:N_old * K], nat.zeros((n_new * K,), "float64")])
+            m.W = self._grow_model("W", N_old * K, nat.zeros((n_new * K,), "float64"))
+            m.C = self._grow_model("C", N_old * K, nat.zeros((n_new * K,), "float64"))
         m.nbr = self.entries
         m.struct = nat.CulshModel64(m.mu, nat.ptr(m.b), nat.ptr(m.bhat), nat.ptr(m.U), nat.ptr(m.V),
                                     nat.ptr(m.W), nat.ptr(m.C), nat.ptr(m.nbr), F, K)

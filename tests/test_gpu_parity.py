@@ -547,3 +547,11 @@ class TestOnlineSession:
         assert pe.neighbors.entries.tobytes() == z[pre + "ext_entries"].tobytes()
         for n in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(pe, n).tobytes() == z[f"{pre}ext_{n}"].tobytes(), n
+        # the appended index views, csc2csr map and baselines == a from-scratch build
+        nat = P._native
+        full = P.extend_ratings(orig, batch).device()
+        d = sess.dev
+        for a in ("col_ptr", "col_rows", "col_vals", "row_ptr", "row_cols", "row_vals", "csc2csr",
+                  "base_b", "base_bhat"):
+            assert nat.to_host(getattr(d, a)).tobytes() == nat.to_host(getattr(full, a)).tobytes(), a
+        assert d.mu == full.mu
