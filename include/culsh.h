@@ -223,6 +223,27 @@ int culsh_sgd_hogwild_epoch(int64_t N_list, const int64_t *col_ptr, const int64_
                             int *ticket,
                             double *loss_out, int *status, void *stream);
 
+/* Packed per-epoch rating stream for the Hogwild kernel (the form e2e ships over
+ * PCIe every epoch): packed[idx] = row (bits 0-26) | value code into lut (bits
+ * 27-30) | has-explicit-neighbour (bit 31); cmask holds the MW mask words of the
+ * ratings with bit 31 set only, column j's from mptr[j].  Pass 1 (packed ==
+ * NULL): mcount[j] = number of such ratings in column j; the caller prefix-sums
+ * it into mptr (N+1).  Pass 2 fills packed and cmask.  *status |= 4 if a value is
+ * not in lut (1..16 fp32 values) or a row index needs more than 27 bits.  Same
+ * information as the (rows, vals, mask) triple of culsh_sgd_hogwild_epoch. */
+int culsh_pack_stream(int64_t N, const int64_t *col_ptr, const int32_t *rows, const float *vals,
+                      const uint32_t *mask, int MW, const float *lut, int n_lut, uint32_t *packed,
+                      int64_t *mcount, const int64_t *mptr, uint32_t *cmask, int *status, void *stream);
+
+/* culsh_sgd_hogwild_epoch over the packed stream (whole columns, warp per
+ * column; flags bit 1 only -- no rotation, no sub-warp kernel).  Identical
+ * updates to the wide-stream kernel on the same data. */
+int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const uint32_t *packed,
+                                   const float *lut, const int64_t *mptr, const uint32_t *cmask,
+                                   const int64_t *resid_ptr, const float *resid, const int32_t *col_order,
+                                   CulshModel32 *m, const CulshRates *r, int flags, int max_warps,
+                                   int *ticket, double *loss_out, int *status, void *stream);
+
 /* --------------------------------------------------------------- eval --- */
 
 /* Per-test-triplet squared error (fp64, exact _predict_one order) and the RMSE.

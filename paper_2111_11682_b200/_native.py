@@ -89,6 +89,9 @@ _SIGS = {
     "culsh_explicit_stream": [_P(CulshData), _f64, _vp, _i32, _vp, _vp, _vp, _vp, _vp],
     "culsh_sgd_hogwild_epoch": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
                                 _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
+    "culsh_pack_stream": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "culsh_sgd_hogwild_epoch_packed": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
+                                       _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
     "culsh_rmse": [_P(CulshData), _P(CulshModel64), _vp, _vp, _vp, _i64, _i32, _f64, _f64, _f64,
                    _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],

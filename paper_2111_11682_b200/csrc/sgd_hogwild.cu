@@ -37,6 +37,24 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Paired fp32 arithmetic (sm_100 FFMA2 / FMUL2: two IEEE fp32 ops, each rounded
+// exactly like FFMA / FMUL, in one instruction).
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(uint64_t x) { return __uint_as_float((uint32_t)x); }
+__device__ __forceinline__ float hi2(uint64_t x) { return __uint_as_float((uint32_t)(x >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
 template <int FV>
 __device__ __forceinline__ void cp_async_row(float *dst, const float *src) {
     if constexpr (FV % 4 == 0) {
@@ -130,7 +148,13 @@ constexpr int hw_smem_per_warp() {
 // cp.async fills kHwDepth-1 updates ahead, so the HBM/L2 latency of the row
 // gather is off the update's critical path.  Each lane copies and later reads
 // only its own FV floats of every row, so the ring needs no warp barrier.
-template <int FV, int KPL, bool ATOMIC>
+//
+// PACK: the rating stream is the packed form built by culsh_pack_stream -- one
+// u32 per rating {row: bits 0-26, value code: bits 27-30 (into lut), has-mask:
+// bit 31} and mask words only for ratings with a set bit (column base mptr[j]),
+// 4 + MW*4*(fraction with explicit neighbours) bytes per rating instead of
+// 8 + 4*MW.  Whole columns in CSC order only (no seg, no rotation).
+template <int FV, int KPL, bool ATOMIC, bool PACK>
 __global__ void __launch_bounds__(kHwWarps * 32, 4)
 hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__restrict__ seg,
                const int32_t *__restrict__ rows, const float *__restrict__ vals,
@@ -139,7 +163,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                float *__restrict__ Bv, float *__restrict__ BHv, float *__restrict__ U,
                float *__restrict__ V, float *__restrict__ W, float *__restrict__ C, int F, int K,
                HwCoef R, int flags, int *__restrict__ ticket, double *__restrict__ loss,
-               int *__restrict__ status) {
+               int *__restrict__ status, const float *__restrict__ lut, const int64_t *__restrict__ mptr) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     constexpr int P = kHwDepth;
     const unsigned lane = lane_id();
@@ -151,9 +175,15 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
     float *s_bring = s_ring + P * 32 * FV;
     float *my_ring = s_ring + lane * FV;
 
-    const bool fl = (int)(lane * FV) < F;   // lane owns factor slots
+    const bool fl = FV > 1 || (int)lane < F;   // lane owns factor slots (F == 32*FV when FV > 1)
     const unsigned lt_mask = (1u << lane) - 1u;
     const float invK = K > 0 ? rsqrtf((float)K) : 0.f;
+    float kgc[KPL];   // gc * |N|^-1/2 with |N| = K (no explicit neighbour), 0 for slots >= K
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) kgc[q] = (int)lane + 32 * q < K ? R.gc * invK : 0.f;
+    s_meta[lane] = make_int4(0, 0, 0, 0);   // every row index the prefetch can see is valid
+    s_meta[lane + 32] = make_int4(0, 0, 0, 0);
+    __syncwarp();
     double col_loss = 0.0;
     int bad = 0;
     const float *Ulane = U + lane * FV;
@@ -186,11 +216,12 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         const int64_t hi = seg ? seg[2 * j + 1] : col_ptr[j + 1];
         const int n = (int)(hi - lo);
         const float *rcol = resid + resid_ptr[j];
+        int64_t mrun = PACK ? mptr[j] : 0;   // packed: next compact mask slot of this column
         // Visiting order: the column's entries rotated to start at position `rot`
         // (a per-column hash when `rotate` is set).  Warps then sweep the rows out of
         // phase with each other instead of in lock-step, which keeps concurrent
         // Hogwild writes to the same u_i rare.
-        const int rot = ((flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
+        const int rot = (!PACK && (flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
         int rrel2 = 0;   // residual offset (relative to the column base) at position lo
         if (lo > c_lo) {   // DSGD block: skip the residuals of the column's earlier row blocks
             int skip = 0;
@@ -217,10 +248,27 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             const bool seg2 = pos >= n;
             if (seg2) pos -= n;
             const int64_t e = lo + pos;
-            const int ri = have ? rows[e] : 0;
-            const float rv = have ? vals[e] : 0.f;
-            const uint32_t m0 = have ? mask[e * KPL] : 0u;
-            const uint32_t m1 = (KPL == 2 && have) ? mask[e * KPL + 1] : 0u;
+            int ri;
+            float rv;
+            uint32_t m0 = 0u, m1 = 0u;
+            if constexpr (PACK) {
+                const uint32_t wd = have ? __ldg(reinterpret_cast<const uint32_t *>(rows) + e) : 0u;
+                ri = (int)(wd & 0x07FFFFFFu);
+                rv = __ldg(lut + ((wd >> 27) & 15u));
+                const bool hm = (wd >> 31) != 0u;
+                const unsigned bal = __ballot_sync(0xffffffffu, hm);
+                if (hm) {
+                    const int64_t mi = mrun + __popc(bal & lt_mask);
+                    m0 = mask[mi * KPL];
+                    if constexpr (KPL == 2) m1 = mask[mi * KPL + 1];
+                }
+                mrun += __popc(bal);
+            } else {
+                ri = have ? rows[e] : 0;
+                rv = have ? vals[e] : 0.f;
+                m0 = have ? mask[e * KPL] : 0u;
+                m1 = (KPL == 2 && have) ? mask[e * KPL + 1] : 0u;
+            }
             const int pc = __popc(m0) + __popc(m1);
             int roff = 0;
             if (__any_sync(0xffffffffu, pc != 0)) {
@@ -266,10 +314,12 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             const int cnt = min(32, n - base);
             for (int k = 0; k < cnt; ++k) {
                 const int tt = base + k;
-                // prefetch P-1 ahead; past the end, re-fetch the last row into an unused slot
+                // prefetch P-1 ahead.  Past the column's end the slot holds a padding (0) or an
+                // older row of this launch (s_meta is zeroed at entry): always a valid row, the
+                // copy lands in a ring slot nobody reads before the column's final wait.
                 {
                     const int tp = tt + P - 1;
-                    const int ip = s_meta[min(tp, n - 1) & 63].x;
+                    const int ip = s_meta[tp & 63].x;
                     float *dst = my_ring + (tp % P) * 32 * FV;
                     if (fl) cp_async_row<FV>(dst, Ulane + (size_t)(unsigned)ip * (unsigned)F);
                     if (lane == 0) cp_async_bytes4(s_bring + (tp % P), Bv + ip);
@@ -284,9 +334,18 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                 float u[FV];
                 load_row<FV>(my_ring + (tt % P) * 32 * FV, u);
                 const float bi = lane == 0 ? s_bring[tt % P] : 0.f;
-                float part = bi;
+                float part;
+                if constexpr (FV % 2 == 0) {
+                    // paired fp32 (FFMA2): even / odd factor partial sums, folded once
+                    uint64_t acc = pack2(bi, 0.f);
 #pragma unroll
-                for (int x = 0; x < FV; ++x) part = fmaf(u[x], fl ? v[x] : 0.f, part);
+                    for (int x = 0; x < FV; x += 2) acc = ffma2(pack2(u[x], u[x + 1]), pack2(v[x], v[x + 1]), acc);
+                    part = lo2(acc) + hi2(acc);
+                } else {
+                    part = bi;
+#pragma unroll
+                    for (int x = 0; x < FV; ++x) part = fmaf(u[x], fl ? v[x] : 0.f, part);
+                }
                 const bool anyex = (m0 | m1) != 0u;   // warp-uniform
                 float inv_r = 0.f, inv_n = invK;
                 float rs[KPL];
@@ -322,11 +381,24 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                     // add the update instead of storing the new value: a concurrent update of the
                     // same row by another warp is then never lost (only computed from a stale u_i)
                     float dlt[FV];
+                    if constexpr (FV % 2 == 0) {
+                        const uint64_t ngu2 = pack2(ngu, ngu), geu2 = pack2(geu, geu);
+                        const uint64_t av2 = pack2(R.av, R.av), gev2 = pack2(gev, gev);
 #pragma unroll
-                    for (int x = 0; x < FV; ++x) {
-                        const float uo = u[x];
-                        dlt[x] = fmaf(ngu, uo, geu * v[x]);
-                        v[x] = fmaf(R.av, v[x], gev * uo);
+                        for (int x = 0; x < FV; x += 2) {
+                            const uint64_t uo = pack2(u[x], u[x + 1]), vo = pack2(v[x], v[x + 1]);
+                            const uint64_t d = ffma2(ngu2, uo, fmul2(geu2, vo));
+                            const uint64_t vn = ffma2(av2, vo, fmul2(gev2, uo));
+                            dlt[x] = lo2(d); dlt[x + 1] = hi2(d);
+                            v[x] = lo2(vn); v[x + 1] = hi2(vn);
+                        }
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < FV; ++x) {
+                            const float uo = u[x];
+                            dlt[x] = fmaf(ngu, uo, geu * v[x]);
+                            v[x] = fmaf(R.av, v[x], gev * uo);
+                        }
                     }
                     if (fl) {
                         if constexpr (FV % 4 == 0) {
@@ -352,13 +424,19 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                     if (lane == 0) Bv[i] = fmaf(R.ab, bi, R.gb * e);
                 }
                 bh = fmaf(R.abh, bh, R.gbh * e);
-                const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
+                if (!anyex) {
+                    // no explicit neighbour: only the implicit weights move (kgc = 0 off K)
 #pragma unroll
-                for (int q = 0; q < KPL; ++q) {
-                    const float wn = fmaf(R.aw, w[q], gwe * rs[q]);
-                    const float cn = fmaf(R.ac, c[q], gce);
-                    w[q] = (kin[q] && ex[q]) ? wn : w[q];
-                    c[q] = (kin[q] && !ex[q]) ? cn : c[q];
+                    for (int q = 0; q < KPL; ++q) c[q] = fmaf(R.ac, c[q], kgc[q] * e);
+                } else {
+                    const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        const float wn = fmaf(R.aw, w[q], gwe * rs[q]);
+                        const float cn = fmaf(R.ac, c[q], gce);
+                        w[q] = (kin[q] && ex[q]) ? wn : w[q];
+                        c[q] = (kin[q] && !ex[q]) ? cn : c[q];
+                    }
                 }
             }
         }
@@ -785,22 +863,23 @@ explicit_stream_kernel(CulshData d, double mu, const int32_t *__restrict__ nbr, 
     }
 }
 
-template <int FV, int KPL>
+template <int FV, int KPL, bool PACK = false>
 int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const int32_t *rows, const float *vals,
                    const uint32_t *mask, const int64_t *resid_ptr, const float *resid,
                    const int32_t *col_order, CulshModel32 *m, const HwCoef &R, int flags, int max_warps,
                    int *ticket,
-                   double *loss, int *status, cudaStream_t st) {
+                   double *loss, int *status, cudaStream_t st, const float *lut = nullptr,
+                   const int64_t *mptr = nullptr) {
     const int threads = kHwWarps * 32;
     const size_t smem = (size_t)kHwWarps * hw_smem_per_warp<FV, KPL>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, true, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, false, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
     int occ = 0;
-    auto kern = (flags & 2) ? hogwild_kernel<FV, KPL, true> : hogwild_kernel<FV, KPL, false>;
+    auto kern = (flags & 2) ? hogwild_kernel<FV, KPL, true, PACK> : hogwild_kernel<FV, KPL, false, PACK>;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     if (occ < 1) occ = 1;
     int64_t blocks = (int64_t)num_sms() * occ;
@@ -811,8 +890,58 @@ int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const 
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, threads, smem, st>>>(
         N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m->mu, m->b, m->bhat, m->U, m->V, m->W,
-        m->C, m->F, m->K, R, flags, ticket, loss, status);
+        m->C, m->F, m->K, R, flags, ticket, loss, status, lut, mptr);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
+}
+
+// ---- packed rating stream (see hogwild_kernel PACK) ---------------------------
+//
+// Warp per column, entries in CSC order.  Pass 1 (packed == nullptr): per-column
+// count of ratings whose mask is non-zero.  Pass 2: packed words + compact mask
+// words at mptr[j] in entry order.  A value missing from lut or a row >= 2^27
+// sets *status |= 4 (the caller then keeps the wide stream).
+__global__ void pack_stream_kernel(int64_t N, const int64_t *__restrict__ col_ptr,
+                                   const int32_t *__restrict__ rows, const float *__restrict__ vals,
+                                   const uint32_t *__restrict__ mask, int MW, const float *__restrict__ lut,
+                                   int n_lut, uint32_t *__restrict__ packed, int64_t *__restrict__ mcount,
+                                   const int64_t *__restrict__ mptr, uint32_t *__restrict__ cmask,
+                                   int *__restrict__ status) {
+    const unsigned lane = lane_id();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < N; j += warps) {
+        const int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
+        int64_t run = packed ? mptr[j] : 0;
+        int bad = 0;
+        for (int64_t b = lo; b < hi; b += 32) {
+            const int64_t e = b + lane;
+            const bool have = e < hi;
+            uint32_t m0 = 0u, m1 = 0u;
+            if (have) {
+                m0 = mask[e * MW];
+                if (MW == 2) m1 = mask[e * MW + 1];
+            }
+            const bool hm = (m0 | m1) != 0u;
+            const unsigned bal = __ballot_sync(0xffffffffu, hm);
+            if (packed && have) {
+                const float v = vals[e];
+                int code = -1;
+                for (int c = 0; c < n_lut; ++c)
+                    if (lut[c] == v) { code = c; break; }
+                const int32_t r = rows[e];
+                if (code < 0 || r < 0 || r >= (1 << 27)) bad = 1;
+                packed[e] = ((uint32_t)r & 0x07FFFFFFu) | ((uint32_t)(code & 15) << 27) | (hm ? 0x80000000u : 0u);
+                if (hm) {
+                    const int64_t mi = run + __popc(bal & lt_mask);
+                    cmask[mi * MW] = m0;
+                    if (MW == 2) cmask[mi * MW + 1] = m1;
+                }
+            }
+            run += __popc(bal);
+        }
+        if (!packed && lane == 0) mcount[j] = run;
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 4);
+    }
 }
 
 }  // namespace culsh
@@ -873,4 +1002,49 @@ extern "C" int culsh_sgd_hogwild_epoch(int64_t N, const int64_t *col_ptr, const 
     if (F == 128) return HW(4);
     return HW(8);
 #undef HW
+}
+
+extern "C" int culsh_pack_stream(int64_t N, const int64_t *col_ptr, const int32_t *rows, const float *vals,
+                                 const uint32_t *mask, int MW, const float *lut, int n_lut, uint32_t *packed,
+                                 int64_t *mcount, const int64_t *mptr, uint32_t *cmask, int *status,
+                                 void *stream) {
+    CULSH_REQUIRE(MW == 1 || MW == 2, "MW must be 1 or 2");
+    CULSH_REQUIRE(n_lut >= 1 && n_lut <= 16, "the value table holds 1..16 values");
+    CULSH_REQUIRE(packed ? (mptr != nullptr && cmask != nullptr) : mcount != nullptr,
+                  "pass 1 needs mcount; pass 2 needs mptr and cmask");
+    if (N <= 0) return CULSH_OK;
+    const int64_t blocks = min64((N + 7) / 8, (int64_t)num_sms() * 16);
+    pack_stream_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(N, col_ptr, rows, vals, mask, MW, lut,
+                                                                           n_lut, packed, mcount, mptr, cmask,
+                                                                           status);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const uint32_t *packed,
+                                              const float *lut, const int64_t *mptr, const uint32_t *cmask,
+                                              const int64_t *resid_ptr, const float *resid,
+                                              const int32_t *col_order, CulshModel32 *m, const CulshRates *r,
+                                              int flags, int max_warps, int *ticket, double *loss_out,
+                                              int *status, void *stream) {
+    const int F = m->F, K = m->K;
+    CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
+    CULSH_REQUIRE((F >= 1 && F <= 32) || F == 64 || F == 128 || F == 256,
+                  "Hogwild mode needs F <= 32 or F in {64, 128, 256}");
+    CULSH_REQUIRE((flags & 5) == 0, "the packed stream supports neither rotation nor the sub-warp kernel");
+    if (N_list <= 0) return CULSH_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    HwCoef R{(float)r->gb, (float)r->gbh, (float)r->gu, (float)r->gv, (float)r->gw, (float)r->gc,
+             (float)(1.0 - r->gb * r->lb), (float)(1.0 - r->gbh * r->lbh), (float)(1.0 - r->gu * r->lu),
+             (float)(1.0 - r->gv * r->lv), (float)(1.0 - r->gw * r->lw), (float)(1.0 - r->gc * r->lc)};
+    const bool k2 = K > 32;
+    const int32_t *rows = reinterpret_cast<const int32_t *>(packed);
+#define HWP(FVv) (k2 ? launch_hogwild<FVv, 2, true>(N_list, col_ptr, nullptr, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr) \
+                     : launch_hogwild<FVv, 1, true>(N_list, col_ptr, nullptr, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr))
+    if (F <= 32) return HWP(1);
+    if (F == 64) return HWP(2);
+    if (F == 128) return HWP(4);
+    return HWP(8);
+#undef HWP
 }

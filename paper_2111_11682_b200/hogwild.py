@@ -62,7 +62,8 @@ class HogwildTrainer:
 
     def __init__(self, ratings, neighbors: NeighborTable | None, config: TrainConfig,
                  dev=None, params: ModelParams | None = None, rotate: bool = False,
-                 max_warps: int | None = None, atomic_rows: bool = True, subwarp: bool = False):
+                 max_warps: int | None = None, atomic_rows: bool = True, subwarp: bool = False,
+                 packed: bool = True):
         config.validate()
         self.rotate = rotate
         self.atomic_rows = atomic_rows
@@ -110,6 +111,37 @@ class HogwildTrainer:
         self.ticket = nat.zeros((1,), "int32")
         self.status = nat.zeros((1,), "int32")
         self.loss = nat.zeros((1,), "float64")
+        self.packed = self._build_packed() if (packed and not rotate and not subwarp) else None
+
+    def _build_packed(self):
+        """Packed rating stream (culsh_pack_stream): 4 B per rating + mask words of the
+        ratings with explicit neighbours only.  None when the data do not fit it
+        (more than 16 distinct values or M >= 2^27); the wide stream is used then."""
+        from .lsh import _value_classes
+        d = self.dev
+        t = nat.torch()
+        if d.nnz == 0 or d.M >= (1 << 27):
+            return None
+        classes = _value_classes(d)
+        if classes is None:
+            return None
+        lut = nat.to_dev(np.unique(np.asarray(classes, np.float32)), np.float32)
+        mcount = nat.zeros((max(d.N, 1),), "int64")
+        mptr = nat.zeros((d.N + 1,), "int64")
+        st = nat.zeros((1,), "int32")
+        nat.call("culsh_pack_stream", d.N, nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(self.vals32),
+                 nat.ptr(self.mask), self.MW, nat.ptr(lut), int(lut.numel()), None, nat.ptr(mcount), None,
+                 None, nat.ptr(st), nat.stream_ptr())
+        t.cumsum(mcount[:d.N], 0, out=mptr[1:])
+        n_m = int(mptr[-1].item())
+        words = nat.zeros((max(d.nnz, 1),), "int32")
+        cmask = nat.zeros((max(n_m * self.MW, 1),), "int32")
+        nat.call("culsh_pack_stream", d.N, nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(self.vals32),
+                 nat.ptr(self.mask), self.MW, nat.ptr(lut), int(lut.numel()), nat.ptr(words), None,
+                 nat.ptr(mptr), nat.ptr(cmask), nat.ptr(st), nat.stream_ptr())
+        if int(st.item()):
+            return None
+        return {"words": words, "cmask": cmask, "mptr": mptr, "lut": lut}
 
     def bytes_per_update(self) -> float:
         """Algorithmic HBM bytes per rating update (SURVEY §8(d) B_upd) + per-column share."""
@@ -127,6 +159,10 @@ class HogwildTrainer:
         d = self.dev
         order = self.col_order if col_order is None else col_order
         n = d.N if n_cols is None else n_cols
+        if self.packed is not None and seg is None:
+            pk = self.packed
+            self._launch_packed(n, pk["words"], pk["cmask"], self.resid, order, rates, self.loss)
+            return
         nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(d.col_rows),
                  nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
                  nat.ptr(self.resid), nat.ptr(order), ctypes.byref(self.model.struct),
@@ -135,26 +171,59 @@ class HogwildTrainer:
                  nat.ptr(self.loss),
                  nat.ptr(self.status), nat.stream_ptr())
 
+    def _launch_packed(self, n, words, cmask, resid, order, rates, loss) -> None:
+        pk, d = self.packed, self.dev
+        nat.call("culsh_sgd_hogwild_epoch_packed", n, nat.ptr(d.col_ptr), nat.ptr(words), nat.ptr(pk["lut"]),
+                 nat.ptr(pk["mptr"]), nat.ptr(cmask), nat.ptr(self.resid_ptr), nat.ptr(resid), nat.ptr(order),
+                 ctypes.byref(self.model.struct), ctypes.byref(rates), 2 if self.atomic_rows else 0,
+                 int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss), nat.ptr(self.status),
+                 nat.stream_ptr())
+
     def epoch(self, t_epoch: int) -> None:
         self.launch_epoch(t_epoch)
         if int(self.status.item()):
             raise TrainingDivergedError(epoch=t_epoch)
 
     def pinned_stream(self) -> dict:
-        """Pinned host copy of the per-epoch rating stream (CSC rows, fp32 values, masks)."""
-        return {"rows": self.dev.col_rows.cpu().pin_memory(),
-                "vals": self.vals32.cpu().pin_memory(),
-                "mask": self.mask.cpu().pin_memory()}
+        """Pinned host copy of the per-epoch rating stream: every per-rating array the
+        epoch reads -- the packed words, the compact explicit masks and residuals when
+        the packed stream is in use, else CSC rows, fp32 values, masks and residuals."""
+        if self.packed is not None:
+            src = {"words": self.packed["words"], "cmask": self.packed["cmask"], "resid": self.resid}
+        else:
+            src = {"rows": self.dev.col_rows, "vals": self.vals32, "mask": self.mask, "resid": self.resid}
+        return {k: v.cpu().pin_memory() for k, v in src.items()}
+
+    def _stream_buffers(self):
+        if self.packed is not None:
+            return (self.packed["words"], self.packed["cmask"], self.resid)
+        return (self.dev.col_rows, self.vals32, self.mask, self.resid)
+
+    def _launch_stream(self, bufs, t_epoch, loss) -> None:
+        c = self.config
+        rates = _rates_struct(c.rates_at(t_epoch), c.regs)
+        d = self.dev
+        if self.packed is not None:
+            words, cmask, resid = bufs
+            self._launch_packed(d.N, words, cmask, resid, self.col_order, rates, loss)
+            return
+        rows_b, vals_b, mask_b, resid_b = bufs
+        nat.call("culsh_sgd_hogwild_epoch", d.N, nat.ptr(d.col_ptr), None, nat.ptr(rows_b),
+                 nat.ptr(vals_b), nat.ptr(mask_b), nat.ptr(self.resid_ptr), nat.ptr(resid_b),
+                 nat.ptr(self.col_order), ctypes.byref(self.model.struct), ctypes.byref(rates),
+                 int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0),
+                 int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss),
+                 nat.ptr(self.status), nat.stream_ptr())
 
     def epoch_from_host(self, host: dict, t_epoch: int):
         """One epoch whose rating stream comes from pinned host memory: H2D copy of
         the stream, the epoch kernel, D2H of the epoch's summed squared error.
         Returns (sum of e^2 over the epoch, h2d bytes, d2h bytes)."""
-        self.dev.col_rows.copy_(host["rows"], non_blocking=True)
-        self.vals32.copy_(host["vals"], non_blocking=True)
-        self.mask.copy_(host["mask"], non_blocking=True)
+        bufs = self._stream_buffers()
+        for dst, src in zip(bufs, host.values()):
+            dst.copy_(src, non_blocking=True)
         self.loss.zero_()
-        self.launch_epoch(t_epoch)
+        self._launch_stream(bufs, t_epoch, self.loss)
         loss = float(self.loss.item())
         if int(self.status.item()):
             raise TrainingDivergedError(epoch=t_epoch)
@@ -169,9 +238,9 @@ class HogwildTrainer:
         t = nat.torch()
         comp = t.cuda.current_stream()
         cstream = t.cuda.Stream()
-        bufs = [(self.dev.col_rows, self.vals32, self.mask),
-                (t.empty_like(self.dev.col_rows), t.empty_like(self.vals32), t.empty_like(self.mask))]
-        src = (host["rows"], host["vals"], host["mask"])
+        first = self._stream_buffers()
+        bufs = [first, tuple(t.empty_like(x) for x in first)]
+        src = tuple(host.values())
         copied = [t.cuda.Event(), t.cuda.Event()]
         used = [t.cuda.Event(), t.cuda.Event()]
         loss_dev = t.zeros(n_epochs, dtype=t.float64, device=self.loss.device)
@@ -192,16 +261,7 @@ class HogwildTrainer:
             comp.wait_event(copied[b])
             if e + 1 < n_epochs:
                 fill(1 - b)
-            rows_b, vals_b, mask_b = bufs[b]
-            c = self.config
-            rates = _rates_struct(c.rates_at(t_start + e), c.regs)
-            d = self.dev
-            nat.call("culsh_sgd_hogwild_epoch", d.N, nat.ptr(d.col_ptr), None, nat.ptr(rows_b),
-                     nat.ptr(vals_b), nat.ptr(mask_b), nat.ptr(self.resid_ptr), nat.ptr(self.resid),
-                     nat.ptr(self.col_order), ctypes.byref(self.model.struct), ctypes.byref(rates),
-                     int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0),
-                     int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss_dev[e:]),
-                     nat.ptr(self.status), nat.stream_ptr())
+            self._launch_stream(bufs[b], t_start + e, loss_dev[e:])
             used[b].record(comp)
             loss_host[e:e + 1].copy_(loss_dev[e:e + 1], non_blocking=True)
         comp.synchronize()

@@ -379,6 +379,77 @@ class TestHogwild:
         assert abs(rm_exact - rm_hog) <= REF_TOL_RMSE, (rm_exact, rm_hog)
 
 
+class TestPackedStream:
+    """The packed per-epoch stream (culsh_pack_stream) carries exactly the wide
+    stream's information, and the packed kernel makes exactly the wide kernel's
+    updates (columns run one launch at a time, so both are deterministic)."""
+
+    def _problem(self, P, K, nvals=5, M=700, N=90, dens=0.08):
+        rng = np.random.default_rng(3)
+        mask = rng.random((M, N)) < dens
+        rows, cols = np.nonzero(mask)
+        vals = rng.integers(1, nvals + 1, len(rows)).astype(float) * 0.5
+        r = P.SparseRatings(M, N, rows, cols, vals)
+        tbl, _ = P.simlsh_topk(r, P.LshConfig(q=20), K)
+        cfg = P.TrainConfig(F=64, K=K, epochs=2, seed=0)
+        return r, tbl, cfg
+
+    @pytest.mark.parametrize("K", [16, 40])
+    def test_decode_equals_wide(self, P, K):
+        from paper_2111_11682_b200 import _native as nat
+        from paper_2111_11682_b200.hogwild import HogwildTrainer
+        r, tbl, cfg = self._problem(P, K)
+        tr = HogwildTrainer(r, tbl, cfg)
+        pk = tr.packed
+        assert pk is not None
+        w = nat.to_host(pk["words"]).view(np.uint32)[:r.nnz]
+        lut = nat.to_host(pk["lut"])
+        rows = nat.to_host(tr.dev.col_rows)[:r.nnz]
+        vals = nat.to_host(tr.vals32)[:r.nnz]
+        MW = tr.MW
+        mask = nat.to_host(tr.mask).view(np.uint32)[:r.nnz * MW].reshape(r.nnz, MW)
+        assert np.array_equal(w & 0x07FFFFFF, rows)
+        assert np.array_equal(lut[(w >> 27) & 15], vals)
+        hm = (w >> 31).astype(bool)
+        assert np.array_equal(hm, mask.any(axis=1))
+        assert hm.any() and not hm.all()
+        cm = nat.to_host(pk["cmask"]).view(np.uint32)[:hm.sum() * MW].reshape(-1, MW)
+        assert np.array_equal(cm, mask[hm])
+        mptr = nat.to_host(pk["mptr"])
+        assert np.array_equal(mptr, np.concatenate([[0], np.cumsum(np.add.reduceat(hm, r.col_ptr[:-1])
+                                                                   * (np.diff(r.col_ptr) > 0))]))
+
+    @pytest.mark.parametrize("K", [16, 40])
+    def test_packed_kernel_equals_wide(self, P, K):
+        import torch
+        from paper_2111_11682_b200.hogwild import HogwildTrainer
+        r, tbl, cfg = self._problem(P, K)
+        out = []
+        for packed in (True, False):
+            tr = HogwildTrainer(r, tbl, cfg, packed=packed)
+            assert (tr.packed is not None) == packed
+            for t in range(2):
+                for j in range(r.N):
+                    tr.launch_epoch(t, col_order=torch.tensor([j], dtype=torch.int32, device="cuda"), n_cols=1)
+            torch.cuda.synchronize()
+            out.append(tr.to_params())
+        a, b = out
+        for name in ("b", "b_hat", "U", "V", "W", "C"):
+            assert getattr(a, name).tobytes() == getattr(b, name).tobytes(), name
+
+    def test_host_stream_epochs(self, P):
+        """train_from_host (per-epoch H2D of the packed stream) == device-resident epochs
+        in expectation: same loss trajectory within Hogwild noise, finite model."""
+        from paper_2111_11682_b200.hogwild import HogwildTrainer
+        r, tbl, cfg = self._problem(P, 16, M=3000, N=400, dens=0.03)
+        tr = HogwildTrainer(r, tbl, cfg)
+        host = tr.pinned_stream()
+        assert set(host) == {"words", "cmask", "resid"}
+        losses, h2d, d2h = tr.train_from_host(host, 0, 3)
+        assert h2d == sum(v.numel() * v.element_size() for v in host.values())
+        assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
 class TestHogwildAtScale:
     """The performance mode against the exact mode (== reference) at C2 / C3 shape on
     structured (skewed, low-rank + noise) data, 90/10 split: |test RMSE diff| <= 0.005."""
