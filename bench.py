@@ -357,9 +357,7 @@ def run_gpu(args):
         "epoch_ms": [p * 1e3 for p in per],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_update": b_upd, "kernel": ("hogwild_sg_kernel<16,8,2,1>" if args.kernel == "subwarp" else
-                                "hogwild_kernel<4,1,%s,%s>" % (str(bool(args.atomic)).lower(),
-                                                                str(tr.packed is not None).lower()))},
+                     "bytes_per_update": b_upd, "kernel": tr.kernel_name()},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,
@@ -403,7 +401,8 @@ def main():
     ap.add_argument("--packed", type=int, default=1,
                     help="packed rating stream (4 B/rating + compact masks) instead of rows/vals/masks")
     ap.add_argument("--kernel", default="warp", choices=["warp", "subwarp"],
-                    help="Hogwild kernel: a warp per column (default) or 16 lanes per column")
+                    help="Hogwild kernel: a warp per column (default; packed stream) or the generic "
+                         "16-lanes-per-column kernel (wide stream)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -143,6 +143,15 @@ class HogwildTrainer:
             return None
         return {"words": words, "cmask": cmask, "mptr": mptr, "lut": lut}
 
+    def kernel_name(self) -> str:
+        """The epoch kernel a whole-matrix launch_epoch runs (for reports)."""
+        F, K = self.config.F, self.K
+        at = str(bool(self.atomic_rows)).lower()
+        if self.subwarp:
+            return "hogwild_sg_kernel"
+        fv = 1 if F <= 32 else F // 32
+        return "hogwild_kernel<%d,%d,%s,%s>" % (fv, self.MW, at, str(self.packed is not None).lower())
+
     def bytes_per_update(self) -> float:
         """Algorithmic HBM bytes per rating update (SURVEY §8(d) B_upd) + per-column share."""
         F, K = self.config.F, self.K

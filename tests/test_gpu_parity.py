@@ -419,21 +419,22 @@ class TestPackedStream:
         assert np.array_equal(mptr, np.concatenate([[0], np.cumsum(np.add.reduceat(hm, r.col_ptr[:-1])
                                                                    * (np.diff(r.col_ptr) > 0))]))
 
-    @pytest.mark.parametrize("K", [16, 40])
-    def test_packed_kernel_equals_wide(self, P, K):
+    def _serial(self, P, r, tbl, cfg, **kw):
         import torch
         from paper_2111_11682_b200.hogwild import HogwildTrainer
+        tr = HogwildTrainer(r, tbl, cfg, **kw)
+        for t in range(2):
+            for j in range(r.N):
+                tr.launch_epoch(t, col_order=torch.tensor([j], dtype=torch.int32, device="cuda"), n_cols=1)
+        torch.cuda.synchronize()
+        return tr, tr.to_params()
+
+    @pytest.mark.parametrize("K", [16, 40])
+    def test_packed_kernel_equals_wide(self, P, K):
         r, tbl, cfg = self._problem(P, K)
-        out = []
-        for packed in (True, False):
-            tr = HogwildTrainer(r, tbl, cfg, packed=packed)
-            assert (tr.packed is not None) == packed
-            for t in range(2):
-                for j in range(r.N):
-                    tr.launch_epoch(t, col_order=torch.tensor([j], dtype=torch.int32, device="cuda"), n_cols=1)
-            torch.cuda.synchronize()
-            out.append(tr.to_params())
-        a, b = out
+        ta, a = self._serial(P, r, tbl, cfg, packed=True)
+        tb, b = self._serial(P, r, tbl, cfg, packed=False)
+        assert ta.packed is not None and tb.packed is None
         for name in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(a, name).tobytes() == getattr(b, name).tobytes(), name
 
