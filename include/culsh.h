@@ -288,6 +288,39 @@ int culsh_append_csc2csr(const CulshData *d, int64_t n_old_cols, const int64_t *
  * exact, hence order-independent, for integer-valued ratings). */
 int culsh_segment_sums(int64_t n, const int64_t *ptr, const double *val, double *out, void *stream);
 
+/* ------------------------------------------------------- similarity --- */
+
+/* Exact GSM top-K by the merge route (similarity.py:164-185 _gsm_topk_kernel):
+ * target columns j_lo..j_lo+n_rows-1, all N candidates each, statistics by an
+ * ascending-row merge in fp64 (similarity.py:57-90), shrunk Pearson with the
+ * reference's expression order, ties to the lower index.  entries: (n_rows, K).
+ * 1 <= K <= min(128, N-1). */
+int culsh_gsm_merge_topk(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                         int64_t N, int64_t j_lo, int64_t n_rows, int K, double lambda_rho,
+                         int32_t *entries, void *stream);
+
+/* Count route, step 1: dense int8 panels xt/rt/qt (N x ld, zero-filled by the
+ * caller): 1 / r / r*r at (j, i - row_lo) for every rating with row_lo <= i <
+ * row_hi (the caller accumulates the products over row passes).  *status |= 1 if a
+ * value is not an integer in [-11, 11] (use the merge route then).  Step 2 is
+ * four int8 GEMMs with int32 accumulation (cuBLASLt). */
+int culsh_gsm_densify_rows(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                           int64_t N, int64_t row_lo, int64_t row_hi, int64_t ld, int8_t *xt,
+                           int8_t *rt, int8_t *qt, int *status, void *stream);
+
+/* Count route, step 3 (after the int32 products g_xx = X'X, g_rx = R'X,
+ * g_rr = R'R, g_qx = Q'X, each N x N with row stride ld): shrunk Pearson of every
+ * pair from the exact integer statistics and the per-column top-K, rows
+ * j_lo..j_lo+n_rows-1 -> entries (n_rows, K).  Bit-identical to the merge route. */
+int culsh_gsm_count_select(const int32_t *g_xx, const int32_t *g_rx, const int32_t *g_rr,
+                           const int32_t *g_qx, int64_t ld, int64_t N, int64_t j_lo, int64_t n_rows,
+                           int K, double lambda_rho, int32_t *entries, void *stream);
+
+/* similarity.py:110-135 pearson / shrunk_similarity of one pair:
+ * out (device, 3 doubles) = {pearson, shrunk, co-support n}. */
+int culsh_pair_similarity(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                          int64_t j1, int64_t j2, double lambda_rho, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -571,3 +571,78 @@ int orc_basic_pass(const int64_t *rows_subset, int64_t n_rows, const int64_t *ro
     }
     return 0;
 }
+
+/* ------------------------------------------------------------ similarity --- */
+
+/* similarity.py:57-90 _pair_stats: co-rated statistics by a sorted merge, sums in
+ * ascending row order.  out = {n, s1, s2, s12, q1, q2}. */
+void orc_pair_stats(const int32_t *r1, const double *v1, int64_t n1, const int32_t *r2,
+                    const double *v2, int64_t n2, double *out) {
+    int64_t n = 0, a = 0, b = 0;
+    double s1 = 0.0, s2 = 0.0, s12 = 0.0, q1 = 0.0, q2 = 0.0;
+    while (a < n1 && b < n2) {
+        if (r1[a] == r2[b]) {
+            double x = v1[a], y = v2[b];
+            n += 1; s1 += x; s2 += y; s12 += x * y; q1 += x * x; q2 += y * y;
+            ++a; ++b;
+        } else if (r1[a] < r2[b]) {
+            ++a;
+        } else {
+            ++b;
+        }
+    }
+    out[0] = (double)n; out[1] = s1; out[2] = s2; out[3] = s12; out[4] = q1; out[5] = q2;
+}
+
+/* similarity.py:93-107 _pearson_from_stats (same expression order, no contraction) */
+double orc_pearson_from_stats(const double *st) {
+    double n = st[0];
+    if (n < 2) return 0.0;
+    double cov = st[3] - st[1] * st[2] / n;
+    double var1 = st[4] - st[1] * st[1] / n;
+    double var2 = st[5] - st[2] * st[2] / n;
+    if (var1 <= 0.0 || var2 <= 0.0) return 0.0;
+    double rho = cov / sqrt(var1 * var2);
+    if (rho > 1.0) rho = 1.0;
+    else if (rho < -1.0) rho = -1.0;
+    return rho;
+}
+
+/* similarity.py:128-135 / :175-178: n/(n+lambda) * rho, 0 without co-support */
+static double shrunk_of(const double *st, double lambda_rho) {
+    if (st[0] == 0.0) return 0.0;
+    return st[0] / (st[0] + lambda_rho) * orc_pearson_from_stats(st);
+}
+
+typedef struct {
+    const int64_t *col_ptr; const int32_t *col_rows; const double *col_vals;
+    int64_t N; int K; double lambda_rho; int32_t *entries;
+} gsm_ctx_t;
+
+static void gsm_body(int64_t lo, int64_t hi, void *p) {
+    gsm_ctx_t *c = (gsm_ctx_t *)p;
+    double *best_sim = (double *)malloc(sizeof(double) * (size_t)c->K);
+    int32_t *best_idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)c->K);
+    double st[6];
+    for (int64_t j1 = lo; j1 < hi; ++j1) {
+        int count = 0;
+        const int64_t a0 = c->col_ptr[j1], a1 = c->col_ptr[j1 + 1];
+        for (int64_t j2 = 0; j2 < c->N; ++j2) {
+            if (j2 == j1) continue;
+            const int64_t b0 = c->col_ptr[j2], b1 = c->col_ptr[j2 + 1];
+            orc_pair_stats(c->col_rows + a0, c->col_vals + a0, a1 - a0, c->col_rows + b0,
+                           c->col_vals + b0, b1 - b0, st);
+            count = topk_insert(best_sim, best_idx, count, c->K, shrunk_of(st, c->lambda_rho), (int32_t)j2);
+        }
+        memcpy(c->entries + j1 * c->K, best_idx, sizeof(int32_t) * (size_t)c->K);
+    }
+    free(best_sim);
+    free(best_idx);
+}
+
+/* similarity.py:164-185 _gsm_topk_kernel: exact all-pairs top-K, prange over j1 */
+void orc_gsm_topk(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals, int64_t N,
+                  int K, double lambda_rho, int32_t *entries, int nthreads) {
+    gsm_ctx_t c = {col_ptr, col_rows, col_vals, N, K, lambda_rho, entries};
+    parallel_for(N, 4, nthreads, gsm_body, &c);
+}

@@ -434,3 +434,34 @@ def train_basic(d: Csr, mu_data, F, epochs, seed, rates_fn, regs, with_biases=Fa
         if bad:
             raise FloatingPointError(f"diverged at epoch {t}")
     return Model(mu, b, bh, U, V, np.zeros((d.N, 0)), np.zeros((d.N, 0)), np.zeros((d.N, 0), np.int32))
+
+
+# ----------------------------------------------------------- similarity ----
+
+def pair_stats(r1, v1, r2, v2) -> np.ndarray:
+    """similarity.py:57-90 -> [n, s1, s2, s12, q1, q2]"""
+    r1, r2 = np.ascontiguousarray(r1, np.int32), np.ascontiguousarray(r2, np.int32)
+    v1, v2 = np.ascontiguousarray(v1, np.float64), np.ascontiguousarray(v2, np.float64)
+    out = np.zeros(6)
+    lib().orc_pair_stats(_p(r1), _p(v1), ctypes.c_int64(len(r1)), _p(r2), _p(v2),
+                         ctypes.c_int64(len(r2)), _p(out))
+    return out
+
+
+def pearson_from_stats(st) -> float:
+    """similarity.py:93-107"""
+    f = lib().orc_pearson_from_stats
+    f.restype = ctypes.c_double
+    st = np.ascontiguousarray(st, np.float64)
+    return float(f(_p(st)))
+
+
+def gsm_topk(col_ptr, col_rows, col_vals, N, K, lambda_rho=100.0, nthreads=None) -> np.ndarray:
+    """similarity.py:164-185 -> (N, K) int32"""
+    ent = np.zeros((N, K), dtype=np.int32)
+    cp = np.ascontiguousarray(col_ptr, np.int64)
+    cr = np.ascontiguousarray(col_rows, np.int32)
+    cv = np.ascontiguousarray(col_vals, np.float64)
+    lib().orc_gsm_topk(_p(cp), _p(cr), _p(cv), ctypes.c_int64(N), K, ctypes.c_double(lambda_rho),
+                       _p(ent), nthreads or n_threads())
+    return ent

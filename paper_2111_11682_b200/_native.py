@@ -92,6 +92,10 @@ _SIGS = {
     "culsh_pack_stream": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "culsh_sgd_hogwild_epoch_packed": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
                                        _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
+    "culsh_gsm_merge_topk": [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
+    "culsh_gsm_densify_rows": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
+    "culsh_gsm_count_select": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
+    "culsh_pair_similarity": [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp],
     "culsh_rmse": [_P(CulshData), _P(CulshModel64), _vp, _vp, _vp, _i64, _i32, _f64, _f64, _f64,
                    _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],

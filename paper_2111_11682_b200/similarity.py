@@ -1,15 +1,28 @@
-"""Neighbour table J^K (reference similarity.py:14-48).
+"""Neighbour table J^K (reference similarity.py:14-48) and the
+exact column-similarity search (similarity.py:51-213): shrunk
+Pearson over co-rated rows, the all-pairs GSM top-K and the random control.
 
-The exact shrunk-Pearson GSM search and the random control of the reference
-(similarity.py:51-213) are a quadratic quality oracle and a control, outside
-the accelerated path (SURVEY §2 Table A), and are not rebuilt here.
+GSM runs on the GPU (csrc/similarity.cu), bit-identical to the reference:
+  * count route (integer ratings in [-11, 11], the usual stars): dense int8
+    panels X (indicator), R (values), Q (squares) and four int8 tensor-core
+    GEMMs with exact int32 accumulation give n = X'X, s1 = R'X, s12 = R'R,
+    q1 = Q'X (s2, q2 by transposition); every statistic is then the exact
+    integer the reference's fp64 sums produce;
+  * merge route (any values): thread per pair, ascending-row merge in fp64,
+    the reference's own summation order.
+Both feed one selection kernel: the reference's fp64 expression tree for the
+shrunk similarity (-fmad=false) and the (similarity desc, index asc) top-K that
+_topk_insert's strict comparisons produce.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
+
+from . import _native as nat
 
 
 @dataclass
@@ -51,3 +64,118 @@ class NeighborTable:
         entries = np.zeros((N, K), dtype=np.int32)
         entries[data[:, 0], data[:, 1]] = data[:, 2]
         return cls(N=N, K=K, entries=entries)
+
+
+@dataclass
+class SimilarityConfig:
+    """similarity.py:51-54"""
+
+    K: int
+    lambda_rho: float = 100.0
+
+
+def _csc(ratings):
+    """Device CSC of a SparseRatings / DeviceSparseRatings / DeviceRatings."""
+    return ratings.device() if hasattr(ratings, "device") else ratings
+
+
+def _pair(ratings, j1: int, j2: int, lambda_rho: float) -> np.ndarray:
+    if not (0 <= j1 < ratings.N and 0 <= j2 < ratings.N):
+        raise ValueError("column index out of range")
+    d = _csc(ratings)
+    out = nat.empty((3,), "float64")
+    nat.call("culsh_pair_similarity", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(d.col_vals),
+             int(j1), int(j2), float(lambda_rho), nat.ptr(out), nat.stream_ptr())
+    return nat.to_host(out)
+
+
+def pearson(ratings, j1: int, j2: int) -> float:
+    """Pearson correlation of two columns over their co-rated rows (similarity.py:110-121)."""
+    if j1 == j2:
+        raise ValueError("pearson requires two distinct columns")
+    return float(_pair(ratings, j1, j2, 100.0)[0])
+
+
+def shrunk_similarity(ratings, j1: int, j2: int, lambda_rho: float = 100.0) -> float:
+    """n/(n+lambda) * rho over the co-rated rows (similarity.py:124-135)."""
+    if j1 == j2:
+        raise ValueError("shrunk_similarity requires two distinct columns")
+    return float(_pair(ratings, j1, j2, lambda_rho)[1])
+
+
+_GSM_MAX_K = 128
+
+
+def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
+    """Count route; False (nothing written) when a value is not an integer in [-11, 11]."""
+    t = nat.torch()
+    N, M = d.N, d.M
+    ld = max(32, (N + 15) // 16 * 16)
+    free = t.cuda.mem_get_info()[0]
+    prod_bytes = 4 * ld * ld * 4
+    # rows of the dense panels per pass (int32 products accumulate exactly across passes)
+    budget = max(int(0.5 * free) - prod_bytes, 3 * ld * 64)
+    mc = max(64, min((M + 63) // 64 * 64, budget // (3 * ld) // 64 * 64))
+    g = [t.zeros((ld, ld), dtype=t.int32, device=nat.device()) for _ in range(4)]
+    st = nat.zeros((1,), "int32")
+    for m0 in range(0, M, mc):
+        m1 = min(M, m0 + mc)
+        w = (m1 - m0 + 63) // 64 * 64
+        pan = t.zeros((3, ld, w), dtype=t.int8, device=nat.device())
+        nat.call("culsh_gsm_densify_rows", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(d.col_vals),
+                 N, m0, m1, w, nat.ptr(pan[0]), nat.ptr(pan[1]), nat.ptr(pan[2]), nat.ptr(st),
+                 nat.stream_ptr())
+        if int(st.item()):
+            return False
+        x, r, q = pan[0], pan[1], pan[2]
+        g[0] += t._int_mm(x, x.t())
+        g[1] += t._int_mm(r, x.t())
+        g[2] += t._int_mm(r, r.t())
+        g[3] += t._int_mm(q, x.t())
+        del pan, x, r, q
+    nat.call("culsh_gsm_count_select", nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]), nat.ptr(g[3]), ld, N,
+             0, N, K, float(lambda_rho), nat.ptr(entries), nat.stream_ptr())
+    return True
+
+
+def gsm_topk(ratings, config: SimilarityConfig, method: str = "auto") -> NeighborTable:
+    """Exact top-K neighbours of every column by shrunk Pearson similarity
+    (similarity.py:188-200): all N*(N-1) pairs, ties to the lower index, rows by
+    descending similarity.  method: "auto" (count route when the ratings allow it,
+    else merge), "count" or "merge" -- every route gives the same bytes."""
+    N = ratings.N
+    K = config.K
+    if K > N - 1:
+        raise ValueError(f"K={K} exceeds N-1={N - 1}")
+    if K < 1:
+        raise ValueError("K must be positive")
+    if K > _GSM_MAX_K:
+        raise ValueError(f"the GPU GSM keeps at most {_GSM_MAX_K} neighbours per column")
+    if method not in ("auto", "count", "merge"):
+        raise ValueError(f"unknown method {method!r}")
+    d = _csc(ratings)
+    entries = nat.empty((N * K,), "int32")
+    done = False
+    if method in ("auto", "count") and d.nnz:
+        done = _gsm_count(d, K, config.lambda_rho, entries)
+        if not done and method == "count":
+            raise ValueError("the count route needs integer ratings in [-11, 11]")
+    if not done:
+        nat.call("culsh_gsm_merge_topk", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(d.col_vals), N, 0,
+                 N, K, float(config.lambda_rho), nat.ptr(entries), nat.stream_ptr())
+    return NeighborTable(N=N, K=K, entries=nat.to_host(entries).reshape(N, K).astype(np.int32))
+
+
+def random_topk(N: int, K: int, seed: int) -> NeighborTable:
+    """Uniform random neighbour selection without replacement, excluding self
+    (similarity.py:203-213).  The values are defined by numpy's PCG64 stream
+    (rng.choice per column), so they are drawn on the host like init_params."""
+    if K > N - 1:
+        raise ValueError(f"K={K} exceeds N-1={N - 1}")
+    rng = np.random.default_rng(seed)
+    entries = np.empty((N, K), dtype=np.int32)
+    for j in range(N):
+        picks = rng.choice(N - 1, size=K, replace=False)
+        picks[picks >= j] += 1
+        entries[j] = picks
+    return NeighborTable(N=N, K=K, entries=entries)

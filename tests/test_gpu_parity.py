@@ -627,3 +627,72 @@ class TestOnlineSession:
                   "base_b", "base_bhat"):
             assert nat.to_host(getattr(d, a)).tobytes() == nat.to_host(getattr(full, a)).tobytes(), a
         assert d.mu == full.mu
+
+
+# -------------------------------------------------------- GSM similarity ---
+
+def _sim_ratings(P, z, pre):
+    return P.SparseRatings(int(z[pre + "M"]), int(z[pre + "N"]), z[pre + "rows"], z[pre + "cols"],
+                           z[pre + "vals"])
+
+
+class TestGsm:
+    """GPU exact similarity (similarity.py) against the reference's own outputs
+    (tests/golden/similarity.npz): bit-exact similarities, identical top-K tables
+    by both the count (int8 tensor-core GEMM) and the merge route."""
+
+    def test_pearson_shrunk_bitwise(self, P):
+        z = load_golden("similarity.npz")
+        for name in ("int", "real"):
+            r = _sim_ratings(P, z, name + "_")
+            Pm, Sm = z[name + "_pearson"], z[name + "_shrunk25"]
+            for a in range(0, r.N, 3):
+                for b in range(r.N):
+                    if a != b:
+                        assert P.pearson(r, a, b) == Pm[a, b], (name, a, b)
+                        assert P.shrunk_similarity(r, a, b, 25.0) == Sm[a, b], (name, a, b)
+        with pytest.raises(ValueError):
+            P.pearson(r, 1, 1)
+
+    def test_gsm_small_cases_both_routes(self, P):
+        z = load_golden("similarity.npz")
+        n_count = 0
+        for name in z["cases"]:
+            r = _sim_ratings(P, z, str(name) + "_")
+            integral = bool(np.all(r.col_vals == np.round(r.col_vals)))
+            for key in z.files:
+                if not key.startswith(f"{name}_gsm_K"):
+                    continue
+                K = int(key.split("_K")[1].split("_")[0])
+                cfg = P.SimilarityConfig(K=K, lambda_rho=float(key.split("_l")[1]))
+                assert np.array_equal(P.gsm_topk(r, cfg, method="merge").entries, z[key]), key
+                if integral:
+                    assert np.array_equal(P.gsm_topk(r, cfg, method="count").entries, z[key]), key
+                    n_count += 1
+        assert n_count >= 20
+        with pytest.raises(ValueError):
+            P.gsm_topk(_sim_ratings(P, z, "real_"), P.SimilarityConfig(K=3), method="count")
+
+    def test_gsm_c1(self, P):
+        z = load_golden("similarity.npz")
+        r = _sim_ratings(P, z, "c1_")
+        for meth in ("count", "merge"):
+            assert np.array_equal(P.gsm_topk(r, P.SimilarityConfig(K=16), method=meth).entries,
+                                  z["c1_gsm_K16"]), meth
+            assert np.array_equal(P.gsm_topk(r, P.SimilarityConfig(K=32, lambda_rho=50.0), method=meth).entries,
+                                  z["c1_gsm_K32_l50"]), meth
+
+    def test_gsm_mid_scale_vs_oracle(self, P, orc):
+        """20,000 x 3,000, ~600k integer ratings: count route == merge route == oracle."""
+        rng = np.random.default_rng(7)
+        M, N, nnz = 20000, 3000, 600000
+        key = np.unique(rng.integers(0, M * N, nnz))
+        rows, cols = (key % M).astype(np.int32), (key // M).astype(np.int32)
+        vals = rng.integers(1, 6, len(key)).astype(np.float64)
+        r = P.SparseRatings(M, N, rows, cols, vals)
+        cfg = P.SimilarityConfig(K=32)
+        a = P.gsm_topk(r, cfg, method="count").entries
+        b = P.gsm_topk(r, cfg, method="merge").entries
+        assert np.array_equal(a, b)
+        ref = orc.gsm_topk(r.col_ptr, r.col_rows, r.col_vals, N, 32, 100.0)
+        assert np.array_equal(a, ref)

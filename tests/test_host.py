@@ -8,7 +8,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import ROOT
+from conftest import ROOT, load_golden
 
 
 def header_functions():
@@ -122,3 +122,15 @@ def test_increment_batch_validation():
         P.make_increment(2, 2, t, new_row_count=1, new_col_count=0)
     b = P.make_increment(2, 2, P.Triplets(np.array([2, 0]), np.array([0, 3]), np.array([1., 2.])))
     assert (b.new_row_count, b.new_col_count, b.M_hat, b.N_hat) == (1, 2, 3, 4)
+
+
+def test_random_topk_matches_reference():
+    """random_topk is defined by numpy's PCG64 stream (similarity.py:203-213)."""
+    import paper_2111_11682_b200 as P
+    z = load_golden("similarity.npz")
+    assert np.array_equal(P.random_topk(2, 1, seed=0).entries, z["rand_2_1_0"])
+    assert np.array_equal(P.random_topk(50, 5, seed=9).entries, z["rand_50_5_9"])
+    assert np.array_equal(P.random_topk(1682, 16, seed=0).entries, z["rand_1682_16_0"])
+    P.random_topk(1000, 32, seed=4).validate()
+    with pytest.raises(ValueError):
+        P.random_topk(4, 4, seed=0)

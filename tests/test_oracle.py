@@ -226,3 +226,54 @@ class TestBasicGolden:
                                 (0.02, 0.02, 0.035, 0.035, 0.002, 0.002), bool(wb), bool(srt))
             for n, a in (("b", m.b), ("b_hat", m.bhat), ("U", m.U), ("V", m.V)):
                 assert a.tobytes() == z[f"{pre}{n}"].tobytes(), (s, n)
+
+
+# ------------------------------------------------------- similarity (GSM) ---
+
+def _col_view(z, pre):
+    M, N = int(z[pre + "M"]), int(z[pre + "N"])
+    rows, cols, vals = z[pre + "rows"], z[pre + "cols"], z[pre + "vals"]
+    order = np.lexsort((rows, cols))
+    col_ptr = np.zeros(N + 1, np.int64)
+    np.cumsum(np.bincount(cols, minlength=N), out=col_ptr[1:])
+    return M, N, col_ptr, rows[order].astype(np.int32), vals[order].astype(np.float64)
+
+
+class TestOracleSimilarity:
+    """oracle GSM restatement == reference similarity.py outputs (tests/golden/similarity.npz)."""
+
+    def test_pearson_and_shrunk_bitwise(self, orc):
+        z = load_golden("similarity.npz")
+        for name in z["cases"]:
+            M, N, cp, cr, cv = _col_view(z, str(name) + "_")
+            P = np.zeros((N, N))
+            S = np.zeros((N, N))
+            for a in range(N):
+                for b in range(N):
+                    if a == b:
+                        continue
+                    st = orc.pair_stats(cr[cp[a]:cp[a + 1]], cv[cp[a]:cp[a + 1]],
+                                        cr[cp[b]:cp[b + 1]], cv[cp[b]:cp[b + 1]])
+                    P[a, b] = orc.pearson_from_stats(st)
+                    S[a, b] = 0.0 if st[0] == 0 else st[0] / (st[0] + 25.0) * P[a, b]
+            assert P.tobytes() == z[f"{name}_pearson"].tobytes(), name
+            assert S.tobytes() == z[f"{name}_shrunk25"].tobytes(), name
+
+    def test_gsm_small_cases(self, orc):
+        z = load_golden("similarity.npz")
+        n = 0
+        for name in z["cases"]:
+            M, N, cp, cr, cv = _col_view(z, str(name) + "_")
+            for key in z.files:
+                if key.startswith(f"{name}_gsm_K"):
+                    K = int(key.split("_K")[1].split("_")[0])
+                    lam = float(key.split("_l")[1])
+                    assert np.array_equal(orc.gsm_topk(cp, cr, cv, N, K, lam), z[key]), key
+                    n += 1
+        assert n >= 30
+
+    def test_gsm_c1(self, orc):
+        z = load_golden("similarity.npz")
+        M, N, cp, cr, cv = _col_view(z, "c1_")
+        assert np.array_equal(orc.gsm_topk(cp, cr, cv, N, 16, 100.0), z["c1_gsm_K16"])
+        assert np.array_equal(orc.gsm_topk(cp, cr, cv, N, 32, 50.0), z["c1_gsm_K32_l50"])
