@@ -616,7 +616,7 @@ static double shrunk_of(const double *st, double lambda_rho) {
 
 typedef struct {
     const int64_t *col_ptr; const int32_t *col_rows; const double *col_vals;
-    int64_t N; int K; double lambda_rho; int32_t *entries;
+    int64_t N; int K; double lambda_rho; int32_t *entries; const int64_t *targets;
 } gsm_ctx_t;
 
 static void gsm_body(int64_t lo, int64_t hi, void *p) {
@@ -624,7 +624,8 @@ static void gsm_body(int64_t lo, int64_t hi, void *p) {
     double *best_sim = (double *)malloc(sizeof(double) * (size_t)c->K);
     int32_t *best_idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)c->K);
     double st[6];
-    for (int64_t j1 = lo; j1 < hi; ++j1) {
+    for (int64_t t = lo; t < hi; ++t) {
+        const int64_t j1 = c->targets ? c->targets[t] : t;
         int count = 0;
         const int64_t a0 = c->col_ptr[j1], a1 = c->col_ptr[j1 + 1];
         for (int64_t j2 = 0; j2 < c->N; ++j2) {
@@ -634,7 +635,7 @@ static void gsm_body(int64_t lo, int64_t hi, void *p) {
                            c->col_vals + b0, b1 - b0, st);
             count = topk_insert(best_sim, best_idx, count, c->K, shrunk_of(st, c->lambda_rho), (int32_t)j2);
         }
-        memcpy(c->entries + j1 * c->K, best_idx, sizeof(int32_t) * (size_t)c->K);
+        memcpy(c->entries + t * c->K, best_idx, sizeof(int32_t) * (size_t)c->K);
     }
     free(best_sim);
     free(best_idx);
@@ -643,6 +644,14 @@ static void gsm_body(int64_t lo, int64_t hi, void *p) {
 /* similarity.py:164-185 _gsm_topk_kernel: exact all-pairs top-K, prange over j1 */
 void orc_gsm_topk(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals, int64_t N,
                   int K, double lambda_rho, int32_t *entries, int nthreads) {
-    gsm_ctx_t c = {col_ptr, col_rows, col_vals, N, K, lambda_rho, entries};
+    gsm_ctx_t c = {col_ptr, col_rows, col_vals, N, K, lambda_rho, entries, NULL};
     parallel_for(N, 4, nthreads, gsm_body, &c);
+}
+
+/* the same for a subset of target columns (all N candidates): entries (n_targets, K) */
+void orc_gsm_topk_targets(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals, int64_t N,
+                          const int64_t *targets, int64_t n_targets, int K, double lambda_rho,
+                          int32_t *entries, int nthreads) {
+    gsm_ctx_t c = {col_ptr, col_rows, col_vals, N, K, lambda_rho, entries, targets};
+    parallel_for(n_targets, 1, nthreads, gsm_body, &c);
 }

@@ -465,3 +465,15 @@ def gsm_topk(col_ptr, col_rows, col_vals, N, K, lambda_rho=100.0, nthreads=None)
     lib().orc_gsm_topk(_p(cp), _p(cr), _p(cv), ctypes.c_int64(N), K, ctypes.c_double(lambda_rho),
                        _p(ent), nthreads or n_threads())
     return ent
+
+
+def gsm_topk_targets(col_ptr, col_rows, col_vals, N, targets, K, lambda_rho=100.0, nthreads=None):
+    """similarity.py:164-185 for the listed target columns only -> (len(targets), K) int32"""
+    tg = np.ascontiguousarray(targets, np.int64)
+    ent = np.zeros((len(tg), K), dtype=np.int32)
+    cp = np.ascontiguousarray(col_ptr, np.int64)
+    cr = np.ascontiguousarray(col_rows, np.int32)
+    cv = np.ascontiguousarray(col_vals, np.float64)
+    lib().orc_gsm_topk_targets(_p(cp), _p(cr), _p(cv), ctypes.c_int64(N), _p(tg), ctypes.c_int64(len(tg)), K,
+                               ctypes.c_double(lambda_rho), _p(ent), nthreads or n_threads())
+    return ent
