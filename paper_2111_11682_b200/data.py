@@ -122,6 +122,34 @@ class SparseRatings:
             self._dev = DeviceRatings(self)
         return self._dev
 
+    def save(self, path) -> None:
+        """LSHMF-R v1 text matrix (data.py:238-243): header, then one ``row col value``
+        line per entry in entry order, values as Python float repr."""
+        with open(path, "w") as fh:
+            fh.write(f"{RATINGS_MAGIC} {RATINGS_VERSION} {self.M} {self.N} {self.nnz}\n")
+            fh.writelines(f"{i} {j} {v!r}\n" for i, j, v in
+                          zip(self.entry_rows.tolist(), self.entry_cols.tolist(), self.entry_values.tolist()))
+
+    @classmethod
+    def load(cls, path) -> "SparseRatings":
+        """Read an LSHMF-R v1 file (data.py:245-257); ValueError on a foreign header."""
+        with open(path) as fh:
+            header = fh.readline().split()
+            if len(header) != 5 or header[0] != RATINGS_MAGIC or header[1] != RATINGS_VERSION:
+                raise ValueError(f"{path}: not a {RATINGS_MAGIC} {RATINGS_VERSION} file")
+            M, N, nnz = int(header[2]), int(header[3]), int(header[4])
+            rows = np.empty(nnz, dtype=np.int32)
+            cols = np.empty(nnz, dtype=np.int32)
+            vals = np.empty(nnz, dtype=np.float64)
+            for k in range(nnz):
+                fields = fh.readline().split()
+                rows[k], cols[k], vals[k] = int(fields[0]), int(fields[1]), float(fields[2])
+        return build_indices(Triplets(rows, cols, vals), M=M, N=N)
+
+
+RATINGS_MAGIC = "LSHMF-R"
+RATINGS_VERSION = "v1"
+
 
 def build_indices(triplets: Triplets, M: int | None = None, N: int | None = None) -> SparseRatings:
     """Index triplets, rejecting out-of-range, non-finite and duplicate entries (data.py:269-286)."""

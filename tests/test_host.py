@@ -134,3 +134,25 @@ def test_random_topk_matches_reference():
     P.random_topk(1000, 32, seed=4).validate()
     with pytest.raises(ValueError):
         P.random_topk(4, 4, seed=0)
+
+
+def test_lshmfr_format_byte_identical(tmp_path):
+    """SparseRatings.save writes the reference's LSHMF-R v1 bytes (data.py:238-243)
+    and load reads them back (data.py:245-257)."""
+    import paper_2111_11682_b200 as P
+    z = load_golden("similarity.npz")
+    for name in z["cases"]:
+        pre = str(name) + "_"
+        r = P.SparseRatings(int(z[pre + "M"]), int(z[pre + "N"]), z[pre + "rows"], z[pre + "cols"],
+                            z[pre + "vals"])
+        path = tmp_path / f"{name}.txt"
+        r.save(path)
+        assert path.read_bytes() == z[pre + "lshmfr"].tobytes(), name
+        back = P.SparseRatings.load(path)
+        assert (back.M, back.N) == (r.M, r.N)
+        assert back.entry_values.tobytes() == r.entry_values.tobytes()
+        assert np.array_equal(back.entry_rows, r.entry_rows)
+    bad = tmp_path / "bad.txt"
+    bad.write_text("NOPE v1 1 1 0\n")
+    with pytest.raises(ValueError):
+        P.SparseRatings.load(bad)
