@@ -236,8 +236,8 @@ int culsh_pack_stream(int64_t N, const int64_t *col_ptr, const int32_t *rows, co
                       int64_t *mcount, const int64_t *mptr, uint32_t *cmask, int *status, void *stream);
 
 /* culsh_sgd_hogwild_epoch over the packed stream (whole columns, warp per
- * column; flags bit 1 only -- no rotation, no sub-warp kernel).  Identical
- * updates to the wide-stream kernel on the same data. */
+ * column; flags bits 0-1 as there, no sub-warp kernel).  Identical updates to
+ * the wide-stream kernel on the same data. */
 int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const uint32_t *packed,
                                    const float *lut, const int64_t *mptr, const uint32_t *cmask,
                                    const int64_t *resid_ptr, const float *resid, const int32_t *col_order,

@@ -153,7 +153,7 @@ constexpr int hw_smem_per_warp() {
 // u32 per rating {row: bits 0-26, value code: bits 27-30 (into lut), has-mask:
 // bit 31} and mask words only for ratings with a set bit (column base mptr[j]),
 // 4 + MW*4*(fraction with explicit neighbours) bytes per rating instead of
-// 8 + 4*MW.  Whole columns in CSC order only (no seg, no rotation).
+// 8 + 4*MW.  Whole columns only (no seg); rotation keeps two mask cursors.
 template <int FV, int KPL, bool ATOMIC, bool PACK>
 __global__ void __launch_bounds__(kHwWarps * 32, 4)
 hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__restrict__ seg,
@@ -216,12 +216,13 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         const int64_t hi = seg ? seg[2 * j + 1] : col_ptr[j + 1];
         const int n = (int)(hi - lo);
         const float *rcol = resid + resid_ptr[j];
-        int64_t mrun = PACK ? mptr[j] : 0;   // packed: next compact mask slot of this column
+        // packed: next compact mask slot of the rotated column's segment 1 ([rot, n)) / 2 ([0, rot))
+        int64_t mrun1 = PACK ? mptr[j] : 0, mrun2 = mrun1;
         // Visiting order: the column's entries rotated to start at position `rot`
         // (a per-column hash when `rotate` is set).  Warps then sweep the rows out of
         // phase with each other instead of in lock-step, which keeps concurrent
         // Hogwild writes to the same u_i rare.
-        const int rot = (!PACK && (flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
+        const int rot = ((flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
         int rrel2 = 0;   // residual offset (relative to the column base) at position lo
         if (lo > c_lo) {   // DSGD block: skip the residuals of the column's earlier row blocks
             int skip = 0;
@@ -231,7 +232,18 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             rrel2 = warp_sum(skip);
         }
         int rrel1 = rrel2;   // ... at position lo + rot
-        if (rot > 0) {
+        if (PACK && rot > 0) {   // (packed streams are whole columns: lo == c_lo, rrel2 == 0)
+            int h = 0;
+            for (int64_t x = lo + lane; x < lo + rot; x += 32)
+                h += (int)(__ldg(reinterpret_cast<const uint32_t *>(rows) + x) >> 31);
+            h = warp_sum(h);
+            int skip = 0;
+            for (int64_t x = mrun2 + lane; x < mrun2 + h; x += 32)
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
+            mrun1 += h;
+            rrel1 += warp_sum(skip);
+        } else if (rot > 0) {
             int skip = 0;
             for (int64_t x = lo + lane; x < lo + rot; x += 32)
 #pragma unroll
@@ -256,13 +268,15 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                 ri = (int)(wd & 0x07FFFFFFu);
                 rv = __ldg(lut + ((wd >> 27) & 15u));
                 const bool hm = (wd >> 31) != 0u;
-                const unsigned bal = __ballot_sync(0xffffffffu, hm);
+                const unsigned b1 = __ballot_sync(0xffffffffu, hm && !seg2);
+                const unsigned b2 = __ballot_sync(0xffffffffu, hm && seg2);
                 if (hm) {
-                    const int64_t mi = mrun + __popc(bal & lt_mask);
+                    const int64_t mi = seg2 ? mrun2 + __popc(b2 & lt_mask) : mrun1 + __popc(b1 & lt_mask);
                     m0 = mask[mi * KPL];
                     if constexpr (KPL == 2) m1 = mask[mi * KPL + 1];
                 }
-                mrun += __popc(bal);
+                mrun1 += __popc(b1);
+                mrun2 += __popc(b2);
             } else {
                 ri = have ? rows[e] : 0;
                 rv = have ? vals[e] : 0.f;
@@ -1031,7 +1045,7 @@ extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col
     CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
     CULSH_REQUIRE((F >= 1 && F <= 32) || F == 64 || F == 128 || F == 256,
                   "Hogwild mode needs F <= 32 or F in {64, 128, 256}");
-    CULSH_REQUIRE((flags & 5) == 0, "the packed stream supports neither rotation nor the sub-warp kernel");
+    CULSH_REQUIRE((flags & 4) == 0, "the packed stream does not run the sub-warp kernel");
     if (N_list <= 0) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));

@@ -111,7 +111,7 @@ class HogwildTrainer:
         self.ticket = nat.zeros((1,), "int32")
         self.status = nat.zeros((1,), "int32")
         self.loss = nat.zeros((1,), "float64")
-        self.packed = self._build_packed() if (packed and not rotate and not subwarp) else None
+        self.packed = self._build_packed() if (packed and not subwarp) else None
 
     def _build_packed(self):
         """Packed rating stream (culsh_pack_stream): 4 B per rating + mask words of the
@@ -184,7 +184,8 @@ class HogwildTrainer:
         pk, d = self.packed, self.dev
         nat.call("culsh_sgd_hogwild_epoch_packed", n, nat.ptr(d.col_ptr), nat.ptr(words), nat.ptr(pk["lut"]),
                  nat.ptr(pk["mptr"]), nat.ptr(cmask), nat.ptr(self.resid_ptr), nat.ptr(resid), nat.ptr(order),
-                 ctypes.byref(self.model.struct), ctypes.byref(rates), 2 if self.atomic_rows else 0,
+                 ctypes.byref(self.model.struct), ctypes.byref(rates),
+                 int(self.rotate) | (2 if self.atomic_rows else 0),
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss), nat.ptr(self.status),
                  nat.stream_ptr())
 

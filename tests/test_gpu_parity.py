@@ -429,11 +429,12 @@ class TestPackedStream:
         torch.cuda.synchronize()
         return tr, tr.to_params()
 
+    @pytest.mark.parametrize("rotate", [False, True])
     @pytest.mark.parametrize("K", [16, 40])
-    def test_packed_kernel_equals_wide(self, P, K):
+    def test_packed_kernel_equals_wide(self, P, K, rotate):
         r, tbl, cfg = self._problem(P, K)
-        ta, a = self._serial(P, r, tbl, cfg, packed=True)
-        tb, b = self._serial(P, r, tbl, cfg, packed=False)
+        ta, a = self._serial(P, r, tbl, cfg, packed=True, rotate=rotate)
+        tb, b = self._serial(P, r, tbl, cfg, packed=False, rotate=rotate)
         assert ta.packed is not None and tb.packed is None
         for name in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(a, name).tobytes() == getattr(b, name).tobytes(), name

@@ -27,16 +27,32 @@ cfg = P.TrainConfig(F=F, K=K, epochs=3, seed=0, alpha_b=0.02, alpha_b_hat=0.02,
                     alpha_u=0.02, alpha_v=0.02, alpha_w=0.001, alpha_c=0.001,
                     lambda_b=0.01, lambda_b_hat=0.01, lambda_u=0.01, lambda_v=0.01,
                     lambda_w=0.05, lambda_c=0.05)
-for packed in (False, True):
-    for atomic in (True, False):
-        h = HogwildTrainer(tr, nbr, cfg, packed=packed, atomic_rows=atomic)
+import time
+if "--stress" in sys.argv:
+    # divergence frequency of the first (largest-step) epoch, fresh model each trial
+    for rotate in (False, True):
+        fails = 0
+        for trial in range(int(sys.argv[sys.argv.index("--stress") + 1])):
+            h = HogwildTrainer(tr, nbr, cfg, rotate=rotate)
+            h.launch_epoch(0)
+            torch.cuda.synchronize()
+            fails += int(h.status.item()) != 0
+            del h
+        print("rotate", rotate, "diverged", fails, flush=True)
+    sys.exit(0)
+for packed in (True,):
+    for atomic, rotate in ((True, False), (True, True)):
+        h = HogwildTrainer(tr, nbr, cfg, packed=packed, atomic_rows=atomic, rotate=rotate)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         out = []
         for t in range(3):
             h.loss.zero_()
             h.launch_epoch(t)
             torch.cuda.synchronize()
             out.append((float(h.loss.item()) / d.nnz, int(h.status.item())))
+        ms = (time.perf_counter() - t0) / 3 * 1e3
         p = h.to_params()
-        print("packed", h.packed is not None, "atomic", atomic, out,
+        print("packed", h.packed is not None, "atomic", atomic, "rotate", rotate, "ms/epoch %.2f" % ms, out,
               "finite U", bool(np.isfinite(p.U).all()), "max|U|", float(np.nanmax(np.abs(p.U))),
               "max|V|", float(np.nanmax(np.abs(p.V))), "max|C|", float(np.nanmax(np.abs(p.C))), flush=True)
