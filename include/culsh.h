@@ -210,7 +210,11 @@ int culsh_explicit_stream(const CulshData *d, double mu, const int32_t *nbr, int
  * value.  flags bit 0: start each column at a per-column hashed offset (warps
  * sweep rows out of phase: fewer concurrent writes to one u_i); bit 1: apply
  * row updates as vector atomic adds of the delta (no lost updates); bit 2: the
- * sub-warp kernel (16 lanes per column) instead of warp-per-column; max_warps > 0
+ * sub-warp kernel (16 lanes per column) instead of warp-per-column; bit 3: seg is
+ * indexed by ticket (work segments: list entry t = column col_order[t], entries
+ * [seg[2t], seg[2t+1] & (2^40-1)), S = seg[2t+1] >> 40 segments in that column; a
+ * segment of a split column (S > 1) runs concurrently with the column's other
+ * segments and atomically adds 1/S of its v/w/c/b_hat change); max_warps > 0
  * caps the number of concurrently active column warps (Hogwild staleness on
  * small matrices), 0 = every resident warp.  loss_out
  * (device double, optional) accumulates sum e^2; *status |= 1 on a non-finite
@@ -235,10 +239,12 @@ int culsh_pack_stream(int64_t N, const int64_t *col_ptr, const int32_t *rows, co
                       const uint32_t *mask, int MW, const float *lut, int n_lut, uint32_t *packed,
                       int64_t *mcount, const int64_t *mptr, uint32_t *cmask, int *status, void *stream);
 
-/* culsh_sgd_hogwild_epoch over the packed stream (whole columns, warp per
- * column; flags bits 0-1 as there, no sub-warp kernel).  Identical updates to
- * the wide-stream kernel on the same data. */
-int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const uint32_t *packed,
+/* culsh_sgd_hogwild_epoch over the packed stream (warp per column or per work
+ * segment; flags bits 0, 1, 3 as there -- seg must be NULL or a per-ticket work
+ * segment list -- no sub-warp kernel).  Identical updates to the wide-stream
+ * kernel on the same data. */
+int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
+                                   const uint32_t *packed,
                                    const float *lut, const int64_t *mptr, const uint32_t *cmask,
                                    const int64_t *resid_ptr, const float *resid, const int32_t *col_order,
                                    CulshModel32 *m, const CulshRates *r, int flags, int max_warps,

@@ -90,7 +90,7 @@ _SIGS = {
     "culsh_sgd_hogwild_epoch": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
                                 _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
     "culsh_pack_stream": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
-    "culsh_sgd_hogwild_epoch_packed": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
+    "culsh_sgd_hogwild_epoch_packed": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _P(CulshModel32),
                                        _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
     "culsh_gsm_merge_topk": [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_gsm_densify_rows": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],

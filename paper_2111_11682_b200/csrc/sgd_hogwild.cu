@@ -137,7 +137,8 @@ constexpr int kHwDepth = 8;      // u_i prefetch depth (updates in flight per wa
 
 template <int FV, int KPL>
 constexpr int hw_smem_per_warp() {
-    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + kHwDepth * 32 * FV * 4 + kHwDepth * 4;
+    // metadata window, mask word 1, u-row ring + b ring, start values of a work segment
+    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + kHwDepth * 32 * FV * 4 + kHwDepth * 4 + 32 * (FV + 2 * KPL + 1) * 4;
 }
 
 // FV floats per lane; F == 32*FV (vector path) or F < 32 with FV == 1 (masked).
@@ -174,6 +175,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
     float *s_ring = reinterpret_cast<float *>(wbase + 64 * 16 + (KPL == 2 ? 64 * 4 : 0));
     float *s_bring = s_ring + P * 32 * FV;
     float *my_ring = s_ring + lane * FV;
+    float *my_start = s_bring + P + lane * (FV + 2 * KPL + 1);   // this lane's segment start values
 
     const bool fl = FV > 1 || (int)lane < F;   // lane owns factor slots (F == 32*FV when FV > 1)
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -211,12 +213,27 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             c[q] = kin[q] ? C[j * K + k] : 0.f;
         }
         float bh = BHv[j];
-        const int64_t c_lo = col_ptr[j];
-        const int64_t lo = seg ? seg[2 * j] : c_lo;
-        const int64_t hi = seg ? seg[2 * j + 1] : col_ptr[j + 1];
+        const int64_t c_lo = col_ptr[j], c_hi = col_ptr[j + 1];
+        // entry range: per-ticket work segment (flags bit 3), per-column DSGD block, or the column
+        const int64_t lo = seg ? seg[(flags & 8) ? 2 * (int64_t)t : 2 * j] : c_lo;
+        int64_t hi = seg ? seg[(flags & 8) ? 2 * (int64_t)t + 1 : 2 * j + 1] : c_hi;
+        // a work segment that is only part of its column runs concurrently with the column's
+        // other S segments (S in bits 40-63 of its end): its column parameters are merged
+        // back as atomic adds of (change / S) -- the average of the segments' changes
+        const int nparts = (flags & 8) ? (int)((uint64_t)hi >> 40) : 1;
+        hi &= (int64_t)0xFFFFFFFFFFLL;
         const int n = (int)(hi - lo);
+        const bool part_col = nparts > 1;
+        const float inv_parts = 1.f / (float)max(nparts, 1);
+        if (part_col) {   // start values, for the deltas merged at the end (lane-private slots)
+#pragma unroll
+            for (int x = 0; x < FV; ++x) my_start[x] = v[x];
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) { my_start[FV + q] = w[q]; my_start[FV + KPL + q] = c[q]; }
+            my_start[FV + 2 * KPL] = bh;
+        }
         const float *rcol = resid + resid_ptr[j];
-        // packed: next compact mask slot of the rotated column's segment 1 ([rot, n)) / 2 ([0, rot))
+        // packed: next compact mask slot of the rotated range's segment 1 ([rot, n)) / 2 ([0, rot))
         int64_t mrun1 = PACK ? mptr[j] : 0, mrun2 = mrun1;
         // Visiting order: the column's entries rotated to start at position `rot`
         // (a per-column hash when `rotate` is set).  Warps then sweep the rows out of
@@ -224,7 +241,19 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         // Hogwild writes to the same u_i rare.
         const int rot = ((flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
         int rrel2 = 0;   // residual offset (relative to the column base) at position lo
-        if (lo > c_lo) {   // DSGD block: skip the residuals of the column's earlier row blocks
+        if (PACK && lo > c_lo) {   // work segment: mask cursor and residual offset at lo
+            int h = 0;
+            for (int64_t x = c_lo + lane; x < lo; x += 32)
+                h += (int)(__ldg(reinterpret_cast<const uint32_t *>(rows) + x) >> 31);
+            h = warp_sum(h);
+            int skip = 0;
+            for (int64_t x = mrun2 + lane; x < mrun2 + h; x += 32)
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
+            mrun2 += h;
+            mrun1 = mrun2;
+            rrel2 = warp_sum(skip);
+        } else if (lo > c_lo) {   // DSGD block: skip the residuals of the column's earlier row blocks
             int skip = 0;
             for (int64_t x = c_lo + lane; x < lo; x += 32)
 #pragma unroll
@@ -232,7 +261,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             rrel2 = warp_sum(skip);
         }
         int rrel1 = rrel2;   // ... at position lo + rot
-        if (PACK && rot > 0) {   // (packed streams are whole columns: lo == c_lo, rrel2 == 0)
+        if (PACK && rot > 0) {
             int h = 0;
             for (int64_t x = lo + lane; x < lo + rot; x += 32)
                 h += (int)(__ldg(reinterpret_cast<const uint32_t *>(rows) + x) >> 31);
@@ -457,16 +486,35 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         cp_async_wait<0>();
         if (!isfinite(lossf)) bad = 1;
         col_loss += (double)lossf;
-        if (fl) store_row<FV>(V + j * F + lane * FV, v);
+        if (!part_col) {
+            if (fl) store_row<FV>(V + j * F + lane * FV, v);
 #pragma unroll
-        for (int q = 0; q < KPL; ++q) {
-            const int k = lane + 32 * q;
-            if (kin[q]) {
-                W[j * K + k] = w[q];
-                C[j * K + k] = c[q];
+            for (int q = 0; q < KPL; ++q) {
+                const int k = lane + 32 * q;
+                if (kin[q]) {
+                    W[j * K + k] = w[q];
+                    C[j * K + k] = c[q];
+                }
             }
+            if (lane == 0) BHv[j] = bh;
+        } else {
+            float vd[FV], zero[FV];
+#pragma unroll
+            for (int x = 0; x < FV; ++x) {
+                vd[x] = (v[x] - my_start[x]) * inv_parts;
+                zero[x] = 0.f;
+            }
+            if (fl) add_row<FV>(V + j * F + lane * FV, vd, zero);
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) {
+                const int k = lane + 32 * q;
+                if (kin[q]) {
+                    atomicAdd(W + j * K + k, (w[q] - my_start[FV + q]) * inv_parts);
+                    atomicAdd(C + j * K + k, (c[q] - my_start[FV + KPL + q]) * inv_parts);
+                }
+            }
+            if (lane == 0) atomicAdd(BHv + j, (bh - my_start[FV + 2 * KPL]) * inv_parts);
         }
-        if (lane == 0) BHv[j] = bh;
         __syncwarp();
     }
     if (lane == 0) {
@@ -1035,7 +1083,8 @@ extern "C" int culsh_pack_stream(int64_t N, const int64_t *col_ptr, const int32_
     return CULSH_OK;
 }
 
-extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const uint32_t *packed,
+extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
+                                              const uint32_t *packed,
                                               const float *lut, const int64_t *mptr, const uint32_t *cmask,
                                               const int64_t *resid_ptr, const float *resid,
                                               const int32_t *col_order, CulshModel32 *m, const CulshRates *r,
@@ -1046,6 +1095,7 @@ extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col
     CULSH_REQUIRE((F >= 1 && F <= 32) || F == 64 || F == 128 || F == 256,
                   "Hogwild mode needs F <= 32 or F in {64, 128, 256}");
     CULSH_REQUIRE((flags & 4) == 0, "the packed stream does not run the sub-warp kernel");
+    CULSH_REQUIRE(seg == nullptr || (flags & 8), "the packed stream takes whole columns or work segments");
     if (N_list <= 0) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
@@ -1054,8 +1104,8 @@ extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col
              (float)(1.0 - r->gv * r->lv), (float)(1.0 - r->gw * r->lw), (float)(1.0 - r->gc * r->lc)};
     const bool k2 = K > 32;
     const int32_t *rows = reinterpret_cast<const int32_t *>(packed);
-#define HWP(FVv) (k2 ? launch_hogwild<FVv, 2, true>(N_list, col_ptr, nullptr, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr) \
-                     : launch_hogwild<FVv, 1, true>(N_list, col_ptr, nullptr, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr))
+#define HWP(FVv) (k2 ? launch_hogwild<FVv, 2, true>(N_list, col_ptr, seg, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr) \
+                     : launch_hogwild<FVv, 1, true>(N_list, col_ptr, seg, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr))
     if (F <= 32) return HWP(1);
     if (F == 64) return HWP(2);
     if (F == 128) return HWP(4);

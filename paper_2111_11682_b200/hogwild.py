@@ -63,7 +63,7 @@ class HogwildTrainer:
     def __init__(self, ratings, neighbors: NeighborTable | None, config: TrainConfig,
                  dev=None, params: ModelParams | None = None, rotate: bool = False,
                  max_warps: int | None = None, atomic_rows: bool = True, subwarp: bool = False,
-                 packed: bool = True):
+                 packed: bool = True, split: bool = True, split_cap: int | None = None):
         config.validate()
         self.rotate = rotate
         self.atomic_rows = atomic_rows
@@ -112,6 +112,7 @@ class HogwildTrainer:
         self.status = nat.zeros((1,), "int32")
         self.loss = nat.zeros((1,), "float64")
         self.packed = self._build_packed() if (packed and not subwarp) else None
+        self.work = self._build_work_list(split_cap) if (split and not subwarp) else None
 
     def _build_packed(self):
         """Packed rating stream (culsh_pack_stream): 4 B per rating + mask words of the
@@ -143,6 +144,40 @@ class HogwildTrainer:
             return None
         return {"words": words, "cmask": cmask, "mptr": mptr, "lut": lut}
 
+    def _build_work_list(self, cap: int | None = None):
+        """Work segments for skewed data: a column longer than the average work of a
+        resident warp (nnz / warps) would bound the epoch by its sequential chain, so it is
+        split into S segments of at most that length, run by different warps concurrently,
+        each from the column's current parameters; each adds 1/S of its change to the
+        column parameters (parameter averaging: a plain sum would apply every segment's
+        pull on v_j at full strength and overshoot).  None when no column is that long."""
+        d = self.dev
+        if d.N == 0 or d.nnz == 0:
+            return None
+        t = nat.torch()
+        if cap is None:
+            warps = 32 * t.cuda.get_device_properties(nat.device()).multi_processor_count
+            # a lone warp runs a chain ~3-4x faster than a fully loaded SM does, so a column
+            # up to 2x the mean per-warp work still finishes within the epoch
+            cap = max(1024, 2 * -(-d.nnz // warps))
+        col_ptr = nat.to_host(d.col_ptr).astype(np.int64)
+        cnt = np.diff(col_ptr)
+        if cnt.max() <= cap:
+            return None
+        nseg = np.maximum(1, -(-cnt // cap))
+        col = np.repeat(np.arange(d.N, dtype=np.int64), nseg)
+        first = np.repeat(np.cumsum(nseg) - nseg, nseg)
+        part = np.arange(len(col)) - first                   # segment index within its column
+        ns = nseg[col]
+        lo = col_ptr[col] + (cnt[col] * part) // ns
+        hi = col_ptr[col] + (cnt[col] * (part + 1)) // ns
+        order = np.argsort(-(hi - lo), kind="stable")       # longest first
+        # segment end carries the column's segment count S in bits 40-63 (1/S-averaged merge)
+        seg = np.stack([lo[order], hi[order] | (ns[order].astype(np.int64) << 40)], axis=1).reshape(-1)
+        return {"n": len(order), "col": nat.to_dev(col[order].astype(np.int32), np.int32),
+                "seg": nat.to_dev(seg.astype(np.int64), np.int64), "cap": int(cap),
+                "split_cols": int((nseg > 1).sum())}
+
     def kernel_name(self) -> str:
         """The epoch kernel a whole-matrix launch_epoch runs (for reports)."""
         F, K = self.config.F, self.K
@@ -168,24 +203,28 @@ class HogwildTrainer:
         d = self.dev
         order = self.col_order if col_order is None else col_order
         n = d.N if n_cols is None else n_cols
-        if self.packed is not None and seg is None:
+        wflag = 0
+        if seg is None and col_order is None and self.work is not None:
+            order, seg, n, wflag = self.work["col"], self.work["seg"], self.work["n"], 8
+        if self.packed is not None and (seg is None or wflag):
             pk = self.packed
-            self._launch_packed(n, pk["words"], pk["cmask"], self.resid, order, rates, self.loss)
+            self._launch_packed(n, pk["words"], pk["cmask"], self.resid, order, rates, self.loss, seg)
             return
         nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(d.col_rows),
                  nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
                  nat.ptr(self.resid), nat.ptr(order), ctypes.byref(self.model.struct),
-                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0),
+                 ctypes.byref(rates),
+                 int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0) | wflag,
                  int(self.max_warps), nat.ptr(self.ticket),
                  nat.ptr(self.loss),
                  nat.ptr(self.status), nat.stream_ptr())
 
-    def _launch_packed(self, n, words, cmask, resid, order, rates, loss) -> None:
+    def _launch_packed(self, n, words, cmask, resid, order, rates, loss, seg=None) -> None:
         pk, d = self.packed, self.dev
-        nat.call("culsh_sgd_hogwild_epoch_packed", n, nat.ptr(d.col_ptr), nat.ptr(words), nat.ptr(pk["lut"]),
-                 nat.ptr(pk["mptr"]), nat.ptr(cmask), nat.ptr(self.resid_ptr), nat.ptr(resid), nat.ptr(order),
-                 ctypes.byref(self.model.struct), ctypes.byref(rates),
-                 int(self.rotate) | (2 if self.atomic_rows else 0),
+        nat.call("culsh_sgd_hogwild_epoch_packed", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(words),
+                 nat.ptr(pk["lut"]), nat.ptr(pk["mptr"]), nat.ptr(cmask), nat.ptr(self.resid_ptr), nat.ptr(resid),
+                 nat.ptr(order), ctypes.byref(self.model.struct), ctypes.byref(rates),
+                 int(self.rotate) | (2 if self.atomic_rows else 0) | (8 if seg is not None else 0),
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss), nat.ptr(self.status),
                  nat.stream_ptr())
 
@@ -213,15 +252,18 @@ class HogwildTrainer:
         c = self.config
         rates = _rates_struct(c.rates_at(t_epoch), c.regs)
         d = self.dev
+        order, seg, n, wflag = self.col_order, None, d.N, 0
+        if self.work is not None:
+            order, seg, n, wflag = self.work["col"], self.work["seg"], self.work["n"], 8
         if self.packed is not None:
             words, cmask, resid = bufs
-            self._launch_packed(d.N, words, cmask, resid, self.col_order, rates, loss)
+            self._launch_packed(n, words, cmask, resid, order, rates, loss, seg)
             return
         rows_b, vals_b, mask_b, resid_b = bufs
-        nat.call("culsh_sgd_hogwild_epoch", d.N, nat.ptr(d.col_ptr), None, nat.ptr(rows_b),
+        nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(rows_b),
                  nat.ptr(vals_b), nat.ptr(mask_b), nat.ptr(self.resid_ptr), nat.ptr(resid_b),
-                 nat.ptr(self.col_order), ctypes.byref(self.model.struct), ctypes.byref(rates),
-                 int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0),
+                 nat.ptr(order), ctypes.byref(self.model.struct), ctypes.byref(rates),
+                 int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0) | wflag,
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss),
                  nat.ptr(self.status), nat.stream_ptr())
 

@@ -41,8 +41,9 @@ if "--stress" in sys.argv:
         print("rotate", rotate, "diverged", fails, flush=True)
     sys.exit(0)
 for packed in (True,):
-    for atomic, rotate in ((True, False), (True, True)):
-        h = HogwildTrainer(tr, nbr, cfg, packed=packed, atomic_rows=atomic, rotate=rotate)
+    for atomic, rotate, split in ((True, False, False), (True, False, True)):
+        h = HogwildTrainer(tr, nbr, cfg, packed=packed, atomic_rows=atomic, rotate=rotate, split=split)
+        print("work list:", None if h.work is None else {k: v for k, v in h.work.items() if k in ("n", "cap", "split_cols")})
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = []
@@ -53,6 +54,6 @@ for packed in (True,):
             out.append((float(h.loss.item()) / d.nnz, int(h.status.item())))
         ms = (time.perf_counter() - t0) / 3 * 1e3
         p = h.to_params()
-        print("packed", h.packed is not None, "atomic", atomic, "rotate", rotate, "ms/epoch %.2f" % ms, out,
+        print("packed", h.packed is not None, "atomic", atomic, "rotate", rotate, "split", split, "ms/epoch %.2f" % ms, out,
               "finite U", bool(np.isfinite(p.U).all()), "max|U|", float(np.nanmax(np.abs(p.U))),
               "max|V|", float(np.nanmax(np.abs(p.V))), "max|C|", float(np.nanmax(np.abs(p.C))), flush=True)
