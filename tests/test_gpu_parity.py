@@ -492,6 +492,42 @@ class TestPackedStream:
             res.append(P.rmse(tr.to_params(), r.triplets(), r))
         assert res[1] <= res[0] + 0.015, res
 
+    @pytest.mark.parametrize("K", [16, 40])
+    def test_explicit_stream_matches_host(self, P, K):
+        """Explicit-neighbour masks and residuals (shared-memory intersection for columns
+        up to 6,144 ratings, per-rating search above) equal a host restatement of
+        factorization.py:287-298's test and residual, bit for bit."""
+        from paper_2111_11682_b200 import _native as nat
+        from paper_2111_11682_b200.hogwild import HogwildTrainer
+        rng = np.random.default_rng(5)
+        M, N = 9000, 50
+        mask = rng.random((M, N)) < 0.05
+        mask[:7000, 3] = True                      # one column above the shared-memory cap
+        rows, cols = np.nonzero(mask)
+        r = P.SparseRatings(M, N, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+        tbl, _ = P.simlsh_topk(r, P.LshConfig(q=20), K)
+        tr = HogwildTrainer(r, tbl, P.TrainConfig(F=64, K=K, epochs=1, seed=0))
+        d = tr.dev
+        mu, bb, bh = d.mu, nat.to_host(d.base_b), nat.to_host(d.base_bhat)
+        MW = tr.MW
+        got_m = nat.to_host(tr.mask).view(np.uint32)[:r.nnz * MW].reshape(r.nnz, MW)
+        got_r = nat.to_host(tr.resid)[:tr.n_explicit]
+        exp_m = np.zeros((r.nnz, MW), np.uint32)
+        exp_r = []
+        dense = {(int(i), int(j)): v for i, j, v in zip(r.entry_rows, r.entry_cols, r.entry_values)}
+        for j in range(N):
+            for e in range(r.col_ptr[j], r.col_ptr[j + 1]):
+                i = int(r.col_rows[e])
+                for k in range(K):
+                    J = int(tbl.entries[j, k])
+                    v = dense.get((i, J))
+                    if v is not None:
+                        exp_m[e, k >> 5] |= np.uint32(1 << (k & 31))
+                        exp_r.append(np.float32(v - (mu + bb[i] + bh[J])))
+        assert np.array_equal(got_m, exp_m)
+        assert np.array_equal(got_r, np.array(exp_r, np.float32))
+        assert tr.n_explicit == len(exp_r)
+
     def test_host_stream_epochs(self, P):
         """train_from_host (per-epoch H2D of the packed stream) == device-resident epochs
         in expectation: same loss trajectory within Hogwild noise, finite model."""
