@@ -67,6 +67,24 @@ def main():
     out.update({"c1_" + k: v for k, v in trip(train, "").items()})
     out["c1_gsm_K16"] = gsm_topk(train, SimilarityConfig(K=16)).entries
     out["c1_gsm_K32_l50"] = gsm_topk(train, SimilarityConfig(K=32, lambda_rho=50.0)).entries
+    # checkpoint / hash-state binary formats (factorization.py:154-185, lsh.py:209-228)
+    from lshmf.factorization import ModelParams
+    from lshmf.lsh import LshConfig, compute_hash_state
+    from lshmf.similarity import NeighborTable
+    g = np.random.default_rng(3)
+    nb = NeighborTable(N=6, K=2, entries=np.array([[1, 2], [0, 2], [0, 1], [4, 5], [3, 5], [3, 4]], np.int32))
+    mp = ModelParams(mu=3.25, b=g.random(7), b_hat=g.random(6), U=g.random((7, 4)), V=g.random((6, 4)),
+                     W=g.random((6, 2)), C=g.random((6, 2)), neighbors=nb)
+    for k in ("b", "b_hat", "U", "V", "W", "C"):
+        out["mp_" + k] = getattr(mp, k)
+    out["mp_entries"] = nb.entries
+    r0 = cases[0][1]
+    hs = compute_hash_state(r0, LshConfig(G=8, p=3, q=7, psi_exponent=2, seed=4))
+    with tempfile.TemporaryDirectory() as d:
+        mp.save(os.path.join(d, "m.bin"))
+        out["mp_bytes"] = np.frombuffer(open(os.path.join(d, "m.bin"), "rb").read(), dtype=np.uint8)
+        hs.save(os.path.join(d, "h.bin"))
+        out["hs_bytes"] = np.frombuffer(open(os.path.join(d, "h.bin"), "rb").read(), dtype=np.uint8)
     out["rand_2_1_0"] = random_topk(2, 1, seed=0).entries
     out["rand_50_5_9"] = random_topk(50, 5, seed=9).entries
     out["rand_1682_16_0"] = random_topk(1682, 16, seed=0).entries

@@ -786,3 +786,15 @@ class TestGsm:
         assert np.array_equal(a, b)
         ref = orc.gsm_topk(r.col_ptr, r.col_rows, r.col_vals, N, 32, 100.0)
         assert np.array_equal(a, ref)
+
+
+def test_hash_state_file_bytes_match_reference(P, tmp_path):
+    """compute_hash_state on the GPU + HashState.save == the reference's file bytes
+    (lsh.py:209-216), and load re-thresholds to the same state."""
+    z = load_golden("similarity.npz")
+    r = _sim_ratings(P, z, "int_")
+    hs = P.compute_hash_state(r, P.LshConfig(G=8, p=3, q=7, psi_exponent=2, seed=4))
+    hs.save(tmp_path / "h.bin")
+    assert (tmp_path / "h.bin").read_bytes() == z["hs_bytes"].tobytes()
+    back = P.HashState.load(tmp_path / "h.bin")
+    assert back.sig.tobytes() == hs.sig.tobytes()

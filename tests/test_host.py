@@ -156,3 +156,15 @@ def test_lshmfr_format_byte_identical(tmp_path):
     bad.write_text("NOPE v1 1 1 0\n")
     with pytest.raises(ValueError):
         P.SparseRatings.load(bad)
+
+
+def test_checkpoint_bytes_match_reference(tmp_path):
+    """ModelParams.save writes the reference's LSHMF-M bytes (factorization.py:154-161)."""
+    import paper_2111_11682_b200 as P
+    z = load_golden("similarity.npz")
+    nb = P.NeighborTable(6, 2, z["mp_entries"])
+    p = P.ModelParams(3.25, z["mp_b"], z["mp_b_hat"], z["mp_U"], z["mp_V"], z["mp_W"], z["mp_C"], nb)
+    p.save(tmp_path / "m.bin")
+    assert (tmp_path / "m.bin").read_bytes() == z["mp_bytes"].tobytes()
+    q = P.ModelParams.load(tmp_path / "m.bin")
+    assert q.V.tobytes() == p.V.tobytes()
