@@ -353,6 +353,8 @@ def run_gpu(args):
                    "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic), "kernel": args.kernel,
                    "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
         "lsh_build_s": lsh_s, "lsh_build_runs_s": lsh_runs, "lsh_candidates": ncand,
+        # the simLSH build's work is nnz*p*q*G signed accumulations
+        "lsh_accumulations_per_s": float(nnz) * lcfg.p * lcfg.q * lcfg.G / lsh_s,
         "prep_s": t_prep, "datagen_s": t_gen, "train_rmse_running": train_rmse,
         "epoch_ms": [p * 1e3 for p in per],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
