@@ -297,7 +297,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     t_prep = time.perf_counter()
     tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params, rotate=bool(args.rotate),
-                        atomic_rows=bool(args.atomic), subwarp=args.kernel == "subwarp",
+                        atomic_rows=bool(args.atomic),
                         packed=bool(args.packed))
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t_prep
@@ -350,7 +350,7 @@ def run_gpu(args):
         "data": "synthetic (random_sparse distribution generated in HBM, integer stars 1-5)",
         "config": {"workload": WORKLOAD[args.config], "M": M, "N": N, "nnz": nnz, "F": F, "K": K,
                    "mode": "hogwild fp32, warp per column", "stream": "packed" if tr.packed is not None else "wide",
-                   "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic), "kernel": args.kernel,
+                   "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic),
                    "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
         "lsh_build_s": lsh_s, "lsh_build_runs_s": lsh_runs, "lsh_candidates": ncand,
         # the simLSH build's work is nnz*p*q*G signed accumulations
@@ -402,9 +402,6 @@ def main():
     ap.add_argument("--atomic", type=int, default=1, help="row updates as atomic adds")
     ap.add_argument("--packed", type=int, default=1,
                     help="packed rating stream (4 B/rating + compact masks) instead of rows/vals/masks")
-    ap.add_argument("--kernel", default="warp", choices=["warp", "subwarp"],
-                    help="Hogwild kernel: a warp per column (default; packed stream) or the generic "
-                         "16-lanes-per-column kernel (wide stream)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -210,7 +210,7 @@ int culsh_explicit_stream(const CulshData *d, double mu, const int32_t *nbr, int
  * value.  flags bit 0: start each column at a per-column hashed offset (warps
  * sweep rows out of phase: fewer concurrent writes to one u_i); bit 1: apply
  * row updates as vector atomic adds of the delta (no lost updates); bit 2: the
- * sub-warp kernel (16 lanes per column) instead of warp-per-column; bit 3: seg is
+ * reserved (must be 0); bit 3: seg is
  * indexed by ticket (work segments: list entry t = column col_order[t], entries
  * [seg[2t], seg[2t+1] & (2^40-1)), S = seg[2t+1] >> 40 segments in that column; a
  * segment of a split column (S > 1) runs concurrently with the column's other
@@ -241,8 +241,7 @@ int culsh_pack_stream(int64_t N, const int64_t *col_ptr, const int32_t *rows, co
 
 /* culsh_sgd_hogwild_epoch over the packed stream (warp per column or per work
  * segment; flags bits 0, 1, 3 as there -- seg must be NULL or a per-ticket work
- * segment list -- no sub-warp kernel).  Identical updates to the wide-stream
- * kernel on the same data. */
+ * segment list).  Identical updates to the wide-stream kernel on the same data. */
 int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
                                    const uint32_t *packed,
                                    const float *lut, const int64_t *mptr, const uint32_t *cmask,

@@ -523,328 +523,6 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
     }
 }
 
-// ---- sub-warp variant ---------------------------------------------------------
-//
-// G lanes own one column (32/G columns per warp), each lane FV = F/G factors and
-// KPL = ceil(K/G) neighbour slots.  All per-update scalar work (metadata read,
-// prefetch issue, the error, bias updates, loop control) is issued once per warp
-// instruction for 32/G updates, and the reduction needs log2(G) shuffles, so the
-// instruction count per update drops roughly by the number of columns per warp.
-// Each sub-group streams its own column exactly like hogwild_kernel (cp.async
-// u-row ring kHwDepth deep, 64-entry metadata window) and fetches its next
-// column from the ticket independently.
-
-constexpr int kSgDepth = 4;   // u-row prefetch depth per sub-group (smem bounds occupancy)
-
-template <int G, int FV, int KPL, int MW>
-struct SgLayout {
-    static constexpr int kMeta = 64 * 16;                 // int4 {row, value, mask0, resid off}
-    static constexpr int kMeta1 = MW == 2 ? 64 * 4 : 0;   // mask word 1
-    static constexpr int kRing = kSgDepth * G * FV * 4;   // u rows
-    static constexpr int kBRing = kSgDepth * 4;           // b_i
-    static constexpr int kSub = kMeta + kMeta1 + kRing + kBRing;
-    static constexpr int kWarp = (32 / G) * kSub;
-};
-
-template <int G>
-__device__ __forceinline__ float sub_sum(float v) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-template <int G, int FV, int KPL, int MW, bool ATOMIC>
-__global__ void __launch_bounds__(kHwWarps * 32)
-hogwild_sg_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__restrict__ seg,
-                  const int32_t *__restrict__ rows, const float *__restrict__ vals,
-                  const uint32_t *__restrict__ mask, const int64_t *__restrict__ resid_ptr,
-                  const float *__restrict__ resid, const int32_t *__restrict__ col_order, float mu,
-                  float *__restrict__ Bv, float *__restrict__ BHv, float *__restrict__ U,
-                  float *__restrict__ V, float *__restrict__ W, float *__restrict__ C, int K, HwCoef R,
-                  int rotate, int *__restrict__ ticket, double *__restrict__ loss,
-                  int *__restrict__ status) {
-    using L = SgLayout<G, FV, KPL, MW>;
-    constexpr int P = kSgDepth;
-    constexpr int F = G * FV;
-    extern __shared__ __align__(16) unsigned char s_raw[];
-    const unsigned lane = lane_id();
-    const int sub = (int)lane / G;
-    const int sl = (int)lane % G;
-    const int sub0 = sub * G;   // first lane of my sub-group
-    const int warp = threadIdx.x >> 5;
-    unsigned char *sbase = s_raw + (size_t)warp * L::kWarp + (size_t)sub * L::kSub;
-    int4 *s_meta = reinterpret_cast<int4 *>(sbase);
-    uint32_t *s_m1 = reinterpret_cast<uint32_t *>(sbase + L::kMeta);
-    float *s_ring = reinterpret_cast<float *>(sbase + L::kMeta + L::kMeta1);
-    float *s_bring = reinterpret_cast<float *>(sbase + L::kMeta + L::kMeta1 + L::kRing);
-    float *my_ring = s_ring + sl * FV;
-    const float *Ulane = U + sl * FV;
-    const float invK = K > 0 ? rsqrtf((float)K) : 0.f;
-    const unsigned below = (1u << (unsigned)sl) - 1u;   // lane bits below me inside k-slot word q
-
-    double tot_loss = 0.0;
-    int bad = 0;
-
-    // per-sub column state (replicated in the sub's lanes)
-    bool alive = true;
-    int n = 0, t = 0, rot = 0;
-    int64_t j = 0, lo = 0;
-    int rrel1 = 0, rrel2 = 0;
-    const float *rcol = resid;
-    float v[FV], w[KPL], c[KPL];
-    float bh = 0.f, lossf = 0.f;
-#pragma unroll
-    for (int x = 0; x < FV; ++x) v[x] = 0.f;
-#pragma unroll
-    for (int q = 0; q < KPL; ++q) { w[q] = 0.f; c[q] = 0.f; }
-
-    // metadata for processing indices [32*ch, 32*ch+32) of the current column; each
-    // lane loads 32/G entries; residual offsets by a segmented prefix (rotation wraps
-    // the column into segment 1 = [rot, n) then segment 2 = [0, rot))
-    auto load_chunk = [&](int ch, bool act) {
-        constexpr int E = 32 / G;
-        int pc[E], seg2[E];
-        int ri[E];
-        float rv[E];
-        uint32_t m0[E], m1[E];
-        int loc1 = 0, loc2 = 0;
-#pragma unroll
-        for (int u = 0; u < E; ++u) {
-            const int k = 32 * ch + sl * E + u;
-            const bool have = act && k < n;
-            int pos = k + rot;
-            seg2[u] = pos >= n;
-            if (seg2[u]) pos -= n;
-            const int64_t e = lo + pos;
-            ri[u] = have ? rows[e] : 0;
-            rv[u] = have ? vals[e] : 0.f;
-            m0[u] = have ? mask[e * MW] : 0u;
-            m1[u] = (MW == 2 && have) ? mask[e * MW + 1] : 0u;
-            pc[u] = __popc(m0[u]) + __popc(m1[u]);
-            if (!have) pc[u] = 0;
-            if (seg2[u]) loc2 += pc[u]; else loc1 += pc[u];
-        }
-        // exclusive scan of (loc1, loc2) over the sub-group's lanes
-        int i1 = loc1, i2 = loc2;
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) {
-            const int y1 = __shfl_up_sync(0xffffffffu, i1, o, G);
-            const int y2 = __shfl_up_sync(0xffffffffu, i2, o, G);
-            if (sl >= o) { i1 += y1; i2 += y2; }
-        }
-        int e1 = rrel1 + i1 - loc1, e2 = rrel2 + i2 - loc2;
-#pragma unroll
-        for (int u = 0; u < E; ++u) {
-            const int roff = seg2[u] ? e2 : e1;
-            if (seg2[u]) e2 += pc[u]; else e1 += pc[u];
-            const int slot = (32 * ch + sl * E + u) & 63;
-            if (act) {
-                s_meta[slot] = make_int4(ri[u], __float_as_int(rv[u]), (int)m0[u], roff);
-                if constexpr (MW == 2) s_m1[slot] = m1[u];
-            }
-        }
-        rrel1 += __shfl_sync(0xffffffffu, i1, sub0 + G - 1);
-        rrel2 += __shfl_sync(0xffffffffu, i2, sub0 + G - 1);
-    };
-    auto issue = [&](int tp) {
-        const int ip = s_meta[tp & 63].x;
-        cp_async_row<FV>(my_ring + (tp % P) * G * FV, Ulane + (size_t)(unsigned)ip * (unsigned)F);
-        if (sl == 0) cp_async_bytes4(s_bring + (tp % P), Bv + ip);
-    };
-
-    for (;;) {
-        // ---- sub-groups whose column is finished fetch the next one ----
-        const bool need = alive && t >= n;
-        if (__any_sync(0xffffffffu, need)) {
-            if (need && n > 0) {   // retire the finished column
-                cp_async_wait<0>();
-                if (!isfinite(lossf)) bad = 1;
-                if (sl == 0) tot_loss += (double)lossf;
-                store_row<FV>(V + j * F + sl * FV, v);
-#pragma unroll
-                for (int q = 0; q < KPL; ++q) {
-                    const int k = sl + G * q;
-                    if (k < K) { W[j * K + k] = w[q]; C[j * K + k] = c[q]; }
-                }
-                if (sl == 0) BHv[j] = bh;
-            }
-            int tk = 0;
-            if (need && sl == 0) tk = atomicAdd(ticket, 1);
-            tk = __shfl_sync(0xffffffffu, tk, sub0);
-            if (need) {
-                if (tk >= N) {
-                    alive = false;
-                    n = 0;
-                    t = 0;
-                } else {
-                    j = col_order ? (int64_t)col_order[tk] : (int64_t)tk;
-                    load_row<FV>(V + j * F + sl * FV, v);
-#pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
-                        const int k = sl + G * q;
-                        w[q] = k < K ? W[j * K + k] : 0.f;
-                        c[q] = k < K ? C[j * K + k] : 0.f;
-                    }
-                    bh = BHv[j];
-                    const int64_t c_lo = col_ptr[j];
-                    lo = seg ? seg[2 * j] : c_lo;
-                    const int64_t hi = seg ? seg[2 * j + 1] : col_ptr[j + 1];
-                    n = (int)(hi - lo);
-                    t = 0;
-                    lossf = 0.f;
-                    rcol = resid + resid_ptr[j];
-                    rot = (rotate && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
-                    // residual offsets at positions lo and lo + rot (relative to the column base)
-                    int s2 = 0, s1 = 0;
-                    for (int64_t x = c_lo + sl; x < lo + rot; x += G) {
-                        int pcx = 0;
-#pragma unroll
-                        for (int q = 0; q < MW; ++q) pcx += __popc(mask[x * MW + q]);
-                        if (x < lo) s2 += pcx; else s1 += pcx;
-                    }
-                    rrel2 = s2;
-                    rrel1 = s1;
-                }
-            }
-            // sub-group sums of the skip counts (all lanes participate in the shuffles)
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) {
-                const int y2 = __shfl_xor_sync(0xffffffffu, rrel2, o);
-                const int y1 = __shfl_xor_sync(0xffffffffu, rrel1, o);
-                if (need) { rrel2 += y2; rrel1 += y1; }
-            }
-            if (need && alive) rrel1 += rrel2;
-            const bool fresh = need && alive;
-            load_chunk(0, fresh);
-            load_chunk(1, fresh && n > 32);
-            __syncwarp();
-            if (fresh) {
-#pragma unroll
-                for (int p = 0; p < P - 1; ++p) {
-                    if (p < n) issue(p);
-                    cp_async_commit();
-                }
-            }
-        }
-        if (!__any_sync(0xffffffffu, alive)) break;
-        const bool act = alive && t < n;
-
-        // ---- metadata window refill (every 32 updates of this sub's column) ----
-        const bool refill = act && (t & 31) == 0 && t > 0;
-        if (__any_sync(0xffffffffu, refill)) {
-            __syncwarp();
-            load_chunk((t >> 5) + 1, refill && t + 32 < n);
-            __syncwarp();
-        }
-
-        // ---- one update per active sub-group ----
-        float u[FV], bi = 0.f;
-        int4 me = make_int4(0, 0, 0, 0);
-        uint32_t m1 = 0;
-        if (act) {
-            if (t + P - 1 < n) issue(t + P - 1);
-            cp_async_commit();
-            cp_async_wait<P - 1>();
-            me = s_meta[t & 63];
-            if constexpr (MW == 2) m1 = s_m1[t & 63];
-            load_row<FV>(my_ring + (t % P) * G * FV, u);
-            if (sl == 0) bi = s_bring[t % P];
-        } else {
-#pragma unroll
-            for (int x = 0; x < FV; ++x) u[x] = 0.f;
-        }
-        const uint32_t m0 = (uint32_t)me.z;
-        float part = bi;
-#pragma unroll
-        for (int x = 0; x < FV; ++x) part = fmaf(u[x], v[x], part);
-        const int nr = __popc(m0) + __popc(m1);
-        const float inv_r = nr > 0 ? rsqrtf((float)nr) : 0.f;
-        const float inv_n = nr > 0 ? (K - nr > 0 ? rsqrtf((float)(K - nr)) : 0.f) : invK;
-        float rs[KPL];
-        bool ex[KPL];
-#pragma unroll
-        for (int q = 0; q < KPL; ++q) {
-            const int k = sl + G * q;                  // neighbour slot of this lane
-            const uint32_t word = (k >> 5) == 0 ? m0 : m1;
-            ex[q] = (word >> (k & 31)) & 1u;
-            int rank = __popc(word & ((1u << (k & 31)) - 1u));
-            if (k >= 32) rank += __popc(m0);
-            rs[q] = ex[q] ? rcol[me.w + rank] : 0.f;
-            part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;   // c = w = 0 for k >= K
-        }
-        part = sub_sum<G>(part);
-        if (act) {
-            const float e = __int_as_float(me.y) - (mu + bh + part);
-            lossf = fmaf(e, e, lossf);
-            const float geu = R.gu * e, gev = R.gv * e;
-            float dlt[FV];
-#pragma unroll
-            for (int x = 0; x < FV; ++x) {
-                const float uo = u[x];
-                const float un = fmaf(R.au, uo, geu * v[x]);
-                dlt[x] = un - uo;
-                u[x] = un;
-                v[x] = fmaf(R.av, v[x], gev * uo);
-            }
-            float *urow = U + (size_t)(unsigned)me.x * (unsigned)F + sl * FV;
-            if (ATOMIC) {
-#pragma unroll
-                for (int x = 0; x < FV; x += 4)
-                    atomicAdd(reinterpret_cast<float4 *>(urow + x), make_float4(dlt[x], dlt[x + 1], dlt[x + 2], dlt[x + 3]));
-                if (sl == 0) atomicAdd(Bv + me.x, fmaf(R.ab, bi, R.gb * e) - bi);
-            } else {
-                store_row<FV>(urow, u);
-                if (sl == 0) Bv[me.x] = fmaf(R.ab, bi, R.gb * e);
-            }
-            bh = fmaf(R.abh, bh, R.gbh * e);
-            const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
-#pragma unroll
-            for (int q = 0; q < KPL; ++q) {
-                if (sl + G * q < K) {
-                    if (ex[q]) w[q] = fmaf(R.aw, w[q], gwe * rs[q]);
-                    else c[q] = fmaf(R.ac, c[q], gce);
-                }
-            }
-            ++t;
-        }
-    }
-    (void)below;
-    if (sl == 0 && loss) atomicAdd(loss, tot_loss);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1);
-}
-
-template <int G, int FV, int KPL, int MW, bool ATOMIC>
-int launch_hogwild_sg(int64_t N, const int64_t *col_ptr, const int64_t *seg, const int32_t *rows,
-                      const float *vals, const uint32_t *mask, const int64_t *resid_ptr, const float *resid,
-                      const int32_t *col_order, CulshModel32 *m, const HwCoef &R, int rotate, int max_warps,
-                      int *ticket, double *loss, int *status, cudaStream_t st) {
-    using L = SgLayout<G, FV, KPL, MW>;
-    auto kern = hogwild_sg_kernel<G, FV, KPL, MW, ATOMIC>;
-    const int threads = kHwWarps * 32;
-    const size_t smem = (size_t)kHwWarps * L::kWarp;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-    if (occ < 1) occ = 1;
-    constexpr int cols_per_block = kHwWarps * (32 / G);
-    int64_t blocks = (int64_t)num_sms() * occ;
-    const int64_t need = (N + cols_per_block - 1) / cols_per_block;
-    if (blocks > need) blocks = need;
-    if (max_warps > 0) {
-        const int64_t cap = (max_warps * (32 / G) + cols_per_block - 1) / cols_per_block;
-        if (blocks > cap) blocks = cap;
-    }
-    if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, threads, smem, st>>>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order,
-                                                  m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->K, R, rotate,
-                                                  ticket, loss, status);
-    return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
-}
-
 // ---- explicit-neighbour stream (one pass per fit) ---------------------------
 
 __device__ __forceinline__ int64_t find_row(const int32_t *__restrict__ rows, int64_t lo, int64_t hi,
@@ -1040,23 +718,7 @@ extern "C" int culsh_sgd_hogwild_epoch(int64_t N, const int64_t *col_ptr, const 
              (float)(1.0 - r->gb * r->lb), (float)(1.0 - r->gbh * r->lbh), (float)(1.0 - r->gu * r->lu),
              (float)(1.0 - r->gv * r->lv), (float)(1.0 - r->gw * r->lw), (float)(1.0 - r->gc * r->lc)};
     const bool k2 = K > 32;
-    const int rotate = flags & 1;
-    const bool atomic_rows = (flags & 2) != 0;
-    if ((flags & 4) && (F == 32 || F == 64 || F == 128 || F == 256)) {
-        // sub-warp kernel (opt-in): G lanes per column
-#define SG(Gv, FVv, KPLv, MWv)                                                                        \
-    (atomic_rows ? launch_hogwild_sg<Gv, FVv, KPLv, MWv, true>(N, col_ptr, seg, rows, vals, mask, resid_ptr,   \
-                                                              resid, col_order, m, R, rotate, max_warps,      \
-                                                              ticket, loss_out, status, st)                   \
-                 : launch_hogwild_sg<Gv, FVv, KPLv, MWv, false>(N, col_ptr, seg, rows, vals, mask, resid_ptr,  \
-                                                               resid, col_order, m, R, rotate, max_warps,     \
-                                                               ticket, loss_out, status, st))
-        if (F == 32) return k2 ? SG(8, 4, 8, 2) : SG(8, 4, 4, 1);
-        if (F == 64) return k2 ? SG(16, 4, 4, 2) : SG(16, 4, 2, 1);
-        if (F == 128) return k2 ? SG(16, 8, 4, 2) : SG(16, 8, 2, 1);
-        return k2 ? SG(16, 16, 4, 2) : SG(16, 16, 2, 1);
-#undef SG
-    }
+    CULSH_REQUIRE((flags & 4) == 0, "flags bit 2 (sub-warp kernel) is no longer supported");
 #define HW(FVv) (k2 ? launch_hogwild<FVv, 2>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st) \
                     : launch_hogwild<FVv, 1>(N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st))
     if (F <= 32) return HW(1);
@@ -1094,7 +756,7 @@ extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col
     CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
     CULSH_REQUIRE((F >= 1 && F <= 32) || F == 64 || F == 128 || F == 256,
                   "Hogwild mode needs F <= 32 or F in {64, 128, 256}");
-    CULSH_REQUIRE((flags & 4) == 0, "the packed stream does not run the sub-warp kernel");
+    CULSH_REQUIRE((flags & 4) == 0, "flags bit 2 (sub-warp kernel) is no longer supported");
     CULSH_REQUIRE(seg == nullptr || (flags & 8), "the packed stream takes whole columns or work segments");
     if (N_list <= 0) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;

@@ -62,12 +62,11 @@ class HogwildTrainer:
 
     def __init__(self, ratings, neighbors: NeighborTable | None, config: TrainConfig,
                  dev=None, params: ModelParams | None = None, rotate: bool = False,
-                 max_warps: int | None = None, atomic_rows: bool = True, subwarp: bool = False,
+                 max_warps: int | None = None, atomic_rows: bool = True,
                  packed: bool = True, split: bool = True, split_cap: int | None = None):
         config.validate()
         self.rotate = rotate
         self.atomic_rows = atomic_rows
-        self.subwarp = subwarp   # 16-lanes-per-column kernel instead of warp per column
         self.config = config
         self.neighbors = neighbors
         K = neighbors.K if neighbors is not None else 0
@@ -111,8 +110,8 @@ class HogwildTrainer:
         self.ticket = nat.zeros((1,), "int32")
         self.status = nat.zeros((1,), "int32")
         self.loss = nat.zeros((1,), "float64")
-        self.packed = self._build_packed() if (packed and not subwarp) else None
-        self.work = self._build_work_list(split_cap) if (split and not subwarp) else None
+        self.packed = self._build_packed() if packed else None
+        self.work = self._build_work_list(split_cap) if split else None
 
     def _build_packed(self):
         """Packed rating stream (culsh_pack_stream): 4 B per rating + mask words of the
@@ -182,8 +181,6 @@ class HogwildTrainer:
         """The epoch kernel a whole-matrix launch_epoch runs (for reports)."""
         F, K = self.config.F, self.K
         at = str(bool(self.atomic_rows)).lower()
-        if self.subwarp:
-            return "hogwild_sg_kernel"
         fv = 1 if F <= 32 else F // 32
         return "hogwild_kernel<%d,%d,%s,%s>" % (fv, self.MW, at, str(self.packed is not None).lower())
 
@@ -214,7 +211,7 @@ class HogwildTrainer:
                  nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
                  nat.ptr(self.resid), nat.ptr(order), ctypes.byref(self.model.struct),
                  ctypes.byref(rates),
-                 int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0) | wflag,
+                 int(self.rotate) | (2 if self.atomic_rows else 0) | wflag,
                  int(self.max_warps), nat.ptr(self.ticket),
                  nat.ptr(self.loss),
                  nat.ptr(self.status), nat.stream_ptr())
@@ -263,7 +260,7 @@ class HogwildTrainer:
         nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(rows_b),
                  nat.ptr(vals_b), nat.ptr(mask_b), nat.ptr(self.resid_ptr), nat.ptr(resid_b),
                  nat.ptr(order), ctypes.byref(self.model.struct), ctypes.byref(rates),
-                 int(self.rotate) | (2 if self.atomic_rows else 0) | (4 if self.subwarp else 0) | wflag,
+                 int(self.rotate) | (2 if self.atomic_rows else 0) | wflag,
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss),
                  nat.ptr(self.status), nat.stream_ptr())
 
