@@ -798,3 +798,51 @@ def test_hash_state_file_bytes_match_reference(P, tmp_path):
     assert (tmp_path / "h.bin").read_bytes() == z["hs_bytes"].tobytes()
     back = P.HashState.load(tmp_path / "h.bin")
     assert back.sig.tobytes() == hs.sig.tobytes()
+
+
+class TestEdgeCases:
+    def test_gsm_empty_columns_negative_values_full_k(self, P, orc):
+        """Empty columns, negative integer ratings, K = N-1: both GSM routes == oracle."""
+        rng = np.random.default_rng(9)
+        M, N = 120, 24
+        mask = rng.random((M, N)) < 0.3
+        mask[:, [3, 17]] = False                      # two empty columns
+        rows, cols = np.nonzero(mask)
+        vals = rng.integers(-11, 12, len(rows)).astype(float)
+        r = P.SparseRatings(M, N, rows, cols, vals)
+        for K in (1, N - 1):
+            ref = orc.gsm_topk(r.col_ptr, r.col_rows, r.col_vals, N, K, 100.0)
+            for meth in ("count", "merge"):
+                got = P.gsm_topk(r, P.SimilarityConfig(K=K), method=meth).entries
+                assert np.array_equal(got, ref), (K, meth)
+
+    def test_hogwild_empty_columns_and_rows(self, P):
+        """Empty columns / rows in every Hogwild stream form: parameters of untouched
+        columns keep their initial values except regularisation-free ones, and the
+        packed kernel equals the wide kernel."""
+        import torch
+        from paper_2111_11682_b200.hogwild import HogwildTrainer
+        rng = np.random.default_rng(4)
+        M, N = 400, 60
+        mask = rng.random((M, N)) < 0.1
+        mask[:, [0, 31, 59]] = False
+        mask[[5, 77], :] = False
+        rows, cols = np.nonzero(mask)
+        r = P.SparseRatings(M, N, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+        tbl, _ = P.simlsh_topk(r, P.LshConfig(q=20), 8)
+        cfg = P.TrainConfig(F=64, K=8, epochs=2, seed=0)
+        out = []
+        for packed in (True, False):
+            tr = HogwildTrainer(r, tbl, cfg, packed=packed)
+            for t in range(2):
+                for j in range(N):
+                    tr.launch_epoch(t, col_order=torch.tensor([j], dtype=torch.int32, device="cuda"), n_cols=1)
+            torch.cuda.synchronize()
+            assert int(tr.status.item()) == 0
+            out.append(tr.to_params())
+        init = P.init_params(M, N, 64, 8, tbl, r.baselines(), cfg)
+        for p in out:
+            assert np.allclose(p.V[[0, 31, 59]], init.V[[0, 31, 59]].astype(np.float32))
+            assert np.allclose(p.U[[5, 77]], init.U[[5, 77]].astype(np.float32))
+        for name in ("b", "b_hat", "U", "V", "W", "C"):
+            assert getattr(out[0], name).tobytes() == getattr(out[1], name).tobytes(), name
