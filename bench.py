@@ -92,23 +92,31 @@ class Clocks:
 
 # ------------------------------------------------------------- CPU oracle ---
 
-def cpu_baseline(dm, nbr_host, F, K, cfg_lsh, budget_s=20.0, threads=None):
-    """The reference algorithm (oracle/ C port, pinned bit-exact to the reference)
-    timed on this host's cores on a bounded sample of the same workload."""
+def cpu_baseline(shape, F, K, cfg_lsh, budget_s=20.0, threads=None):
+    """The reference algorithm (oracle/ C port, pinned bit-exact to the reference) timed
+    on this host's cores on a bounded sample of the same workload, with no GPU involved:
+    2 % of the rows of a host-generated matrix of the same shape and density (every
+    sampled row keeps its full ~nnz/M ratings, so each update's K neighbour lookups cost
+    what they cost on the full matrix), simLSH top-K of the sample, then parallel_epoch
+    (the reference's parallel_train, D = threads) over it."""
     from oracle import oracle as orc
-    from paper_2111_11682_b200 import _native as nat
+    M, N, nnz = shape
     threads = threads or (os.cpu_count() or 1)
-    d = dm.dev
-    # SGD sample: rows [0, Ms) with their complete rating lists (so the K neighbour
-    # lookups search full-length rows), every column, the GPU-built J^K.
-    row_ptr = nat.to_host(d.row_ptr)
-    Ms = max(1, min(dm.M, int(dm.M * 0.02)))
-    rows, cols, vals = (np.repeat(np.arange(Ms, dtype=np.int32), np.diff(row_ptr[:Ms + 1])),
-                        nat.to_host(d.row_cols[:int(row_ptr[Ms])]), nat.to_host(d.row_vals[:int(row_ptr[Ms])]))
-    csr, mu = orc.build_csr(Ms, dm.N, rows, cols, vals)
-    m = orc.init_model(Ms, dm.N, F, K, nbr_host, mu, csr.base_b, csr.base_bhat, 0)
+    rng = np.random.default_rng(0)
+    Ms = max(1, min(M, int(M * 0.02)))
+    counts = np.maximum(1, rng.binomial(N, nnz / (M * N), Ms))
+    key = np.unique(np.repeat(np.arange(Ms, dtype=np.int64), counts) * N +
+                    rng.integers(0, N, int(counts.sum())))
+    rows, cols = (key // N).astype(np.int32), (key % N).astype(np.int32)
+    vals = rng.integers(1, 6, len(key)).astype(np.float64)
+    csr, mu = orc.build_csr(Ms, N, rows, cols, vals)
+    G, p, q, e = cfg_lsh
+    t1 = time.perf_counter()
+    hs = orc.simlsh_topk(csr.col_ptr, csr.col_rows, csr.col_vals, Ms, G, p, q, e, 0, K, threads)
+    lsh_sample_s = time.perf_counter() - t1
+    m = orc.init_model(Ms, N, F, K, hs.entries, mu, csr.base_b, csr.base_bhat, 0)
     rates = orc.make_rates((0.02, 0.02, 0.02, 0.02, 0.001, 0.001), (0.01, 0.01, 0.01, 0.01, 0.05, 0.05))
-    D = max(1, min(threads, Ms, dm.N))
+    D = max(1, min(threads, Ms, N))
     part = orc.partition(csr, D)
     t0 = time.perf_counter()
     n_ep = 0
@@ -119,39 +127,25 @@ def cpu_baseline(dm, nbr_host, F, K, cfg_lsh, budget_s=20.0, threads=None):
             break
     sgd_s = time.perf_counter() - t0
     ups = len(rows) * n_ep / sgd_s
-    # simLSH sample: the first Nc columns with all their ratings, all p*q*G maps
-    G, p, q, e = cfg_lsh
-    col_ptr = nat.to_host(d.col_ptr)
-    Nc = max(1, min(dm.N, 200))
-    hi = int(col_ptr[Nc])
-    bits = orc.assign_bits(0, q, p, dm.M, G)
-    t1 = time.perf_counter()
-    orc.accumulate_all(col_ptr[:Nc + 1], nat.to_host(d.col_rows[:hi]), nat.to_host(d.col_vals[:hi]),
-                       bits, e, threads)
-    lsh_s = (time.perf_counter() - t1) * dm.N / Nc
     return {"value": ups, "unit": "updates/s", "cores": threads, "kind": "port",
-            "sample": (f"oracle parallel_epoch (DSGD D={D}, reference parallel_train) over rows "
-                       f"[0,{Ms}) x all {dm.N} columns = {len(rows)} ratings, {n_ep} epoch(s) in "
-                       f"{sgd_s:.1f}s; simLSH accumulate on {Nc} of {dm.N} columns, extrapolated"),
-            "lsh_build_s_extrapolated": lsh_s}
+            "sample": (f"host-generated {Ms} x {N} sample (2 % of the rows at the workload's density, "
+                       f"{len(rows)} ratings): oracle simLSH top-K in {lsh_sample_s:.2f}s, then "
+                       f"parallel_epoch (reference parallel_train, D={D}) x {n_ep} in {sgd_s:.2f}s"),
+            "lsh_build_s_extrapolated": lsh_sample_s * nnz / max(len(rows), 1)}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU implementation of the path (oracle port)."""
+    """--impl reference: the reference's CPU implementation of the path (oracle port),
+    host cores only -- no GPU is touched on this arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import torch
-    from paper_2111_11682_b200 import synth, lsh
-    from paper_2111_11682_b200 import _native as nat
-    M, N, nnz, F, K, e = synth.SHAPES[args.config]
-    dm = synth.random_sparse_device(M, N, nnz, seed=0)
-    ent, _, _ = lsh.simlsh_topk_device(dm.dev, lsh.LshConfig(psi_exponent=e), K)
-    nbr = nat.to_host(ent)[:N * K].reshape(N, K)
+    from paper_2111_11682_b200.synth import SHAPES
+    M, N, nnz, F, K, e = SHAPES[args.config]
     vals = []
     cb = None
     for s in range(args.warmup + args.steps):
-        cb = cpu_baseline(dm, nbr, F, K, (8, 3, 100, e), budget_s=8.0)
+        cb = cpu_baseline((M, N, nnz), F, K, (8, 3, 100, e), budget_s=8.0)
         if s >= args.warmup:
             vals.append(cb["value"])
     v = float(np.median(vals))
@@ -336,7 +330,7 @@ def run_gpu(args):
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(dm, nbr_host, F, K, (8, 3, 100, e), budget_s=args.cpu_budget)
+            cpu = cpu_baseline((M, N, nnz), F, K, (8, 3, 100, e), budget_s=args.cpu_budget)
         except Exception as ex:  # the CPU leg must not sink the GPU line
             cpu = {"value": None, "error": repr(ex)}
 
