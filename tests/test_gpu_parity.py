@@ -846,3 +846,75 @@ class TestEdgeCases:
             assert np.allclose(p.U[[5, 77]], init.U[[5, 77]].astype(np.float32))
         for name in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(out[0], name).tobytes() == getattr(out[1], name).tobytes(), name
+
+
+class TestApiGolden:
+    """Public functions called standalone vs the reference's outputs on stored inputs
+    (tests/golden/api.npz, tests/golden/make_golden_api.py), bit for bit."""
+
+    @pytest.fixture(scope="class")
+    def g(self, P):
+        z = load_golden("api.npz")
+        M, N = (int(x) for x in z["orig_shape"])
+        orig = P.SparseRatings(M, N, z["orig_rows"], z["orig_cols"], z["orig_vals"])
+        tbl = P.NeighborTable(N, 5, z["table"])
+        p = P.ModelParams(float(z["p_mu"]), z["p_b"].copy(), z["p_b_hat"].copy(), z["p_U"].copy(),
+                          z["p_V"].copy(), z["p_W"].copy(), z["p_C"].copy(), tbl)
+        s = z["b_shape"]
+        batch = P.IncrementBatch(int(s[0]), int(s[1]), int(s[2]), int(s[3]), z["b_rows"], z["b_cols"],
+                                 z["b_vals"])
+        lc = P.LshConfig(G=6, p=2, q=5, psi_exponent=2, seed=3)
+        cfg = P.TrainConfig(F=4, K=5, epochs=3, seed=2)
+        return z, orig, tbl, p, batch, lc, cfg
+
+    def test_baselines_predict_split_objective(self, P, g):
+        z, orig, tbl, p, batch, lc, cfg = g
+        st = P.compute_baselines(orig)
+        assert st.mu == float(z["base_mu"]) and st.b.tobytes() == z["base_b"].tobytes()
+        assert st.b_hat.tobytes() == z["base_bhat"].tobytes()
+        pairs = z["pairs"]
+        pred = np.array([P.predict(int(i), int(j), p, orig) for i, j in pairs])
+        assert pred.tobytes() == z["pred"].tobytes()
+        pc = np.array([P.predict(int(i), int(j), p, orig, clamp=(2.0, 4.0)) for i, j in pairs])
+        assert pc.tobytes() == z["pred_clamped"].tobytes()
+        for (i, j), m in zip(pairs, z["split_explicit"]):
+            s = P.split_neighbors(int(i), int(j), tbl, orig)
+            assert np.array_equal(np.flatnonzero(m), s.explicit)
+            assert np.array_equal(np.flatnonzero(m == 0), s.implicit)
+        assert P.objective_value(p, orig, cfg.regs) == float(z["objective"])
+
+    def test_sgd_update(self, P, g):
+        z, orig, tbl, p, batch, lc, cfg = g
+        q = p.copy()
+        i0, j0 = (int(x) for x in z["sgd_ij"])
+        err = P.sgd_update(i0, j0, q, tuple(z["sgd_rates"]), cfg.regs, orig)
+        assert err == float(z["sgd_err"])
+        for k in ("b", "b_hat", "U", "V", "W", "C"):
+            assert getattr(q, k).tobytes() == z["sgd_" + k].tobytes(), k
+
+    def test_parallel_train_instrumented(self, P, g):
+        z, orig, tbl, p, batch, lc, cfg = g
+        pp, rep = P.parallel_train(orig, tbl, cfg, 3, instrument=True)
+        assert [rep.stages_checked, rep.disjoint_violations, rep.epochs_checked,
+                rep.coverage_violations] == list(z["instr"])
+        assert rep.ok
+        assert pp.U.tobytes() == z["par_U"].tobytes()
+
+    def test_online_stages_standalone(self, P, g):
+        z, orig, tbl, p, batch, lc, cfg = g
+        state = P.compute_hash_state(orig, lc)
+        hashes = P.assign_row_hashes(batch.M_hat, lc)
+        se = P.update_hashes_incremental(state, batch, hashes)
+        assert se.acc.tobytes() == z["inc_acc"].tobytes()
+        ne = P.topk_for_new(se, tbl, 5, lc.seed)
+        assert np.array_equal(ne.entries, z["new_entries"])
+        re_ = P.extend_ratings(orig, batch)
+        assert np.array_equal(re_.entry_rows, z["ext_rows"]) and np.array_equal(re_.entry_cols, z["ext_cols"])
+        assert re_.entry_values.tobytes() == z["ext_vals"].tobytes()
+        pe = P.extend_params(p, batch, ne, cfg)
+        for k in ("b", "b_hat", "U", "V", "W", "C"):
+            assert getattr(pe, k).tobytes() == z["extp_" + k].tobytes(), k
+        pt = P.train_incremental(pe, batch, ne, re_, cfg)
+        assert (pt is pe) == bool(z["inc_in_place"])          # trains its argument in place
+        for k in ("b", "b_hat", "U", "V", "W", "C"):
+            assert getattr(pt, k).tobytes() == z["inc_" + k].tobytes(), k
