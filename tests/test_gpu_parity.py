@@ -848,27 +848,28 @@ class TestEdgeCases:
             assert getattr(out[0], name).tobytes() == getattr(out[1], name).tobytes(), name
 
 
+@pytest.fixture(scope="module")
+def api_case(P):
+    z = load_golden("api.npz")
+    M, N = (int(x) for x in z["orig_shape"])
+    orig = P.SparseRatings(M, N, z["orig_rows"], z["orig_cols"], z["orig_vals"])
+    tbl = P.NeighborTable(N, 5, z["table"])
+    p = P.ModelParams(float(z["p_mu"]), z["p_b"].copy(), z["p_b_hat"].copy(), z["p_U"].copy(),
+                      z["p_V"].copy(), z["p_W"].copy(), z["p_C"].copy(), tbl)
+    s = z["b_shape"]
+    batch = P.IncrementBatch(int(s[0]), int(s[1]), int(s[2]), int(s[3]), z["b_rows"], z["b_cols"],
+                             z["b_vals"])
+    lc = P.LshConfig(G=6, p=2, q=5, psi_exponent=2, seed=3)
+    cfg = P.TrainConfig(F=4, K=5, epochs=3, seed=2)
+    return z, orig, tbl, p, batch, lc, cfg
+
+
 class TestApiGolden:
     """Public functions called standalone vs the reference's outputs on stored inputs
     (tests/golden/api.npz, tests/golden/make_golden_api.py), bit for bit."""
 
-    @pytest.fixture(scope="class")
-    def g(self, P):
-        z = load_golden("api.npz")
-        M, N = (int(x) for x in z["orig_shape"])
-        orig = P.SparseRatings(M, N, z["orig_rows"], z["orig_cols"], z["orig_vals"])
-        tbl = P.NeighborTable(N, 5, z["table"])
-        p = P.ModelParams(float(z["p_mu"]), z["p_b"].copy(), z["p_b_hat"].copy(), z["p_U"].copy(),
-                          z["p_V"].copy(), z["p_W"].copy(), z["p_C"].copy(), tbl)
-        s = z["b_shape"]
-        batch = P.IncrementBatch(int(s[0]), int(s[1]), int(s[2]), int(s[3]), z["b_rows"], z["b_cols"],
-                                 z["b_vals"])
-        lc = P.LshConfig(G=6, p=2, q=5, psi_exponent=2, seed=3)
-        cfg = P.TrainConfig(F=4, K=5, epochs=3, seed=2)
-        return z, orig, tbl, p, batch, lc, cfg
-
-    def test_baselines_predict_split_objective(self, P, g):
-        z, orig, tbl, p, batch, lc, cfg = g
+    def test_baselines_predict_split_objective(self, P, api_case):
+        z, orig, tbl, p, batch, lc, cfg = api_case
         st = P.compute_baselines(orig)
         assert st.mu == float(z["base_mu"]) and st.b.tobytes() == z["base_b"].tobytes()
         assert st.b_hat.tobytes() == z["base_bhat"].tobytes()
@@ -883,8 +884,8 @@ class TestApiGolden:
             assert np.array_equal(np.flatnonzero(m == 0), s.implicit)
         assert P.objective_value(p, orig, cfg.regs) == float(z["objective"])
 
-    def test_sgd_update(self, P, g):
-        z, orig, tbl, p, batch, lc, cfg = g
+    def test_sgd_update(self, P, api_case):
+        z, orig, tbl, p, batch, lc, cfg = api_case
         q = p.copy()
         i0, j0 = (int(x) for x in z["sgd_ij"])
         err = P.sgd_update(i0, j0, q, tuple(z["sgd_rates"]), cfg.regs, orig)
@@ -892,16 +893,16 @@ class TestApiGolden:
         for k in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(q, k).tobytes() == z["sgd_" + k].tobytes(), k
 
-    def test_parallel_train_instrumented(self, P, g):
-        z, orig, tbl, p, batch, lc, cfg = g
+    def test_parallel_train_instrumented(self, P, api_case):
+        z, orig, tbl, p, batch, lc, cfg = api_case
         pp, rep = P.parallel_train(orig, tbl, cfg, 3, instrument=True)
         assert [rep.stages_checked, rep.disjoint_violations, rep.epochs_checked,
                 rep.coverage_violations] == list(z["instr"])
         assert rep.ok
         assert pp.U.tobytes() == z["par_U"].tobytes()
 
-    def test_online_stages_standalone(self, P, g):
-        z, orig, tbl, p, batch, lc, cfg = g
+    def test_online_stages_standalone(self, P, api_case):
+        z, orig, tbl, p, batch, lc, cfg = api_case
         state = P.compute_hash_state(orig, lc)
         hashes = P.assign_row_hashes(batch.M_hat, lc)
         se = P.update_hashes_incremental(state, batch, hashes)
