@@ -376,6 +376,9 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                 const uint32_t m1 = KPL == 2 ? s_m1[tt & 63] : 0u;
                 float u[FV];
                 load_row<FV>(my_ring + (tt % P) * 32 * FV, u);
+                if constexpr (FV == 1) {
+                    if (!fl) u[0] = 0.f;   // lanes >= F never fill their ring slot (garbage, maybe NaN)
+                }
                 const float bi = lane == 0 ? s_bring[tt % P] : 0.f;
                 float part;
                 if constexpr (FV % 2 == 0) {

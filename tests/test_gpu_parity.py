@@ -919,3 +919,18 @@ class TestApiGolden:
         assert (pt is pe) == bool(z["inc_in_place"])          # trains its argument in place
         for k in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(pt, k).tobytes() == z["inc_" + k].tobytes(), k
+
+
+@pytest.mark.parametrize("F,K", [(8, 8), (32, 48), (256, 64)])
+def test_hogwild_shapes_c1(P, c1, F, K):
+    """Every Hogwild kernel instantiation family (F < 32 masked lanes, K > 32 two mask
+    words, F = 256) trains to the exact mode's test RMSE within the 0.005 bar."""
+    z, tr, te = c1
+    nbr = P.NeighborTable(tr.N, 32, z["lsh_entries32"])
+    if K != 32:
+        tbl, _ = P.simlsh_topk(tr, P.LshConfig(), K)
+        nbr = tbl
+    cfg = P.TrainConfig(F=F, K=K, epochs=12, seed=0)
+    exact = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
+    hog = P.rmse(P.train_full(tr, nbr, cfg, mode="hogwild"), te, tr)
+    assert abs(hog - exact) <= REF_TOL_RMSE, (F, K, hog, exact)
