@@ -934,3 +934,24 @@ def test_hogwild_shapes_c1(P, c1, F, K):
     exact = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
     hog = P.rmse(P.train_full(tr, nbr, cfg, mode="hogwild"), te, tr)
     assert abs(hog - exact) <= REF_TOL_RMSE, (F, K, hog, exact)
+
+
+@pytest.mark.parametrize("F,K", [(128, 40), (256, 64), (1, 1)])
+def test_exact_mode_large_shapes_vs_oracle(P, orc, F, K):
+    """Exact mode at shapes the reference fixtures do not reach (F up to 256, K > 32 with
+    two mask words, F = K = 1): bit-identical to the oracle (itself pinned to the
+    reference)."""
+    rng = np.random.default_rng(F + K)
+    M, N = 90, 70
+    mask = rng.random((M, N)) < 0.2
+    rows, cols = np.nonzero(mask)
+    vals = rng.integers(1, 6, len(rows)).astype(float)
+    r = P.SparseRatings(M, N, rows, cols, vals)
+    tbl = P.random_topk(N, K, seed=1)
+    tc = P.TrainConfig(F=F, K=K, epochs=2, seed=3)
+    p = P.train_full(r, tbl, tc)
+    d, mu = orc.build_csr(M, N, rows, cols, vals)
+    m = orc.train_full(d, mu, tbl.entries, F, K, 2, 3, tc.rates_at, tc.regs)
+    assert p.U.tobytes() == m.U.tobytes() and p.V.tobytes() == m.V.tobytes()
+    assert p.W.tobytes() == m.W.tobytes() and p.C.tobytes() == m.C.tobytes()
+    assert p.b.tobytes() == m.b.tobytes() and p.b_hat.tobytes() == m.bhat.tobytes()
