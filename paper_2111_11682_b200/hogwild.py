@@ -245,13 +245,18 @@ class HogwildTrainer:
             return (self.packed["words"], self.packed["cmask"], self.resid)
         return (self.dev.col_rows, self.vals32, self.mask, self.resid)
 
-    def _launch_stream(self, bufs, t_epoch, loss) -> None:
+    def _launch_stream(self, bufs, t_epoch, loss, launch=None) -> None:
+        """One epoch (or, with ``launch`` = (order, seg, n), part of one) over the stream
+        buffers ``bufs``."""
         c = self.config
         rates = _rates_struct(c.rates_at(t_epoch), c.regs)
         d = self.dev
         order, seg, n, wflag = self.col_order, None, d.N, 0
         if self.work is not None:
             order, seg, n, wflag = self.work["col"], self.work["seg"], self.work["n"], 8
+        if launch is not None:
+            order, seg, n = launch
+            wflag = 8 if seg is not None else 0
         if self.packed is not None:
             words, cmask, resid = bufs
             self._launch_packed(n, words, cmask, resid, order, rates, loss, seg)
@@ -263,6 +268,46 @@ class HogwildTrainer:
                  int(self.rotate) | (2 if self.atomic_rows else 0) | wflag,
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss),
                  nat.ptr(self.status), nat.stream_ptr())
+
+    def _chunk_plan(self, n_chunks: int):
+        """Column ranges of ~equal rating count for a pipelined first epoch: per chunk the
+        element range of every stream array and the chunk's launch list (its columns, or
+        its work segments, in the epoch's longest-first order)."""
+        key = ("chunks", n_chunks)
+        if getattr(self, "_plan_key", None) == key:
+            return self._plan
+        t = nat.torch()
+        d = self.dev
+        col_ptr = nat.to_host(d.col_ptr).astype(np.int64)
+        rptr = nat.to_host(self.resid_ptr).astype(np.int64)
+        cb = np.unique(np.searchsorted(col_ptr, np.linspace(0, d.nnz, n_chunks + 1), side="left"))
+        cb[0], cb[-1] = 0, d.N
+        if self.work is not None:
+            wcol = nat.to_host(self.work["col"]).astype(np.int64)
+            wseg = nat.to_host(self.work["seg"]).reshape(-1, 2)
+        else:
+            order = nat.to_host(self.col_order).astype(np.int64)
+        mptr = nat.to_host(self.packed["mptr"]).astype(np.int64) if self.packed is not None else None
+        plan = []
+        for c0, c1 in zip(cb[:-1], cb[1:]):
+            if c1 <= c0:
+                continue
+            e0, e1 = int(col_ptr[c0]), int(col_ptr[c1])
+            if self.packed is not None:
+                ranges = [(e0, e1), (int(mptr[c0]) * self.MW, int(mptr[c1]) * self.MW),
+                          (int(rptr[c0]), int(rptr[c1]))]
+            else:
+                ranges = [(e0, e1), (e0, e1), (e0 * self.MW, e1 * self.MW), (int(rptr[c0]), int(rptr[c1]))]
+            if self.work is not None:
+                sel = (wcol >= c0) & (wcol < c1)
+                launch = (nat.to_dev(wcol[sel].astype(np.int32), np.int32),
+                          nat.to_dev(np.ascontiguousarray(wseg[sel]).reshape(-1), np.int64), int(sel.sum()))
+            else:
+                sel = order[(order >= c0) & (order < c1)]
+                launch = (nat.to_dev(sel.astype(np.int32), np.int32), None, len(sel))
+            plan.append((ranges, launch))
+        self._plan_key, self._plan = key, plan
+        return plan
 
     def epoch_from_host(self, host: dict, t_epoch: int):
         """One epoch whose rating stream comes from pinned host memory: H2D copy of
@@ -279,10 +324,13 @@ class HogwildTrainer:
         h2d = sum(int(v.numel() * v.element_size()) for v in host.values())
         return loss, h2d, 8 + 4
 
-    def train_from_host(self, host: dict, t_start: int, n_epochs: int):
+    def train_from_host(self, host: dict, t_start: int, n_epochs: int, first_chunks: int = 4):
         """Epochs whose rating stream comes from pinned host memory every epoch, with
         the H2D copy of epoch e+1 (copy stream, double buffer) overlapping the
         kernel of epoch e, and each epoch's loss copied back (D2H) as it finishes.
+        The first epoch, which has no earlier kernel to hide its copy behind, is
+        pipelined in ``first_chunks`` column ranges: range c's kernel runs while range
+        c+1 is copied (Hogwild order within an epoch is free).
         Returns (per-epoch sum of e^2, h2d bytes per epoch, d2h bytes per epoch)."""
         t = nat.torch()
         comp = t.cuda.current_stream()
@@ -304,9 +352,29 @@ class HogwildTrainer:
 
         for b in (0, 1):
             used[b].record(comp)
-        fill(0)
+        plan = self._chunk_plan(first_chunks) if first_chunks > 1 and n_epochs > 0 else None
+        if plan is None:
+            fill(0)
+        else:   # epoch 0: chunk c's copy on the copy stream, its kernel after it on comp
+            evs = []
+            with t.cuda.stream(cstream):
+                for ranges, _ in plan:
+                    for dst, s_, (a, z) in zip(bufs[0], src, ranges):
+                        dst[a:z].copy_(s_[a:z], non_blocking=True)
+                    ev = t.cuda.Event()
+                    ev.record(cstream)
+                    evs.append(ev)
         for e in range(n_epochs):
             b = e % 2
+            if plan is not None and e == 0:
+                if n_epochs > 1:
+                    fill(1)
+                for ev, (_, launch) in zip(evs, plan):
+                    comp.wait_event(ev)
+                    self._launch_stream(bufs[0], t_start, loss_dev[0:], launch)
+                used[0].record(comp)
+                loss_host[0:1].copy_(loss_dev[0:1], non_blocking=True)
+                continue
             comp.wait_event(copied[b])
             if e + 1 < n_epochs:
                 fill(1 - b)
