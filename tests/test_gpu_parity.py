@@ -955,3 +955,45 @@ def test_exact_mode_large_shapes_vs_oracle(P, orc, F, K):
     assert p.U.tobytes() == m.U.tobytes() and p.V.tobytes() == m.V.tobytes()
     assert p.W.tobytes() == m.W.tobytes() and p.C.tobytes() == m.C.tobytes()
     assert p.b.tobytes() == m.b.tobytes() and p.b_hat.tobytes() == m.bhat.tobytes()
+
+
+@pytest.fixture(scope="module")
+def c2_uniform(P):
+    from paper_2111_11682_b200 import _native as nat, synth
+    M, N, nnz, F, K, e = synth.SHAPES["c2"]
+    dm = synth.random_sparse_device(M, N, nnz, seed=0)
+    d = dm.dev
+    return dm, (nat.to_host(d.col_ptr), nat.to_host(d.col_rows), nat.to_host(d.col_vals)), (M, N, F, K, e)
+
+
+class TestAtScaleVsOracle:
+    """Full C2-shape parity (20M ratings), where no reference fixture exists: the GPU
+    against the oracle (pinned to the reference) on the same device-generated matrix."""
+
+    def test_simlsh_topk_c2_bit_exact(self, P, orc, c2_uniform):
+        from paper_2111_11682_b200 import _native as nat, lsh
+        dm, (cp, cr, cv), (M, N, F, K, e) = c2_uniform
+        ent, state, _ = lsh.simlsh_topk_device(dm.dev, P.LshConfig(psi_exponent=e, seed=0), K)
+        ref = orc.simlsh_topk(cp, cr, cv, M, 8, 3, 100, e, 0, K)
+        assert state.acc.tobytes() == ref.acc.tobytes()
+        assert state.sig.tobytes() == ref.sig.tobytes()
+        assert np.array_equal(nat.to_host(ent)[:N * K].reshape(N, K), ref.entries)
+
+    def test_dsgd_epoch_c2_bit_exact(self, P, orc, c2_uniform):
+        """parallel_train(D=16), one exact epoch at C2 scale == the oracle's parallel_epoch."""
+        import torch
+        from paper_2111_11682_b200 import _native as nat, lsh
+        from paper_2111_11682_b200.data import DeviceSparseRatings
+        dm, (cp, cr, cv), (M, N, F, K, e) = c2_uniform
+        d = dm.dev
+        col = torch.repeat_interleave(torch.arange(N, device="cuda"), d.col_ptr[1:] - d.col_ptr[:-1]).to(torch.int32)
+        r = DeviceSparseRatings(M, N, d.col_rows, col, d.col_vals)
+        ent, _, _ = lsh.simlsh_topk_device(r.device(), P.LshConfig(psi_exponent=e), K)
+        nbr = P.NeighborTable(N, K, nat.to_host(ent)[:N * K].reshape(N, K))
+        cfg = P.TrainConfig(F=F, K=K, epochs=1, seed=0)
+        p = P.parallel_train(r, nbr, cfg, 16)
+        rows = np.repeat(np.arange(N, dtype=np.int32), np.diff(cp))
+        csr, mu = orc.build_csr(M, N, cr, rows, cv)
+        m = orc.parallel_train(csr, mu, nbr.entries, F, K, 1, 0, cfg.rates_at, cfg.regs, 16)
+        assert p.U.tobytes() == m.U.tobytes() and p.V.tobytes() == m.V.tobytes()
+        assert p.W.tobytes() == m.W.tobytes() and p.C.tobytes() == m.C.tobytes()
