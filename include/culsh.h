@@ -326,6 +326,15 @@ int culsh_gsm_count_select(const int32_t *g_xx, const int32_t *g_rx, const int32
 int culsh_pair_similarity(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
                           int64_t j1, int64_t j2, double lambda_rho, double *out, void *stream);
 
+/* ------------------------------------------------------------- ingest --- */
+
+/* data.py:312-346 split_holdout core on HOST memory: perm is the numpy PCG64
+ * permutation the caller drew (the reference's stream); entry e is moved to the test
+ * side while fewer than n_test are taken and its row and column both keep a training
+ * entry.  in_test: nnz bytes (0/1).  Returns the number taken, or a negative error. */
+int64_t culsh_split_holdout(const int32_t *entry_rows, const int32_t *entry_cols, int64_t nnz, int64_t M,
+                            int64_t N, const int64_t *perm, int64_t n_test, uint8_t *in_test);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,7 @@ _SIGS = {
     "culsh_gsm_densify_rows": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
     "culsh_gsm_count_select": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_pair_similarity": [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp],
+    "culsh_split_holdout": [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp],
     "culsh_rmse": [_P(CulshData), _P(CulshModel64), _vp, _vp, _vp, _i64, _i32, _f64, _f64, _f64,
                    _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
@@ -105,7 +106,8 @@ _SIGS = {
     "culsh_append_csc2csr": [_P(CulshData), _i64, _vp, _vp, _vp, _i64, _vp, _vp],
     "culsh_segment_sums": [_i64, _vp, _vp, _vp, _vp],
 }
-_RESTYPES = {"culsh_last_error": ctypes.c_char_p, "culsh_version": ctypes.c_char_p}
+_RESTYPES = {"culsh_last_error": ctypes.c_char_p, "culsh_version": ctypes.c_char_p,
+             "culsh_split_holdout": ctypes.c_int64}
 
 _lib = None
 

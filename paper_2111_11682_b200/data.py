@@ -298,3 +298,45 @@ class DeviceRatings:
         self.base_b = nat.to_dev(b, np.float64)
         self.base_bhat = nat.to_dev(b_hat, np.float64)
         self.struct = self._make_struct()
+
+
+def transform_ratings(triplets: Triplets, zero_floor: float | None = None,
+                      scale: float | None = None) -> Triplets:
+    """Replace exact-zero values by ``zero_floor``, then divide by ``scale``
+    (data.py:150-163); the inverse scale is applied at evaluation time."""
+    if scale is not None and scale <= 0:
+        raise ValueError(f"scale must be positive, got {scale}")
+    values = np.array(triplets.values, dtype=np.float64, copy=True)
+    if zero_floor is not None:
+        values[values == 0.0] = zero_floor
+    if scale is not None:
+        values = values / scale
+    return Triplets(triplets.rows, triplets.cols, values, triplets.row_ids, triplets.col_ids)
+
+
+def split_holdout(ratings: SparseRatings, test_fraction: float, seed: int):
+    """Deterministic holdout split (data.py:312-346): returns (train SparseRatings over
+    the same index space, test Triplets).  Entries move to the test side in the order of
+    numpy's PCG64 permutation (the reference's stream, drawn here) while their row and
+    column keep a training entry; the sequential decisions run natively
+    (culsh_split_holdout) instead of as an interpreted loop."""
+    import ctypes
+    if not (0 <= test_fraction < 1):
+        raise ValueError(f"test_fraction must be in [0, 1), got {test_fraction}")
+    nnz = ratings.nnz
+    n_test = int(round(test_fraction * nnz))
+    in_test = np.zeros(nnz, dtype=np.uint8)
+    if n_test > 0:
+        perm = np.ascontiguousarray(np.random.default_rng(seed).permutation(nnz), dtype=np.int64)
+        rows = np.ascontiguousarray(ratings.entry_rows, dtype=np.int32)
+        cols = np.ascontiguousarray(ratings.entry_cols, dtype=np.int32)
+        p = lambda a: ctypes.c_void_p(a.ctypes.data)
+        nat.call("culsh_split_holdout", p(rows), p(cols), nnz, ratings.M, ratings.N, p(perm), n_test,
+                 p(in_test))
+    mask = in_test.astype(bool)
+    keep = ~mask
+    train = SparseRatings(ratings.M, ratings.N, ratings.entry_rows[keep], ratings.entry_cols[keep],
+                          ratings.entry_values[keep], ratings.row_ids, ratings.col_ids)
+    test = Triplets(ratings.entry_rows[mask].copy(), ratings.entry_cols[mask].copy(),
+                    ratings.entry_values[mask].copy(), ratings.row_ids, ratings.col_ids)
+    return train, test

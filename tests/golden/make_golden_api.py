@@ -92,6 +92,19 @@ def main():
     out["inc_in_place"] = np.int64(pt is pe)
     for k in ("b", "b_hat", "U", "V", "W", "C"):
         out["inc_" + k] = getattr(pt, k)
+    # holdout split (data.py:312-346) and value transform (data.py:150-163)
+    from lshmf.data import split_holdout, transform_ratings, Triplets
+    big = random_sparse(400, 300, 0.08, seed=9)
+    for k, v in (("rows", big.entry_rows), ("cols", big.entry_cols), ("vals", big.entry_values)):
+        out["split_in_" + k] = v
+    for frac, sd in ((0.1, 0), (0.3, 4), (0.0, 1)):
+        tr_, te_ = split_holdout(big, frac, sd)
+        out[f"split_{int(frac * 10)}_{sd}_test_rows"] = te_.rows
+        out[f"split_{int(frac * 10)}_{sd}_test_cols"] = te_.cols
+        out[f"split_{int(frac * 10)}_{sd}_train_rows"] = tr_.entry_rows
+    tt = transform_ratings(Triplets(np.array([0, 1, 2]), np.array([0, 1, 1]), np.array([0.0, 50.0, 100.0])),
+                           zero_floor=0.5, scale=20.0)
+    out["transform_vals"] = tt.values
     np.savez_compressed(os.path.join(OUT, "api.npz"), **out)
     print("wrote", len(out), "arrays")
 

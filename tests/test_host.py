@@ -168,3 +168,24 @@ def test_checkpoint_bytes_match_reference(tmp_path):
     assert (tmp_path / "m.bin").read_bytes() == z["mp_bytes"].tobytes()
     q = P.ModelParams.load(tmp_path / "m.bin")
     assert q.V.tobytes() == p.V.tobytes()
+
+
+def test_split_holdout_and_transform_match_reference():
+    """split_holdout (native sequential core, numpy PCG64 permutation) and
+    transform_ratings reproduce the reference's outputs exactly (api.npz)."""
+    import paper_2111_11682_b200 as P
+    z = load_golden("api.npz")
+    r = P.SparseRatings(400, 300, z["split_in_rows"], z["split_in_cols"], z["split_in_vals"])
+    for frac, sd in ((0.1, 0), (0.3, 4), (0.0, 1)):
+        tr, te = P.split_holdout(r, frac, sd)
+        key = f"split_{int(frac * 10)}_{sd}_"
+        assert np.array_equal(te.rows, z[key + "test_rows"]) and np.array_equal(te.cols, z[key + "test_cols"])
+        assert np.array_equal(tr.entry_rows, z[key + "train_rows"])
+        assert tr.nnz + len(te) == r.nnz
+    with pytest.raises(ValueError):
+        P.split_holdout(r, 1.0, 0)
+    tt = P.transform_ratings(P.Triplets(np.array([0, 1, 2]), np.array([0, 1, 1]), np.array([0.0, 50.0, 100.0])),
+                             zero_floor=0.5, scale=20.0)
+    assert tt.values.tobytes() == z["transform_vals"].tobytes()
+    with pytest.raises(ValueError):
+        P.transform_ratings(tt, scale=0.0)
