@@ -76,6 +76,24 @@ inline int num_sms() {
     return n;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default pool; keep
+// freed blocks cached in the pool instead of returning them to the driver at every
+// synchronisation (release threshold 0 by default), which would re-map memory on each
+// call of a frequently called entry point.
+inline void keep_pool_memory() {
+    static bool done = false;
+    if (!done) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done = true;
+    }
+}
+
 inline int status_of(cudaError_t e) { return e == cudaSuccess ? CULSH_OK : CULSH_ECUDA; }
 
 }  // namespace culsh

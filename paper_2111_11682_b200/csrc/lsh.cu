@@ -643,6 +643,7 @@ extern "C" int culsh_row_hash_table(uint64_t seed, int q, int p, int G, int64_t 
     if (row_hi <= row_lo) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     uint64_t *keys = nullptr;
+    keep_pool_memory();
     CULSH_CHECK(cudaMallocAsync(&keys, sizeof(uint64_t) * q * p, st));
     map_keys_kernel<<<(q * p + 255) / 256, 256, 0, st>>>(seed, q, p, keys);
     const int ns = (G + 7) / 8;

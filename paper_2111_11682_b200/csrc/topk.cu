@@ -151,7 +151,10 @@ struct DevBuf {
     void *p = nullptr;
     cudaStream_t st;
     explicit DevBuf(cudaStream_t s) : st(s) {}
-    cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, n ? n : 16, st); }
+    cudaError_t alloc(size_t n) {
+        keep_pool_memory();
+        return cudaMallocAsync(&p, n ? n : 16, st);
+    }
     ~DevBuf() { if (p) cudaFreeAsync(p, st); }
     template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
 };

@@ -82,6 +82,10 @@ class OnlineSession:
 
     def __init__(self, dev: DeviceRatings, state: HashState, entries, K: int, params: ModelParams,
                  config: TrainConfig, reserve: float = 1.25):
+        t = nat.torch()
+        if dev.nnz and not bool(t.all(dev.col_vals == t.round(dev.col_vals)).item()):
+            raise ValueError("OnlineSession keeps every sum exact and needs integer-valued ratings; "
+                             "use absorb_increment for other values")
         self.dev = dev
         self.state = state
         self.lsh: LshConfig = state.config
@@ -128,6 +132,8 @@ class OnlineSession:
         if batch.base_M != self.M or batch.base_N != self.N:
             raise ValueError("increment base shape does not match the session")
         batch.validate()
+        if len(batch.values) and not np.all(np.asarray(batch.values) == np.round(batch.values)):
+            raise ValueError("OnlineSession needs integer-valued ratings; use absorb_increment")
         c = self.lsh
         tm = {}
 
@@ -195,27 +201,22 @@ class OnlineSession:
         scale = cfg.effective_init_scale
         U_new = rng.uniform(0.0, scale, size=(batch.new_row_count, F))
         V_new = rng.uniform(0.0, scale, size=(batch.new_col_count, F))
-        b_new = np.zeros(batch.new_row_count)
-        bh_new = np.zeros(batch.new_col_count)
-        if len(batch.rows):
-            # bincount sums in entry order, as np.add.at does (online.py:205-215), over
-            # the entries of new rows / new columns only
-            sel_r = batch.rows >= M_old
-            r_new = batch.rows[sel_r] - M_old
-            rs = np.bincount(r_new, weights=batch.values[sel_r], minlength=batch.new_row_count)
-            rc = np.bincount(r_new, minlength=batch.new_row_count).astype(np.float64)
-            sel = rc > 0
-            b_new[sel] = rs[sel] / rc[sel] - self.mu
-            sel_c = batch.cols >= N_old
-            c_new = batch.cols[sel_c] - N_old
-            cs = np.bincount(c_new, weights=batch.values[sel_c], minlength=batch.new_col_count)
-            cc = np.bincount(c_new, minlength=batch.new_col_count).astype(np.float64)
-            sel = cc > 0
-            bh_new[sel] = cs[sel] / cc[sel] - self.mu
+        # new biases: batch means of the new variables minus mu (online.py:205-215); the
+        # batch's own row / column segments (rptr_d, cptr_d) give exact integer sums
+        def batch_means(ptr, vals, first, count):
+            if count == 0:
+                return t.zeros(0, dtype=t.float64, device=nat.device())
+            sums = nat.empty((count,), "float64")
+            nat.call("culsh_segment_sums", count, nat.ptr(ptr[first:]), nat.ptr(vals), nat.ptr(sums),
+                     nat.stream_ptr())
+            cnt = (ptr[first + 1:first + count + 1] - ptr[first:first + count]).to(t.float64)
+            return t.where(cnt > 0, sums / cnt.clamp(min=1) - self.mu, t.zeros_like(sums))
+        b_new = batch_means(rptr_d, rval_d, M_old, batch.new_row_count)
+        bh_new = batch_means(cptr_d, cval_d, N_old, batch.new_col_count)
         m = self.model
         K = self.K
-        m.b = self._grow_model("b", M_old, nat.to_dev(b_new))
-        m.bhat = self._grow_model("bhat", N_old, nat.to_dev(bh_new))
+        m.b = self._grow_model("b", M_old, b_new)
+        m.bhat = self._grow_model("bhat", N_old, bh_new)
         m.U = self._grow_model("U", M_old * F, nat.to_dev(U_new.reshape(-1)))
         m.V = self._grow_model("V", N_old * F, nat.to_dev(V_new.reshape(-1)))
         if K:
@@ -229,17 +230,25 @@ class OnlineSession:
         dv = self.dev
         sc = _Scratch(M_hat, N_hat)
         _plan_full(dv, sc, N_old, N_hat, 0, M_hat)
+        t_plan = time.perf_counter()
+        t.cuda.synchronize()
+        t_row = 0.0
         for ep in range(cfg.epochs):
             rates = _rates_struct(cfg.rates_at(ep), cfg.regs)
+            t1 = time.perf_counter()
             nat.call("culsh_sgd_exact_rowpass", ctypes.byref(dv.struct), ctypes.byref(m.struct),
                      ctypes.byref(rates), M_old, M_hat, N_old, nat.ptr(sc.status), nat.stream_ptr())
+            t.cuda.synchronize()
+            t_row += time.perf_counter() - t1
             if not sc.status_value():
                 _colpass(dv, m, sc, rates, N_old, N_hat, 2, M_old)
             if sc.status_value():
                 raise TrainingDivergedError(epoch=ep)
+        tm["inc_plan"] = t_plan - t0
+        tm["inc_rowpass"] = t_row
         t0 = mark("train_incremental", t0)
         self.M, self.N = M_hat, N_hat
-        tm["total"] = sum(tm.values())
+        tm["total"] = sum(v for k, v in tm.items() if not k.startswith("inc_"))
         tm["batch_ratings"] = int(len(batch.rows))
         return tm
 
