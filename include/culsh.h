@@ -180,6 +180,22 @@ int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRate
                             int64_t col_hi, int row_mode, int64_t M_old, int variant,
                             int *row_last, int *ticket, int *status, void *stream);
 
+/* Neighbour lookups (factorization.py:218-232) of every CSC entry of columns
+ * [col_lo, col_hi), ahead of a column pass: mask (entries x (K<=32 ? 1 : 2) u32, bit k
+ * set iff row i rated J[j,k]) and rv (entries x K f64, the ratings found), entry
+ * index relative to col_ptr[col_lo]. */
+int culsh_exact_lookup(const CulshData *d, const CulshModel64 *m, int64_t col_lo, int64_t col_hi,
+                       uint32_t *mask, double *rv, void *stream);
+
+/* culsh_sgd_exact_colpass reading the lookups from culsh_exact_lookup (pre_base =
+ * col_ptr[col_lo] of that call) instead of searching inside the dependent update
+ * chain -- the same values, bit-identical result. */
+int culsh_sgd_exact_colpass_pre(const CulshData *d, CulshModel64 *m, const CulshRates *r,
+                                const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
+                                int64_t col_hi, int row_mode, int64_t M_old, int variant,
+                                int *row_last, int *ticket, int *status, const uint32_t *pre_mask,
+                                const double *pre_rv, int64_t pre_base, void *stream);
+
 /* online.py:230-250 _online_row_pass (rows [row_lo,row_hi), columns < N_old). */
 int culsh_sgd_exact_rowpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
                             int64_t row_lo, int64_t row_hi, int64_t N_old, int *status,

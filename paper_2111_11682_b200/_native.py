@@ -84,6 +84,9 @@ _SIGS = {
     "culsh_block_pointers": [_vp, _vp, _i64, _vp, _i32, _vp, _vp],
     "culsh_sgd_exact_colpass": [_P(CulshData), _P(CulshModel64), _P(CulshRates), _vp, _vp, _i64,
                                 _i64, _i32, _i64, _i32, _vp, _vp, _vp, _vp],
+    "culsh_exact_lookup": [_P(CulshData), _P(CulshModel64), _i64, _i64, _vp, _vp, _vp],
+    "culsh_sgd_exact_colpass_pre": [_P(CulshData), _P(CulshModel64), _P(CulshRates), _vp, _vp, _i64,
+                                    _i64, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "culsh_sgd_exact_rowpass": [_P(CulshData), _P(CulshModel64), _P(CulshRates), _i64, _i64, _i64,
                                 _vp, _vp],
     "culsh_explicit_stream": [_P(CulshData), _f64, _vp, _i32, _vp, _vp, _vp, _vp, _vp],

@@ -85,12 +85,22 @@ __device__ __forceinline__ Scalars exact_error(const double *buf, int F, int K, 
     return s;
 }
 
+// Precomputed neighbour lookups of a column range (culsh_exact_lookup): per CSC entry
+// idx, KPL mask words at mask[(idx - base) * KPL] (bit k: row i rated J[j,k]) and the
+// looked-up ratings rv[(idx - base) * K + k].  With them the column kernel's per-update
+// critical path loses its K dependent binary searches; the values are the same reads.
+struct ExactPre {
+    const uint32_t *mask;
+    const double *rv;
+    int64_t base;
+};
+
 template <int FPL, int KPL>
 __global__ void __launch_bounds__(256)
 exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                  const int32_t *__restrict__ chain_lo, int64_t col_lo, int64_t col_hi, int row_mode,
                  int64_t M_old, int variant, int *__restrict__ row_last, int *__restrict__ ticket,
-                 int *__restrict__ status) {
+                 int *__restrict__ status, ExactPre pre) {
     extern __shared__ double s_buf[];
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
@@ -140,7 +150,13 @@ exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
             for (int q = 0; q < KPL; ++q) {
                 const int k = lane + 32 * q;
                 double rv = 0.0;
-                expl[q] = k < K && lookup(P.row_ptr, P.row_cols, P.row_vals, i, nb[q], &rv);
+                if (pre.mask) {
+                    const int64_t li = idx - pre.base;
+                    expl[q] = k < K && ((__ldg(pre.mask + li * KPL + q) >> lane) & 1u);
+                    if (expl[q]) rv = __ldg(pre.rv + li * K + k);
+                } else {
+                    expl[q] = k < K && lookup(P.row_ptr, P.row_cols, P.row_vals, i, nb[q], &rv);
+                }
                 resid[q] = expl[q] ? rv - (mu + bbi + bbn[q]) : 0.0;
                 emask[q] = __ballot_sync(0xffffffffu, expl[q]);
             }
@@ -362,10 +378,37 @@ __global__ void block_pointers_kernel(const int64_t *__restrict__ col_ptr, const
     }
 }
 
+// Neighbour lookups of every entry of columns [col_lo, col_hi): warp per entry (grid
+// stride), lane k searches J[j,k] in row i (the _lookup of factorization.py:218-232).
+__global__ void exact_lookup_kernel(ExactModel P, int64_t col_lo, int64_t col_hi, int KPL,
+                                    uint32_t *__restrict__ mask, double *__restrict__ rv) {
+    const unsigned lane = lane_id();
+    const int K = P.K;
+    const int64_t e_lo = P.col_ptr[col_lo], e_hi = P.col_ptr[col_hi];
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t e = e_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < e_hi; e += warps) {
+        int64_t lo = col_lo, hi = col_hi;   // column of entry e: last j with col_ptr[j] <= e
+        while (hi - lo > 1) {
+            const int64_t m = (lo + hi) >> 1;
+            if (P.col_ptr[m] <= e) lo = m; else hi = m;
+        }
+        const int64_t j = lo;
+        const int32_t i = P.col_rows[e];
+        for (int q = 0; q < KPL; ++q) {
+            const int k = (int)lane + 32 * q;
+            double v = 0.0;
+            const bool hit = k < K && lookup(P.row_ptr, P.row_cols, P.row_vals, i, P.nbr[j * K + k], &v);
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (lane == 0) mask[(e - e_lo) * KPL + q] = bal;
+            if (k < K) rv[(e - e_lo) * K + k] = v;
+        }
+    }
+}
+
 template <int FPL, int KPL>
 int launch_col(const ExactModel &P, const CulshRates &R, const int64_t *seg, const int32_t *chain_lo,
                int64_t col_lo, int64_t col_hi, int row_mode, int64_t M_old, int variant, int *row_last,
-               int *ticket, int *status, cudaStream_t st) {
+               int *ticket, int *status, cudaStream_t st, ExactPre pre) {
     const int threads = 128;
     const size_t smem = (size_t)(threads / 32) * (P.F + P.K) * sizeof(double);
     int occ = 0;
@@ -377,7 +420,7 @@ int launch_col(const ExactModel &P, const CulshRates &R, const int64_t *seg, con
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
     exact_col_kernel<FPL, KPL><<<(unsigned)blocks, threads, smem, st>>>(
-        P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status);
+        P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status, pre);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
 }
 
@@ -460,10 +503,10 @@ extern "C" int culsh_pass_plan(const int64_t *col_ptr, const int32_t *col_rows, 
     return CULSH_OK;
 }
 
-extern "C" int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
-                                       const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
-                                       int64_t col_hi, int row_mode, int64_t M_old, int variant,
-                                       int *row_last, int *ticket, int *status, void *stream) {
+static int exact_colpass_impl(const CulshData *d, CulshModel64 *m, const CulshRates *r, const int64_t *seg,
+                              const int32_t *chain_lo, int64_t col_lo, int64_t col_hi, int row_mode,
+                              int64_t M_old, int variant, int *row_last, int *ticket, int *status, void *stream,
+                              ExactPre pre) {
     CULSH_REQUIRE(m->F >= 1 && m->F <= 256, "F must be in [1, 256]");
     CULSH_REQUIRE(m->K >= 0 && m->K <= 64, "K must be in [0, 64]");
     if (col_hi <= col_lo) return CULSH_OK;
@@ -472,9 +515,39 @@ extern "C" int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, cons
     CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     const ExactModel P = make_model(d, m);
     const CulshRates R = *r;
-#define CALL_COL(a, b) launch_col<a, b>(P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status, st)
+#define CALL_COL(a, b) launch_col<a, b>(P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status, st, pre)
     CULSH_DISPATCH_FK(m->F, m->K, CALL_COL);
 #undef CALL_COL
+}
+
+extern "C" int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
+                                       const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
+                                       int64_t col_hi, int row_mode, int64_t M_old, int variant,
+                                       int *row_last, int *ticket, int *status, void *stream) {
+    return exact_colpass_impl(d, m, r, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket,
+                              status, stream, ExactPre{nullptr, nullptr, 0});
+}
+
+extern "C" int culsh_exact_lookup(const CulshData *d, const CulshModel64 *m, int64_t col_lo, int64_t col_hi,
+                                  uint32_t *mask, double *rv, void *stream) {
+    CULSH_REQUIRE(m->K >= 1 && m->K <= 64, "K must be in [1, 64]");
+    if (col_hi <= col_lo) return CULSH_OK;
+    const ExactModel P = make_model(d, m);
+    const int KPL = m->K <= 32 ? 1 : 2;
+    exact_lookup_kernel<<<(unsigned)(num_sms() * 16), 256, 0, (cudaStream_t)stream>>>(P, col_lo, col_hi, KPL,
+                                                                                     mask, rv);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_sgd_exact_colpass_pre(const CulshData *d, CulshModel64 *m, const CulshRates *r,
+                                           const int64_t *seg, const int32_t *chain_lo, int64_t col_lo,
+                                           int64_t col_hi, int row_mode, int64_t M_old, int variant,
+                                           int *row_last, int *ticket, int *status, const uint32_t *pre_mask,
+                                           const double *pre_rv, int64_t pre_base, void *stream) {
+    CULSH_REQUIRE(pre_mask != nullptr && pre_rv != nullptr, "precomputed lookups missing");
+    return exact_colpass_impl(d, m, r, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket,
+                              status, stream, ExactPre{pre_mask, pre_rv, pre_base});
 }
 
 extern "C" int culsh_sgd_exact_rowpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,

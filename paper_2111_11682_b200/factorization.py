@@ -257,11 +257,37 @@ def _plan_full(dev, sc: _Scratch, col_lo, col_hi, row_lo, row_hi) -> None:
 
 
 def _colpass(dev, dm: DeviceModel64, sc: _Scratch, rates: nat.CulshRates, col_lo, col_hi,
-             row_mode: int, M_old: int = 0, variant: int = 0) -> None:
+             row_mode: int, M_old: int = 0, variant: int = 0, pre=None) -> None:
+    """One exact column pass; ``pre`` = _exact_lookups(...) of the same columns."""
+    if pre is not None:
+        mask, rv, base = pre
+        nat.call("culsh_sgd_exact_colpass_pre", ctypes.byref(dev.struct), ctypes.byref(dm.struct),
+                 ctypes.byref(rates), nat.ptr(sc.seg), nat.ptr(sc.chain), col_lo, col_hi, row_mode,
+                 M_old, variant, nat.ptr(sc.row_last), nat.ptr(sc.ticket), nat.ptr(sc.status),
+                 nat.ptr(mask), nat.ptr(rv), base, nat.stream_ptr())
+        return
     nat.call("culsh_sgd_exact_colpass", ctypes.byref(dev.struct), ctypes.byref(dm.struct),
              ctypes.byref(rates), nat.ptr(sc.seg), nat.ptr(sc.chain), col_lo, col_hi, row_mode,
              M_old, variant, nat.ptr(sc.row_last), nat.ptr(sc.ticket), nat.ptr(sc.status),
              nat.stream_ptr())
+
+
+def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int):
+    """Neighbour lookups of columns [col_lo, col_hi) for _colpass's ``pre`` (worth it for
+    a few long columns, e.g. an online batch's new columns: the searches leave the
+    dependent update chain).  None when K == 0 or the range is empty."""
+    K = dm.struct.K
+    if K == 0 or col_hi <= col_lo:
+        return None
+    cp = dev.col_ptr
+    base = int(cp[col_lo].item())
+    n = int(cp[col_hi].item()) - base
+    kpl = 1 if K <= 32 else 2
+    mask = nat.empty((max(n * kpl, 1),), "int32")
+    rv = nat.empty((max(n * K, 1),), "float64")
+    nat.call("culsh_exact_lookup", ctypes.byref(dev.struct), ctypes.byref(dm.struct), col_lo, col_hi,
+             nat.ptr(mask), nat.ptr(rv), nat.stream_ptr())
+    return mask, rv, base
 
 
 def _check_model_dims(F: int, K: int) -> None:

@@ -28,7 +28,7 @@ import numpy as np
 from . import _native as nat
 from .data import DeviceRatings
 from .factorization import (DeviceModel64, ModelParams, TrainConfig, TrainingDivergedError,
-                            _Scratch, _colpass, _plan_full, _rates_struct)
+                            _Scratch, _colpass, _exact_lookups, _plan_full, _rates_struct)
 from .lsh import HashState, LshConfig, RowHashes, _ns, _table_alloc, _topk_device
 from .online import IncrementBatch, device_segments
 
@@ -230,6 +230,7 @@ class OnlineSession:
         dv = self.dev
         sc = _Scratch(M_hat, N_hat)
         _plan_full(dv, sc, N_old, N_hat, 0, M_hat)
+        pre = _exact_lookups(dv, m, N_old, N_hat)   # the new columns' neighbour lookups, once
         t_plan = time.perf_counter()
         t.cuda.synchronize()
         t_row = 0.0
@@ -241,10 +242,10 @@ class OnlineSession:
             t.cuda.synchronize()
             t_row += time.perf_counter() - t1
             if not sc.status_value():
-                _colpass(dv, m, sc, rates, N_old, N_hat, 2, M_old)
+                _colpass(dv, m, sc, rates, N_old, N_hat, 2, M_old, pre=pre)
             if sc.status_value():
                 raise TrainingDivergedError(epoch=ep)
-        tm["inc_plan"] = t_plan - t0
+        tm["inc_plan_lookups"] = t_plan - t0
         tm["inc_rowpass"] = t_row
         t0 = mark("train_incremental", t0)
         self.M, self.N = M_hat, N_hat
