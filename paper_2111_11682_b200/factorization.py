@@ -272,16 +272,20 @@ def _colpass(dev, dm: DeviceModel64, sc: _Scratch, rates: nat.CulshRates, col_lo
              nat.stream_ptr())
 
 
-def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int):
-    """Neighbour lookups of columns [col_lo, col_hi) for _colpass's ``pre`` (worth it for
-    a few long columns, e.g. an online batch's new columns: the searches leave the
-    dependent update chain).  None when K == 0 or the range is empty."""
+def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fraction: float = 1.0):
+    """Neighbour lookups of columns [col_lo, col_hi) for _colpass's ``pre``: the K
+    dependent binary searches of every update leave the update chain (which is what
+    bounds a pass on long columns / hot rows).  None when K == 0, the range is empty, or
+    the arrays (entries x K x 8 B) would exceed ``mem_fraction`` of the free memory."""
     K = dm.struct.K
     if K == 0 or col_hi <= col_lo:
         return None
     cp = dev.col_ptr
     base = int(cp[col_lo].item())
     n = int(cp[col_hi].item()) - base
+    t = nat.torch()
+    if n * K * 8.5 > mem_fraction * t.cuda.mem_get_info()[0]:
+        return None
     kpl = 1 if K <= 32 else 2
     mask = nat.empty((max(n * kpl, 1),), "int32")
     rv = nat.empty((max(n * K, 1),), "float64")
@@ -500,8 +504,9 @@ def train_full(ratings: SparseRatings, neighbors: NeighborTable | None,
     dm = DeviceModel64(params)
     sc = _Scratch(ratings.M, ratings.N)
     _plan_full(dev, sc, 0, ratings.N, 0, ratings.M)
+    pre = _exact_lookups(dev, dm, 0, ratings.N, 0.25)   # once per fit, reused every epoch
     for t in range(config.epochs):
-        _colpass(dev, dm, sc, _rates_struct(config.rates_at(t), config.regs), 0, ratings.N, 1)
+        _colpass(dev, dm, sc, _rates_struct(config.rates_at(t), config.regs), 0, ratings.N, 1, pre=pre)
         if sc.status_value():
             dm.download(params)
             raise TrainingDivergedError(epoch=t)

@@ -40,16 +40,29 @@ def per_epoch(make, extra=2):
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     M, N, nnz, F, K, e = synth.SHAPES[name]
-    dm = synth.random_sparse_device(M, N, nnz, seed=0)
-    d = dm.dev
-    col = torch.repeat_interleave(torch.arange(N, device="cuda"), d.col_ptr[1:] - d.col_ptr[:-1]).to(torch.int32)
-    r = DeviceSparseRatings(M, N, d.col_rows, col, d.col_vals)
-    del col
+    if "--structured" in sys.argv:   # skewed, low-rank-plus-noise stars (SURVEY §8(d) perf-stress)
+        rows, cols, vals = synth.structured_triplets_device(M, N, nnz, seed=0)
+        r = DeviceSparseRatings(M, N, rows, cols, vals)
+        del rows, cols, vals
+    else:
+        dm = synth.random_sparse_device(M, N, nnz, seed=0)
+        d = dm.dev
+        col = torch.repeat_interleave(torch.arange(N, device="cuda"), d.col_ptr[1:] - d.col_ptr[:-1]).to(torch.int32)
+        r = DeviceSparseRatings(M, N, d.col_rows, col, d.col_vals)
+        del col, dm
     d = r.device()
     ent, _, _ = lsh.simlsh_topk_device(d, P.LshConfig(psi_exponent=e), K)
     nbr = P.NeighborTable(N, K, nat.to_host(ent)[:N * K].reshape(N, K))
     cfg = lambda ep: P.TrainConfig(F=F, K=K, epochs=ep, seed=0, **RATES)
-    out = {"config": name, "M": M, "N": N, "nnz": int(d.nnz), "F": F, "K": K}
+    out = {"config": name, "data": "structured" if "--structured" in sys.argv else "uniform", "M": M, "N": N,
+           "nnz": int(d.nnz), "F": F, "K": K}
+    if "--exact-only" in sys.argv:
+        s = per_epoch(lambda ep: P.train_full(r, nbr, cfg(ep)))
+        out["train_full_exact_s_per_epoch"] = s
+        s = per_epoch(lambda ep: P.parallel_train(r, nbr, cfg(ep), 4))
+        out["parallel_train_D4_exact_s_per_epoch"] = s
+        print(json.dumps(out), flush=True)
+        return
     s = per_epoch(lambda ep: P.train_full(r, nbr, cfg(ep)))
     out["train_full_exact_s_per_epoch"] = s
     out["train_full_exact_updates_per_s"] = d.nnz / s
