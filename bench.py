@@ -294,7 +294,7 @@ def run_gpu(args):
     t_prep = time.perf_counter()
     tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params, rotate=bool(args.rotate),
                         atomic_rows=bool(args.atomic),
-                        packed=bool(args.packed))
+                        packed=bool(args.packed), p16=bool(args.p16))
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t_prep
     del params
@@ -380,7 +380,7 @@ def e2e_streaming(tr, args):
     dt = time.perf_counter() - t0
     return {"value": tr.nnz * steps / dt, "unit": "updates/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps,
-            "stream": sorted(host),
+            "stream": sorted(host),   # 2-byte records when they fit (see HogwildTrainer._stream_buffers)
             "api": "HogwildTrainer.train_from_host (pinned host rating stream -- every per-rating array the "
                    "epoch reads -- copied H2D per epoch, double-buffered copy/compute overlap, loss D2H per epoch)"}
 
@@ -394,6 +394,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--p16", type=int, default=1, help="2-byte packed records (row deltas) when they fit")
     ap.add_argument("--rotate", type=int, default=0, help="per-column rotated visiting order")
     ap.add_argument("--atomic", type=int, default=1, help="row updates as atomic adds")
     ap.add_argument("--packed", type=int, default=1,

@@ -265,6 +265,23 @@ int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const
                                    CulshModel32 *m, const CulshRates *r, int flags, int max_warps,
                                    int *ticket, double *loss_out, int *status, void *stream);
 
+/* 2-byte per-rating stream (rows without rotation): words[idx] = row delta from the
+ * previous entry of the column (12 bits; 0 for the first) | value code (3 bits) |
+ * has-explicit-neighbour (1 bit); first_row[j] = row of column j's first entry.
+ * *status |= 4 if a delta or the value table does not fit (use culsh_pack_stream). */
+int culsh_pack16(int64_t N, const int64_t *col_ptr, const int32_t *rows, const float *vals,
+                 const uint32_t *mask, int MW, const float *lut, int n_lut, uint16_t *words,
+                 int32_t *first_row, int *status, void *stream);
+
+/* culsh_sgd_hogwild_epoch_packed over the 2-byte stream (rows rebuilt by a warp prefix
+ * sum; cmask / mptr as for the 4-byte stream; no rotation).  Identical updates. */
+int culsh_sgd_hogwild_epoch_packed16(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
+                                     const uint16_t *packed, const int32_t *first_row, const float *lut,
+                                     const int64_t *mptr, const uint32_t *cmask, const int64_t *resid_ptr,
+                                     const float *resid, const int32_t *col_order, CulshModel32 *m,
+                                     const CulshRates *r, int flags, int max_warps, int *ticket,
+                                     double *loss_out, int *status, void *stream);
+
 /* --------------------------------------------------------------- eval --- */
 
 /* Per-test-triplet squared error (fp64, exact _predict_one order) and the RMSE.

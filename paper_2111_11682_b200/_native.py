@@ -100,6 +100,9 @@ _SIGS = {
     "culsh_gsm_count_select": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_pair_similarity": [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp],
     "culsh_split_holdout": [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp],
+    "culsh_pack16": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
+    "culsh_sgd_hogwild_epoch_packed16": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                         _P(CulshModel32), _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
     "culsh_rmse": [_P(CulshData), _P(CulshModel64), _vp, _vp, _vp, _i64, _i32, _f64, _f64, _f64,
                    _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
@@ -220,7 +223,7 @@ def to_host(x, dtype=None) -> np.ndarray:
 def empty(shape, dtype: str):
     t = torch()
     tmap = {"int32": t.int32, "int64": t.int64, "float64": t.float64, "float32": t.float32,
-            "uint8": t.uint8, "uint64": t.int64, "uint32": t.int32}
+            "uint8": t.uint8, "uint64": t.int64, "uint32": t.int32, "int16": t.int16}
     return t.empty(shape, dtype=tmap[dtype], device=device())
 
 

@@ -155,7 +155,12 @@ constexpr int hw_smem_per_warp() {
 // bit 31} and mask words only for ratings with a set bit (column base mptr[j]),
 // 4 + MW*4*(fraction with explicit neighbours) bytes per rating instead of
 // 8 + 4*MW.  Whole columns only (no seg); rotation keeps two mask cursors.
-template <int FV, int KPL, bool ATOMIC, bool PACK>
+//
+// P16 (with PACK, no rotation): 2-byte records {row delta from the previous entry of the
+// column: 12 bits, value code: 3 bits, has-mask: 1 bit}, rows rebuilt by a warp prefix sum
+// from first_row[j]; the per-epoch stream is then 2 + MW*4*(fraction flagged) bytes per
+// rating + 4 per column.
+template <int FV, int KPL, bool ATOMIC, bool PACK, bool P16>
 __global__ void __launch_bounds__(kHwWarps * 32, 4)
 hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__restrict__ seg,
                const int32_t *__restrict__ rows, const float *__restrict__ vals,
@@ -164,7 +169,8 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                float *__restrict__ Bv, float *__restrict__ BHv, float *__restrict__ U,
                float *__restrict__ V, float *__restrict__ W, float *__restrict__ C, int F, int K,
                HwCoef R, int flags, int *__restrict__ ticket, double *__restrict__ loss,
-               int *__restrict__ status, const float *__restrict__ lut, const int64_t *__restrict__ mptr) {
+               int *__restrict__ status, const float *__restrict__ lut, const int64_t *__restrict__ mptr,
+               const int32_t *__restrict__ first_row) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     constexpr int P = kHwDepth;
     const unsigned lane = lane_id();
@@ -233,6 +239,9 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             my_start[FV + 2 * KPL] = bh;
         }
         const float *rcol = resid + resid_ptr[j];
+        const uint16_t *p16 = reinterpret_cast<const uint16_t *>(rows);
+        int carry = 0;   // P16: row of the entry before the next chunk
+        if constexpr (P16) carry = first_row[j];
         // packed: next compact mask slot of the rotated range's segment 1 ([rot, n)) / 2 ([0, rot))
         int64_t mrun1 = PACK ? mptr[j] : 0, mrun2 = mrun1;
         // Visiting order: the column's entries rotated to start at position `rot`
@@ -242,10 +251,18 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         const int rot = ((flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
         int rrel2 = 0;   // residual offset (relative to the column base) at position lo
         if (PACK && lo > c_lo) {   // work segment: mask cursor and residual offset at lo
-            int h = 0;
-            for (int64_t x = c_lo + lane; x < lo; x += 32)
-                h += (int)(__ldg(reinterpret_cast<const uint32_t *>(rows) + x) >> 31);
+            int h = 0, dsum = 0;
+            for (int64_t x = c_lo + lane; x < lo; x += 32) {
+                if constexpr (P16) {
+                    const uint32_t w16 = __ldg(p16 + x);
+                    h += (int)(w16 >> 15);
+                    dsum += (int)(w16 & 0xFFFu);
+                } else {
+                    h += (int)(__ldg(reinterpret_cast<const uint32_t *>(rows) + x) >> 31);
+                }
+            }
             h = warp_sum(h);
+            if constexpr (P16) carry += warp_sum(dsum);
             int skip = 0;
             for (int64_t x = mrun2 + lane; x < mrun2 + h; x += 32)
 #pragma unroll
@@ -293,10 +310,27 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             float rv;
             uint32_t m0 = 0u, m1 = 0u;
             if constexpr (PACK) {
-                const uint32_t wd = have ? __ldg(reinterpret_cast<const uint32_t *>(rows) + e) : 0u;
-                ri = (int)(wd & 0x07FFFFFFu);
-                rv = __ldg(lut + ((wd >> 27) & 15u));
-                const bool hm = (wd >> 31) != 0u;
+                uint32_t code;
+                bool hm;
+                if constexpr (P16) {
+                    const uint32_t w16 = have ? (uint32_t)__ldg(p16 + e) : 0u;
+                    int incl = (int)(w16 & 0xFFFu);
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if ((int)lane >= o) incl += y;
+                    }
+                    ri = carry + incl;   // lanes past the end repeat the last row (a valid row)
+                    carry = __shfl_sync(0xffffffffu, ri, 31);
+                    code = (w16 >> 12) & 7u;
+                    hm = (w16 >> 15) != 0u;
+                } else {
+                    const uint32_t wd = have ? __ldg(reinterpret_cast<const uint32_t *>(rows) + e) : 0u;
+                    ri = (int)(wd & 0x07FFFFFFu);
+                    code = (wd >> 27) & 15u;
+                    hm = (wd >> 31) != 0u;
+                }
+                rv = __ldg(lut + code);
                 const unsigned b1 = __ballot_sync(0xffffffffu, hm && !seg2);
                 const unsigned b2 = __ballot_sync(0xffffffffu, hm && seg2);
                 if (hm) {
@@ -539,23 +573,23 @@ __device__ __forceinline__ int64_t find_row(const int32_t *__restrict__ rows, in
     return -1;
 }
 
-template <int FV, int KPL, bool PACK = false>
+template <int FV, int KPL, bool PACK = false, bool P16 = false>
 int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const int32_t *rows, const float *vals,
                    const uint32_t *mask, const int64_t *resid_ptr, const float *resid,
                    const int32_t *col_order, CulshModel32 *m, const HwCoef &R, int flags, int max_warps,
                    int *ticket,
                    double *loss, int *status, cudaStream_t st, const float *lut = nullptr,
-                   const int64_t *mptr = nullptr) {
+                   const int64_t *mptr = nullptr, const int32_t *first_row = nullptr) {
     const int threads = kHwWarps * 32;
     const size_t smem = (size_t)kHwWarps * hw_smem_per_warp<FV, KPL>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, true, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, false, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, true, PACK, P16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hogwild_kernel<FV, KPL, false, PACK, P16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
     int occ = 0;
-    auto kern = (flags & 2) ? hogwild_kernel<FV, KPL, true, PACK> : hogwild_kernel<FV, KPL, false, PACK>;
+    auto kern = (flags & 2) ? hogwild_kernel<FV, KPL, true, PACK, P16> : hogwild_kernel<FV, KPL, false, PACK, P16>;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     if (occ < 1) occ = 1;
     int64_t blocks = (int64_t)num_sms() * occ;
@@ -566,7 +600,7 @@ int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const 
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, threads, smem, st>>>(
         N, col_ptr, seg, rows, vals, mask, resid_ptr, resid, col_order, m->mu, m->b, m->bhat, m->U, m->V, m->W,
-        m->C, m->F, m->K, R, flags, ticket, loss, status, lut, mptr);
+        m->C, m->F, m->K, R, flags, ticket, loss, status, lut, mptr, first_row);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
 }
 
@@ -616,6 +650,37 @@ __global__ void pack_stream_kernel(int64_t N, const int64_t *__restrict__ col_pt
             run += __popc(bal);
         }
         if (!packed && lane == 0) mcount[j] = run;
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 4);
+    }
+}
+
+// 2-byte packed records (see hogwild_kernel P16): warp per column, delta from the
+// previous entry's row (0 for the first, whose row goes to first_row[j]); *status |= 4
+// when a delta needs more than 12 bits or a value more than 3 code bits.  The mask
+// words of the flagged entries are those of culsh_pack_stream (cmask, mptr).
+__global__ void pack16_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows,
+                              const float *__restrict__ vals, const uint32_t *__restrict__ mask, int MW,
+                              const float *__restrict__ lut, int n_lut, uint16_t *__restrict__ words,
+                              int32_t *__restrict__ first_row, int *__restrict__ status) {
+    const unsigned lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < N; j += warps) {
+        const int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
+        if (lane == 0) first_row[j] = hi > lo ? rows[lo] : 0;
+        int bad = 0;
+        for (int64_t e = lo + lane; e < hi; e += 32) {
+            const int32_t r = rows[e];
+            const int32_t prev = e > lo ? rows[e - 1] : r;
+            const int delta = r - prev;
+            const float v = vals[e];
+            int code = -1;
+            for (int c = 0; c < n_lut; ++c)
+                if (lut[c] == v) { code = c; break; }
+            uint32_t m = mask[e * MW];
+            if (MW == 2) m |= mask[e * MW + 1];
+            if (code < 0 || code > 7 || delta < 0 || delta > 0xFFF) bad = 1;
+            words[e] = (uint16_t)((delta & 0xFFF) | ((code & 7) << 12) | (m ? 0x8000u : 0u));
+        }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 4);
     }
 }
@@ -811,3 +876,48 @@ extern "C" int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col
     return HWP(8);
 #undef HWP
 }
+
+extern "C" int culsh_sgd_hogwild_epoch_packed16(int64_t N_list, const int64_t *col_ptr, const int64_t *seg,
+                                                const uint16_t *packed, const int32_t *first_row,
+                                              const float *lut, const int64_t *mptr, const uint32_t *cmask,
+                                              const int64_t *resid_ptr, const float *resid,
+                                              const int32_t *col_order, CulshModel32 *m, const CulshRates *r,
+                                              int flags, int max_warps, int *ticket, double *loss_out,
+                                              int *status, void *stream) {
+    const int F = m->F, K = m->K;
+    CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
+    CULSH_REQUIRE((F >= 1 && F <= 32) || F == 64 || F == 128 || F == 256,
+                  "Hogwild mode needs F <= 32 or F in {64, 128, 256}");
+    CULSH_REQUIRE((flags & 4) == 0, "flags bit 2 (sub-warp kernel) is no longer supported");
+    CULSH_REQUIRE(seg == nullptr || (flags & 8), "the packed stream takes whole columns or work segments");
+    CULSH_REQUIRE((flags & 1) == 0, "the 2-byte stream does not run the rotated order");
+    if (N_list <= 0) return CULSH_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    CULSH_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    HwCoef R{(float)r->gb, (float)r->gbh, (float)r->gu, (float)r->gv, (float)r->gw, (float)r->gc,
+             (float)(1.0 - r->gb * r->lb), (float)(1.0 - r->gbh * r->lbh), (float)(1.0 - r->gu * r->lu),
+             (float)(1.0 - r->gv * r->lv), (float)(1.0 - r->gw * r->lw), (float)(1.0 - r->gc * r->lc)};
+    const bool k2 = K > 32;
+    const int32_t *rows = reinterpret_cast<const int32_t *>(packed);
+#define HWP(FVv) (k2 ? launch_hogwild<FVv, 2, true, true>(N_list, col_ptr, seg, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr, first_row) \
+                     : launch_hogwild<FVv, 1, true, true>(N_list, col_ptr, seg, rows, nullptr, cmask, resid_ptr, resid, col_order, m, R, flags, max_warps, ticket, loss_out, status, st, lut, mptr, first_row))
+    if (F <= 32) return HWP(1);
+    if (F == 64) return HWP(2);
+    if (F == 128) return HWP(4);
+    return HWP(8);
+#undef HWP
+}
+
+extern "C" int culsh_pack16(int64_t N, const int64_t *col_ptr, const int32_t *rows, const float *vals,
+                            const uint32_t *mask, int MW, const float *lut, int n_lut, uint16_t *words,
+                            int32_t *first_row, int *status, void *stream) {
+    CULSH_REQUIRE(MW == 1 || MW == 2, "MW must be 1 or 2");
+    CULSH_REQUIRE(n_lut >= 1 && n_lut <= 8, "the 2-byte stream holds 1..8 values");
+    if (N <= 0) return CULSH_OK;
+    const int64_t blocks = min64((N + 7) / 8, (int64_t)num_sms() * 16);
+    pack16_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(N, col_ptr, rows, vals, mask, MW, lut, n_lut,
+                                                                      words, first_row, status);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+

@@ -418,24 +418,47 @@ class TestPackedStream:
         mptr = nat.to_host(pk["mptr"])
         assert np.array_equal(mptr, np.concatenate([[0], np.cumsum(np.add.reduceat(hm, r.col_ptr[:-1])
                                                                    * (np.diff(r.col_ptr) > 0))]))
+        # the 2-byte records: rows = first_row + running deltas per column, same codes / flags
+        assert pk["w16"] is not None
+        w16 = nat.to_host(pk["w16"]).view(np.uint16)[:r.nnz].astype(np.int64)
+        first = nat.to_host(pk["first_row"])[:r.N]
+        col_of = np.repeat(np.arange(r.N), np.diff(r.col_ptr))
+        delta = w16 & 0xFFF
+        run = np.cumsum(delta) - np.repeat(np.cumsum(delta)[r.col_ptr[:-1]] - delta[r.col_ptr[:-1]],
+                                           np.diff(r.col_ptr))
+        assert np.array_equal(first[col_of] + run, rows)
+        assert np.array_equal(lut[(w16 >> 12) & 7], vals)
+        assert np.array_equal((w16 >> 15).astype(bool), hm)
 
-    def _serial(self, P, r, tbl, cfg, **kw):
+    def _serial(self, P, r, tbl, cfg, streamed=False, **kw):
+        """Columns one launch at a time (deterministic).  streamed: through the stream
+        format the host path ships (2-byte records when they fit) instead of the
+        device-resident one."""
         import torch
+        from paper_2111_11682_b200.factorization import _rates_struct
         from paper_2111_11682_b200.hogwild import HogwildTrainer
         tr = HogwildTrainer(r, tbl, cfg, **kw)
         for t in range(2):
             for j in range(r.N):
-                tr.launch_epoch(t, col_order=torch.tensor([j], dtype=torch.int32, device="cuda"), n_cols=1)
+                col = torch.tensor([j], dtype=torch.int32, device="cuda")
+                if streamed:
+                    tr._launch_packed(1, tr._stream_buffers(), col, _rates_struct(cfg.rates_at(t), cfg.regs),
+                                      tr.loss)
+                else:
+                    tr.launch_epoch(t, col_order=col, n_cols=1)
         torch.cuda.synchronize()
         return tr, tr.to_params()
 
+    @pytest.mark.parametrize("p16", [True, False])
     @pytest.mark.parametrize("rotate", [False, True])
     @pytest.mark.parametrize("K", [16, 40])
-    def test_packed_kernel_equals_wide(self, P, K, rotate):
+    def test_packed_kernel_equals_wide(self, P, K, rotate, p16):
+        """4-byte and (unrotated) 2-byte records make the wide kernel's updates."""
         r, tbl, cfg = self._problem(P, K)
-        ta, a = self._serial(P, r, tbl, cfg, packed=True, rotate=rotate)
+        ta, a = self._serial(P, r, tbl, cfg, streamed=True, packed=True, rotate=rotate, p16=p16)
         tb, b = self._serial(P, r, tbl, cfg, packed=False, rotate=rotate)
         assert ta.packed is not None and tb.packed is None
+        assert (ta.packed["w16"] is not None) == (p16 and not rotate)
         for name in ("b", "b_hat", "U", "V", "W", "C"):
             assert getattr(a, name).tobytes() == getattr(b, name).tobytes(), name
 
@@ -460,7 +483,7 @@ class TestPackedStream:
                     col, seg = wk["col"][s_:s_ + 1], wk["seg"][2 * s_:2 * s_ + 2]
                     if packed:
                         pk = tr.packed
-                        tr._launch_packed(1, pk["words"], pk["cmask"], tr.resid, col, rates, tr.loss, seg)
+                        tr._launch_packed(1, tr._stream_buffers(), col, rates, tr.loss, seg)
                     else:
                         d = tr.dev
                         nat.call("culsh_sgd_hogwild_epoch", 1, nat.ptr(d.col_ptr), nat.ptr(seg),
@@ -535,7 +558,7 @@ class TestPackedStream:
         r, tbl, cfg = self._problem(P, 16, M=3000, N=400, dens=0.03)
         tr = HogwildTrainer(r, tbl, cfg)
         host = tr.pinned_stream()
-        assert set(host) == {"words", "cmask", "resid"}
+        assert set(host) == {"w16", "first_row", "cmask", "resid"}
         losses, h2d, d2h = tr.train_from_host(host, 0, 3)
         assert h2d == sum(v.numel() * v.element_size() for v in host.values())
         assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
