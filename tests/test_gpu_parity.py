@@ -1020,3 +1020,27 @@ class TestAtScaleVsOracle:
         m = orc.parallel_train(csr, mu, nbr.entries, F, K, 1, 0, cfg.rates_at, cfg.regs, 16)
         assert p.U.tobytes() == m.U.tobytes() and p.V.tobytes() == m.V.tobytes()
         assert p.W.tobytes() == m.W.tobytes() and p.C.tobytes() == m.C.tobytes()
+
+
+def test_api_edge_behaviour_matches_reference(P):
+    """Small-edge behaviour of the public API, as the reference behaves (recorded from
+    lshmf on the same 3x2 matrix): tiny top-K tables, K > N-1, K = 0, zero epochs, empty
+    test set, out-of-range predict, config validation, D out of range."""
+    r = P.build_indices(P.Triplets(np.array([0, 1, 2]), np.array([0, 1, 0]), np.array([3., 4., 5.])), M=3, N=2)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(q=4), 1)
+    assert tbl.entries.tolist() == [[1], [0]]
+    with pytest.raises(ValueError):
+        P.simlsh_topk(r, P.LshConfig(q=4), 2)
+    assert P.train_full(r, None, P.TrainConfig(F=3, K=0, epochs=2)).U.shape == (3, 3)
+    assert P.train_full(r, None, P.TrainConfig(F=3, K=0, epochs=0)).U.shape == (3, 3)
+    p = P.train_full(r, None, P.TrainConfig(F=3, K=0, epochs=1))
+    with pytest.raises(ValueError):
+        P.rmse(p, P.Triplets(np.array([], int), np.array([], int), np.array([])), r)
+    with pytest.raises(IndexError):
+        P.predict(5, 0, p, r)
+    assert P.gsm_topk(r, P.SimilarityConfig(K=1)).entries.tolist() == [[1], [0]]
+    with pytest.raises(ValueError):
+        P.LshConfig(G=65).validate()
+    for D in (0, 5):
+        with pytest.raises(ValueError):
+            P.parallel_train(r, None, P.TrainConfig(F=3, K=0, epochs=1), D)
