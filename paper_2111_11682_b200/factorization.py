@@ -431,9 +431,7 @@ def train_basic(ratings: SparseRatings, config: TrainConfig, with_biases: bool =
         # rotated visiting order: the row-major transpose has short "columns" (a user's ~200
         # ratings) swept in near lock-step by every resident warp, so without it many warps
         # update the same item row from one stale copy at once (diverged at C3, 1 run in 2)
-        tr = HogwildTrainer(None, None, tcfg, dev=tdev, params=tp, rotate=True)
-        if not with_biases:   # biases stay 0: zero rates
-            tr.config = replace(tcfg, alpha_b=1e-300, alpha_b_hat=1e-300)
+        tr = HogwildTrainer(None, None, tcfg, dev=tdev, params=tp, rotate=True, train_biases=with_biases)
         for t in range(config.epochs):
             tr.epoch(t)
             if epoch_callback is not None:

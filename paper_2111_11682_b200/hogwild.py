@@ -64,7 +64,7 @@ class HogwildTrainer:
                  dev=None, params: ModelParams | None = None, rotate: bool = False,
                  max_warps: int | None = None, atomic_rows: bool = True,
                  packed: bool = True, split: bool = True, split_cap: int | None = None,
-                 p16: bool = True):
+                 p16: bool = True, train_biases: bool = True):
         config.validate()
         self.rotate = rotate
         self.atomic_rows = atomic_rows
@@ -111,6 +111,7 @@ class HogwildTrainer:
         self.ticket = nat.zeros((1,), "int32")
         self.status = nat.zeros((1,), "int32")
         self.loss = nat.zeros((1,), "float64")
+        self.train_biases = train_biases
         self.use_p16 = p16   # 2-byte records when deltas and values fit (not with rotation)
         self.packed = self._build_packed() if packed else None
         self.work = self._build_work_list(split_cap) if split else None
@@ -189,6 +190,14 @@ class HogwildTrainer:
                 "seg": nat.to_dev(seg.astype(np.int64), np.int64), "cap": int(cap),
                 "split_cols": int((nseg > 1).sum())}
 
+    def _rates(self, t_epoch: int):
+        """Epoch t's rates (factorization.py:99); with train_biases False the two bias
+        rates are 0, so b and b_hat keep their values (basic MF without biases)."""
+        r = list(self.config.rates_at(t_epoch))
+        if not self.train_biases:
+            r[0] = r[1] = 0.0
+        return _rates_struct(tuple(r), self.config.regs)
+
     def kernel_name(self) -> str:
         """The epoch kernel a whole-matrix launch_epoch (device-resident stream) runs."""
         F, K = self.config.F, self.K
@@ -208,7 +217,7 @@ class HogwildTrainer:
         """Enqueue one epoch (no host synchronisation).  With ``seg`` / ``col_order``
         it runs one DSGD block: the listed columns, entry ranges from seg."""
         c = self.config
-        rates = _rates_struct(c.rates_at(t_epoch), c.regs)
+        rates = self._rates(t_epoch)
         d = self.dev
         order = self.col_order if col_order is None else col_order
         n = d.N if n_cols is None else n_cols
@@ -279,7 +288,7 @@ class HogwildTrainer:
         """One epoch (or, with ``launch`` = (order, seg, n), part of one) over the stream
         buffers ``bufs``."""
         c = self.config
-        rates = _rates_struct(c.rates_at(t_epoch), c.regs)
+        rates = self._rates(t_epoch)
         d = self.dev
         order, seg, n, wflag = self.col_order, None, d.N, 0
         if self.work is not None:
