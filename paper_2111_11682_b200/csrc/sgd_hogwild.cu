@@ -137,15 +137,16 @@ constexpr int kHwDepth = 8;      // u_i prefetch depth (updates in flight per wa
 
 template <int FV, int KPL>
 constexpr int hw_smem_per_warp() {
-    // metadata window, mask word 1, u-row ring + b ring, start values of a work segment
-    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + kHwDepth * 32 * FV * 4 + kHwDepth * 4 + 32 * (FV + 2 * KPL + 1) * 4;
+    // metadata window, mask word 1, u-row ring, b_i and deferred b updates of the window,
+    // start values of a work segment
+    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + kHwDepth * 32 * FV * 4 + 2 * 64 * 4 + 32 * (FV + 2 * KPL + 1) * 4;
 }
 
 // FV floats per lane; F == 32*FV (vector path) or F < 32 with FV == 1 (masked).
 //
 // Per warp, shared memory holds (a) the column's next 64 entries' metadata
 // {row, value, mask, residual offset} refilled 32 at a time, read with one
-// broadcast LDS.128 per update, and (b) a ring of kHwDepth u-rows (+ b_i) that
+// broadcast LDS.128 per update (+ b_i of each entry), and (b) a ring of kHwDepth u-rows that
 // cp.async fills kHwDepth-1 updates ahead, so the HBM/L2 latency of the row
 // gather is off the update's critical path.  Each lane copies and later reads
 // only its own FV floats of every row, so the ring needs no warp barrier.
@@ -179,9 +180,10 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
     int4 *s_meta = reinterpret_cast<int4 *>(wbase);                           // 64 x 16 B
     uint32_t *s_m1 = reinterpret_cast<uint32_t *>(wbase + 64 * 16);           // KPL == 2
     float *s_ring = reinterpret_cast<float *>(wbase + 64 * 16 + (KPL == 2 ? 64 * 4 : 0));
-    float *s_bring = s_ring + P * 32 * FV;
+    float *s_b = s_ring + P * 32 * FV;   // b_i of the staged entries (cp.async at chunk load)
+    float *s_db = s_b + 64;               // their b updates, applied when the slot is refilled
     float *my_ring = s_ring + lane * FV;
-    float *my_start = s_bring + P + lane * (FV + 2 * KPL + 1);   // this lane's segment start values
+    float *my_start = s_db + 64 + lane * (FV + 2 * KPL + 1);   // this lane's segment start values
 
     const bool fl = FV > 1 || (int)lane < F;   // lane owns factor slots (F == 32*FV when FV > 1)
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -364,12 +366,23 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             const int slot = (32 * ch + lane) & 63;
             s_meta[slot] = make_int4(ri, __float_as_int(rv), (int)m0, roff);
             if constexpr (KPL == 2) s_m1[slot] = m1;
+            cp_async_bytes4(s_b + slot, Bv + ri);   // lands with the next committed group
+        };
+        // b_i is read when its entry is staged (32-64 updates ahead) and its update is
+        // applied when the slot is refilled: one gather and one atomic per lane per 32
+        // updates instead of a lane-0 copy and atomic per update (Hogwild staleness)
+        auto flush_b = [&](int first, int count) {
+            if ((int)lane < count) {
+                const int slot = (first + (int)lane) & 63;
+                const int ib = s_meta[slot].x;
+                if constexpr (ATOMIC) atomicAdd(Bv + ib, s_db[slot]);
+                else Bv[ib] = s_db[slot];
+            }
         };
         auto issue = [&](int tp) {
             const int ip = s_meta[tp & 63].x;
             float *dst = my_ring + (tp % P) * 32 * FV;
             if (fl) cp_async_row<FV>(dst, Ulane + (size_t)(unsigned)ip * (unsigned)F);
-            if (lane == 0) cp_async_bytes4(s_bring + (tp % P), Bv + ip);
         };
 
         load_chunk(0);
@@ -382,145 +395,162 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         }
         float lossf = 0.f;
         const float ngu = -R.gu * (1.f - R.au) / R.gu;   // = -(gu*lu): delta_u = ngu*u + gu*e*v
-        for (int base = 0; base < n; base += 32) {
-            if (base > 0) {
-                __syncwarp();   // every lane is done with the half being refilled
-                if (base + 32 < n) load_chunk((base >> 5) + 1);
-                __syncwarp();
+        // one update: entry in metadata slot ms / ring slot rsl; prefetch of the entry P-1
+        // ahead (slots pms / prs)
+        auto step = [&](const int ms, const int pms, const int rsl, const int prs) {
+            // prefetch P-1 ahead.  Past the column's end the slot holds a padding (0) or an
+            // older row of this launch (s_meta is zeroed at entry): always a valid row, the
+            // copy lands in a ring slot nobody reads before the column's final wait.
+            {
+                const int ip = s_meta[pms].x;
+                float *dst = my_ring + prs * 32 * FV;
+                if (fl) cp_async_row<FV>(dst, Ulane + (size_t)(unsigned)ip * (unsigned)F);
             }
-            const int cnt = min(32, n - base);
-            for (int k = 0; k < cnt; ++k) {
-                const int tt = base + k;
-                // prefetch P-1 ahead.  Past the column's end the slot holds a padding (0) or an
-                // older row of this launch (s_meta is zeroed at entry): always a valid row, the
-                // copy lands in a ring slot nobody reads before the column's final wait.
-                {
-                    const int tp = tt + P - 1;
-                    const int ip = s_meta[tp & 63].x;
-                    float *dst = my_ring + (tp % P) * 32 * FV;
-                    if (fl) cp_async_row<FV>(dst, Ulane + (size_t)(unsigned)ip * (unsigned)F);
-                    if (lane == 0) cp_async_bytes4(s_bring + (tp % P), Bv + ip);
+            cp_async_commit();
+            cp_async_wait<P - 1>();
+            const int4 me = s_meta[ms];
+            const int i = me.x;
+            const float r = __int_as_float(me.y);
+            const uint32_t m0 = (uint32_t)me.z;
+            const uint32_t m1 = KPL == 2 ? s_m1[ms] : 0u;
+            float u[FV];
+            load_row<FV>(my_ring + rsl * 32 * FV, u);
+            if constexpr (FV == 1) {
+                if (!fl) u[0] = 0.f;   // lanes >= F never fill their ring slot (garbage, maybe NaN)
+            }
+            const float bi = s_b[ms];
+            float part;
+            if constexpr (FV % 2 == 0) {
+                // paired fp32 (FFMA2): even / odd factor partial sums, folded once
+                uint64_t acc = pack2(0.f, 0.f);
+#pragma unroll
+                for (int x = 0; x < FV; x += 2) acc = ffma2(pack2(u[x], u[x + 1]), pack2(v[x], v[x + 1]), acc);
+                part = lo2(acc) + hi2(acc);
+            } else {
+                part = 0.f;
+#pragma unroll
+                for (int x = 0; x < FV; ++x) part = fmaf(u[x], fl ? v[x] : 0.f, part);
+            }
+            const bool anyex = (m0 | m1) != 0u;   // warp-uniform
+            float inv_r = 0.f, inv_n = invK;
+            float rs[KPL];
+            bool ex[KPL];
+            if (!anyex) {
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) {
+                    ex[q] = false;
+                    rs[q] = 0.f;
+                    part = fmaf(c[q], invK, part);
                 }
-                cp_async_commit();
-                cp_async_wait<P - 1>();
-                const int4 me = s_meta[tt & 63];
-                const int i = me.x;
-                const float r = __int_as_float(me.y);
-                const uint32_t m0 = (uint32_t)me.z;
-                const uint32_t m1 = KPL == 2 ? s_m1[tt & 63] : 0u;
-                float u[FV];
-                load_row<FV>(my_ring + (tt % P) * 32 * FV, u);
-                if constexpr (FV == 1) {
-                    if (!fl) u[0] = 0.f;   // lanes >= F never fill their ring slot (garbage, maybe NaN)
+            } else {
+                const int nr = __popc(m0) + __popc(m1);
+                const int nn = K - nr;
+                inv_r = rsqrtf((float)nr);
+                inv_n = nn > 0 ? rsqrtf((float)nn) : 0.f;
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) {
+                    const uint32_t mq = q == 0 ? m0 : m1;
+                    ex[q] = (mq >> lane) & 1u;
+                    const int rank = (q == 0 ? 0 : __popc(m0)) + __popc(mq & lt_mask);
+                    rs[q] = ex[q] ? rcol[me.w + rank] : 0.f;
+                    part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;
                 }
-                const float bi = lane == 0 ? s_bring[tt % P] : 0.f;
-                float part;
+            }
+            part = warp_sum(part);
+            const float e = r - (mu + bh + bi + part);
+            lossf = fmaf(e, e, lossf);
+            // fused update of every touched parameter (factorization.py:307-328 rules)
+            const float geu = R.gu * e, gev = R.gv * e;
+            float* urow = U + (size_t)(unsigned)i * (unsigned)F + lane * FV;
+            if constexpr (ATOMIC) {
+                // add the update instead of storing the new value: a concurrent update of the
+                // same row by another warp is then never lost (only computed from a stale u_i)
+                float dlt[FV];
                 if constexpr (FV % 2 == 0) {
-                    // paired fp32 (FFMA2): even / odd factor partial sums, folded once
-                    uint64_t acc = pack2(bi, 0.f);
+                    const uint64_t ngu2 = pack2(ngu, ngu), geu2 = pack2(geu, geu);
+                    const uint64_t av2 = pack2(R.av, R.av), gev2 = pack2(gev, gev);
 #pragma unroll
-                    for (int x = 0; x < FV; x += 2) acc = ffma2(pack2(u[x], u[x + 1]), pack2(v[x], v[x + 1]), acc);
-                    part = lo2(acc) + hi2(acc);
-                } else {
-                    part = bi;
-#pragma unroll
-                    for (int x = 0; x < FV; ++x) part = fmaf(u[x], fl ? v[x] : 0.f, part);
-                }
-                const bool anyex = (m0 | m1) != 0u;   // warp-uniform
-                float inv_r = 0.f, inv_n = invK;
-                float rs[KPL];
-                bool ex[KPL];
-                if (!anyex) {
-#pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
-                        ex[q] = false;
-                        rs[q] = 0.f;
-                        part = fmaf(c[q], invK, part);
+                    for (int x = 0; x < FV; x += 2) {
+                        const uint64_t uo = pack2(u[x], u[x + 1]), vo = pack2(v[x], v[x + 1]);
+                        const uint64_t d = ffma2(ngu2, uo, fmul2(geu2, vo));
+                        const uint64_t vn = ffma2(av2, vo, fmul2(gev2, uo));
+                        dlt[x] = lo2(d); dlt[x + 1] = hi2(d);
+                        v[x] = lo2(vn); v[x + 1] = hi2(vn);
                     }
-                } else {
-                    const int nr = __popc(m0) + __popc(m1);
-                    const int nn = K - nr;
-                    inv_r = rsqrtf((float)nr);
-                    inv_n = nn > 0 ? rsqrtf((float)nn) : 0.f;
-#pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
-                        const uint32_t mq = q == 0 ? m0 : m1;
-                        ex[q] = (mq >> lane) & 1u;
-                        const int rank = (q == 0 ? 0 : __popc(m0)) + __popc(mq & lt_mask);
-                        rs[q] = ex[q] ? rcol[me.w + rank] : 0.f;
-                        part += ex[q] ? rs[q] * w[q] * inv_r : c[q] * inv_n;
-                    }
-                }
-                part = warp_sum(part);
-                const float e = r - (mu + bh + part);
-                lossf = fmaf(e, e, lossf);
-                // fused update of every touched parameter (factorization.py:307-328 rules)
-                const float geu = R.gu * e, gev = R.gv * e;
-                float* urow = U + (size_t)(unsigned)i * (unsigned)F + lane * FV;
-                if constexpr (ATOMIC) {
-                    // add the update instead of storing the new value: a concurrent update of the
-                    // same row by another warp is then never lost (only computed from a stale u_i)
-                    float dlt[FV];
-                    if constexpr (FV % 2 == 0) {
-                        const uint64_t ngu2 = pack2(ngu, ngu), geu2 = pack2(geu, geu);
-                        const uint64_t av2 = pack2(R.av, R.av), gev2 = pack2(gev, gev);
-#pragma unroll
-                        for (int x = 0; x < FV; x += 2) {
-                            const uint64_t uo = pack2(u[x], u[x + 1]), vo = pack2(v[x], v[x + 1]);
-                            const uint64_t d = ffma2(ngu2, uo, fmul2(geu2, vo));
-                            const uint64_t vn = ffma2(av2, vo, fmul2(gev2, uo));
-                            dlt[x] = lo2(d); dlt[x + 1] = hi2(d);
-                            v[x] = lo2(vn); v[x + 1] = hi2(vn);
-                        }
-                    } else {
-#pragma unroll
-                        for (int x = 0; x < FV; ++x) {
-                            const float uo = u[x];
-                            dlt[x] = fmaf(ngu, uo, geu * v[x]);
-                            v[x] = fmaf(R.av, v[x], gev * uo);
-                        }
-                    }
-                    if (fl) {
-                        if constexpr (FV % 4 == 0) {
-#pragma unroll
-                            for (int x = 0; x < FV; x += 4)
-                                atomicAdd(reinterpret_cast<float4 *>(urow + x),
-                                          make_float4(dlt[x], dlt[x + 1], dlt[x + 2], dlt[x + 3]));
-                        } else if constexpr (FV == 2) {
-                            atomicAdd(reinterpret_cast<float2 *>(urow), make_float2(dlt[0], dlt[1]));
-                        } else {
-                            atomicAdd(urow, dlt[0]);
-                        }
-                    }
-                    if (lane == 0) atomicAdd(Bv + i, fmaf(R.ab - 1.f, bi, R.gb * e));
                 } else {
 #pragma unroll
                     for (int x = 0; x < FV; ++x) {
                         const float uo = u[x];
-                        u[x] = fmaf(R.au, uo, geu * v[x]);
+                        dlt[x] = fmaf(ngu, uo, geu * v[x]);
                         v[x] = fmaf(R.av, v[x], gev * uo);
                     }
-                    if (fl) store_row<FV>(urow, u);
-                    if (lane == 0) Bv[i] = fmaf(R.ab, bi, R.gb * e);
                 }
-                bh = fmaf(R.abh, bh, R.gbh * e);
-                if (!anyex) {
-                    // no explicit neighbour: only the implicit weights move (kgc = 0 off K)
+                if (fl) {
+                    if constexpr (FV % 4 == 0) {
 #pragma unroll
-                    for (int q = 0; q < KPL; ++q) c[q] = fmaf(R.ac, c[q], kgc[q] * e);
-                } else {
-                    const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
-#pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
-                        const float wn = fmaf(R.aw, w[q], gwe * rs[q]);
-                        const float cn = fmaf(R.ac, c[q], gce);
-                        w[q] = (kin[q] && ex[q]) ? wn : w[q];
-                        c[q] = (kin[q] && !ex[q]) ? cn : c[q];
+                        for (int x = 0; x < FV; x += 4)
+                            atomicAdd(reinterpret_cast<float4 *>(urow + x),
+                                      make_float4(dlt[x], dlt[x + 1], dlt[x + 2], dlt[x + 3]));
+                    } else if constexpr (FV == 2) {
+                        atomicAdd(reinterpret_cast<float2 *>(urow), make_float2(dlt[0], dlt[1]));
+                    } else {
+                        atomicAdd(urow, dlt[0]);
                     }
+                }
+                s_db[ms] = fmaf(R.ab - 1.f, bi, R.gb * e);   // same value from every lane
+            } else {
+#pragma unroll
+                for (int x = 0; x < FV; ++x) {
+                    const float uo = u[x];
+                    u[x] = fmaf(R.au, uo, geu * v[x]);
+                    v[x] = fmaf(R.av, v[x], gev * uo);
+                }
+                if (fl) store_row<FV>(urow, u);
+                s_db[ms] = fmaf(R.ab, bi, R.gb * e);
+            }
+            bh = fmaf(R.abh, bh, R.gbh * e);
+            if (!anyex) {
+                // no explicit neighbour: only the implicit weights move (kgc = 0 off K)
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) c[q] = fmaf(R.ac, c[q], kgc[q] * e);
+            } else {
+                const float gce = R.gc * inv_n * e, gwe = R.gw * inv_r * e;
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) {
+                    const float wn = fmaf(R.aw, w[q], gwe * rs[q]);
+                    const float cn = fmaf(R.ac, c[q], gce);
+                    w[q] = (kin[q] && ex[q]) ? wn : w[q];
+                    c[q] = (kin[q] && !ex[q]) ? cn : c[q];
+                }
+            }
+        };
+        for (int base = 0; base < n; base += 32) {
+            if (base > 0) {
+                __syncwarp();   // every lane is done with the half being refilled
+                flush_b(base - 32, 32);
+                if (base + 32 < n) load_chunk((base >> 5) + 1);
+                __syncwarp();
+            }
+            const int cnt = min(32, n - base);
+            if (FV <= 4 && cnt == 32) {
+                // whole chunk: P-update groups with compile-time ring slots (base % 32 == 0);
+                // FV == 8 keeps the rolled loop (register budget of 4 CTAs per SM)
+                static_assert(32 % P == 0, "ring depth must divide the chunk");
+                for (int k = 0; k < 32; k += P) {
+                    const int g0 = (base + k) & 63, g1 = (base + k + P) & 63;
+#pragma unroll
+                    for (int s = 0; s < P; ++s) step(g0 + s, s == 0 ? g0 + P - 1 : g1 + s - 1, s, (s + P - 1) % P);
+                }
+            } else {
+                for (int k = 0; k < cnt; ++k) {
+                    const int tt = base + k;
+                    step(tt & 63, (tt + P - 1) & 63, tt % P, (tt + P - 1) % P);
                 }
             }
         }
         cp_async_wait<0>();
+        __syncwarp();
+        if (n > 0) flush_b(((n - 1) >> 5) << 5, n - (((n - 1) >> 5) << 5));
         if (!isfinite(lossf)) bad = 1;
         col_loss += (double)lossf;
         if (!part_col) {
