@@ -55,11 +55,17 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
     return d;
 }
 
+// u-row ring slot layout: FV % 4 == 0 stores a lane's floats 4..7, 8..11, ... in further
+// 512-byte planes (plane q/4 at +32*q floats), so every 16-byte access of the warp covers
+// 512 contiguous bytes (bank-conflict-free); otherwise lane-contiguous FV floats.
+template <int FV>
+constexpr int ring_lane_stride() { return FV % 4 == 0 ? 4 : FV; }
+
 template <int FV>
 __device__ __forceinline__ void cp_async_row(float *dst, const float *src) {
     if constexpr (FV % 4 == 0) {
 #pragma unroll
-        for (int x = 0; x < FV; x += 4) cp_async_bytes16(dst + x, src + x);
+        for (int x = 0; x < FV; x += 4) cp_async_bytes16(dst + 32 * x, src + x);
     } else if constexpr (FV == 4) {
         cp_async_bytes16(dst, src);
     } else if constexpr (FV == 2) {
@@ -125,6 +131,23 @@ __device__ __forceinline__ void load_row(const float *__restrict__ p, float (&x)
     }
 }
 
+// Ring read (layout: ring_lane_stride): one 16-byte ld.shared per 4 floats.  (Left to itself the compiler splits the
+// float4 into two 8-byte loads, which at a 16-byte lane stride are 2-way bank-conflicted:
+// 8 shared wavefronts per row instead of 4.)
+template <int FV>
+__device__ __forceinline__ void load_ring(const float *p, float (&x)[FV]) {
+    if constexpr (FV % 4 == 0) {
+        const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+#pragma unroll
+        for (int q = 0; q < FV; q += 4)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x[q]), "=f"(x[q + 1]), "=f"(x[q + 2]), "=f"(x[q + 3])
+                         : "r"(a + 4 * 32 * q));
+    } else {
+        load_row<FV>(p, x);
+    }
+}
+
 // Decay factors a = 1 - gamma*lambda of the six rules, so every update is
 // x' = a*x + gamma*(gradient term): one FMUL + one FFMA per element.
 struct HwCoef {
@@ -182,7 +205,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
     float *s_ring = reinterpret_cast<float *>(wbase + 64 * 16 + (KPL == 2 ? 64 * 4 : 0));
     float *s_b = s_ring + P * 32 * FV;   // b_i of the staged entries (cp.async at chunk load)
     float *s_db = s_b + 64;               // their b updates, applied when the slot is refilled
-    float *my_ring = s_ring + lane * FV;
+    float *my_ring = s_ring + lane * ring_lane_stride<FV>();
     float *my_start = s_db + 64 + lane * (FV + 2 * KPL + 1);   // this lane's segment start values
 
     const bool fl = FV > 1 || (int)lane < F;   // lane owns factor slots (F == 32*FV when FV > 1)
@@ -414,7 +437,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             const uint32_t m0 = (uint32_t)me.z;
             const uint32_t m1 = KPL == 2 ? s_m1[ms] : 0u;
             float u[FV];
-            load_row<FV>(my_ring + rsl * 32 * FV, u);
+            load_ring<FV>(my_ring + rsl * 32 * FV, u);
             if constexpr (FV == 1) {
                 if (!fl) u[0] = 0.f;   // lanes >= F never fill their ring slot (garbage, maybe NaN)
             }
