@@ -959,6 +959,37 @@ def test_hogwild_shapes_c1(P, c1, F, K):
     assert abs(hog - exact) <= REF_TOL_RMSE, (F, K, hog, exact)
 
 
+def test_hogwild_divergence_raises(P):
+    """A diverging Hogwild fit (non-finite partials take the fp32 shuffle reduction, not the
+    fixed-point redux) raises TrainingDivergedError like the exact modes."""
+    rng = np.random.default_rng(42)
+    mask = rng.random((40, 30)) < 0.5
+    rows, cols = np.nonzero(mask)
+    r = P.SparseRatings(40, 30, rows, cols, rng.integers(1, 6, len(rows)).astype(float))
+    ent = np.stack([np.delete(np.arange(30), j)[:4] for j in range(30)]).astype(np.int32)
+    cfg = P.TrainConfig(F=128, K=4, alpha_b=1e12, alpha_b_hat=1e12, alpha_u=1e12, alpha_v=1e12,
+                        alpha_w=1e12, alpha_c=1e12, epochs=3, seed=1)
+    with pytest.raises(P.TrainingDivergedError):
+        P.train_full(r, P.NeighborTable(30, 4, ent), cfg, mode="hogwild")
+
+
+def test_hogwild_large_magnitude_ratings(P, c1):
+    """Ratings on a 0-100 scale (the Yahoo-style values of C5): per-lane partial sums can
+    leave the fixed-point reduction's +-32 window, where the kernel falls back to the fp32
+    shuffle tree; Hogwild still lands within the tolerance (scaled by 20) of the exact fit."""
+    z, tr, te = c1
+    s = 20.0
+    tr2 = P.SparseRatings(tr.M, tr.N, z["train_rows"].astype(np.int32), z["train_cols"].astype(np.int32),
+                          z["train_vals"].astype(np.float64) * s)
+    te2 = P.Triplets(te.rows, te.cols, te.values * s)
+    nbr = P.NeighborTable(tr.N, 32, z["lsh_entries32"])
+    cfg = P.TrainConfig(F=128, K=32, epochs=8, seed=0, alpha_b=0.002, alpha_b_hat=0.002, alpha_u=0.002,
+                        alpha_v=0.002, alpha_w=0.0001, alpha_c=0.0001)
+    exact = P.rmse(P.train_full(tr2, nbr, cfg), te2, tr2)
+    hog = P.rmse(P.train_full(tr2, nbr, cfg, mode="hogwild"), te2, tr2)
+    assert np.isfinite(hog) and abs(hog - exact) <= REF_TOL_RMSE * s, (hog, exact)
+
+
 @pytest.mark.parametrize("F,K", [(128, 40), (256, 64), (1, 1)])
 def test_exact_mode_large_shapes_vs_oracle(P, orc, F, K):
     """Exact mode at shapes the reference fixtures do not reach (F up to 256, K > 32 with
