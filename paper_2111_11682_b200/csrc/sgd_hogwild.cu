@@ -6,9 +6,11 @@
 // streamed in CSC order (row, value, explicit-neighbour mask, compact residuals)
 // and every update reads and writes the row parameters u_i / b_i in HBM without
 // locks (rows are Hogwild, as in Alg. 3).  Per update the warp does one float4
-// gather of u_i per lane, one fused shuffle reduction of
+// gather of u_i per lane, one fused warp reduction of
 //   u_i.v_j + |R|^-1/2 sum_expl resid*w + |N|^-1/2 sum_impl c
-// and one float4 store of the updated u_i.  Columns are handed out through a
+// and one float4 atomic add of the u_i delta (b_i travels with the entry window:
+// read when the entry is staged, its update applied when the slot is refilled).
+// Columns are handed out through a
 // ticket counter in descending-nnz order (longest first) for load balance.
 //
 // The explicit-neighbour test and residuals depend only on (data, J^K)
