@@ -959,6 +959,48 @@ def test_hogwild_shapes_c1(P, c1, F, K):
     assert abs(hog - exact) <= REF_TOL_RMSE, (F, K, hog, exact)
 
 
+def test_hogwild_dsgd_stages_c1(P, c1):
+    """The multi-GPU DSGD performance path (dsgd.bench_main): each stage runs the Hogwild
+    kernel on (row block, column block) entry ranges from culsh_pass_plan.  Here one process
+    runs every rank's block of a stage in one launch; the D stages cover every rating once
+    per epoch and the fit lands within the RMSE bar of the exact mode."""
+    import torch
+    from paper_2111_11682_b200 import _native as nat
+    from paper_2111_11682_b200.dsgd import RingPlan
+    from paper_2111_11682_b200.hogwild import HogwildTrainer
+    z, tr, te = c1
+    nbr = P.NeighborTable(tr.N, 32, z["lsh_entries32"])
+    cfg = P.TrainConfig(F=32, K=32, epochs=12, seed=0)
+    exact = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
+    D = 3
+    ht = HogwildTrainer(tr, nbr, cfg)
+    d = ht.dev
+    M, N = d.M, d.N
+    plan = RingPlan(D, M, N)
+    rb_t = nat.to_dev(plan.row_bounds)
+    bp = nat.empty((N * (D + 1),), "int64")
+    nat.call("culsh_block_pointers", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), N, nat.ptr(rb_t), D + 1,
+             nat.ptr(bp), nat.stream_ptr())
+    cbt = nat.to_dev(plan.col_bounds)
+    segs = []
+    for s in range(D):
+        seg = nat.zeros((2 * N,), "int64")
+        chain = nat.zeros((N,), "int32")
+        nat.call("culsh_pass_plan", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), N, 1, 0, N, 0, M,
+                 nat.ptr(bp), nat.ptr(cbt), D, s, nat.ptr(seg), nat.ptr(chain), nat.stream_ptr())
+        segs.append(seg)
+    sh = nat.to_host
+    covered = sum(sh(sg)[1::2].astype(np.int64) - sh(sg)[0::2] for sg in segs)
+    assert np.array_equal(covered, np.diff(sh(d.col_ptr)))          # every rating once per epoch
+    cols = torch.arange(N, dtype=torch.int32, device="cuda")
+    for ep in range(cfg.epochs):
+        for s in range(D):
+            ht.launch_epoch(ep, seg=segs[s], col_order=cols, n_cols=N)
+    assert int(ht.status.item()) == 0
+    hog = P.rmse(ht.to_params(), te, tr)
+    assert abs(hog - exact) <= REF_TOL_RMSE, (hog, exact)
+
+
 def test_hogwild_divergence_raises(P):
     """A diverging Hogwild fit (non-finite partials take the fp32 shuffle reduction, not the
     fixed-point redux) raises TrainingDivergedError like the exact modes."""
