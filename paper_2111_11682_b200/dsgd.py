@@ -302,7 +302,8 @@ def bench_main(args, metric, workload, rates):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
                 "data": "synthetic (random_sparse distribution generated in HBM)",
                 "config": {"workload": workload[args.config], "parallelism": f"dsgd{D}",
-                           "exchange": "NCCL send/recv ring shift of u/b row blocks per stage",
+                           "exchange": ("NCCL send/recv ring shift of u/b row blocks per stage" if backend == "nccl" else
+                                        f"{backend} ring shift of u/b row blocks per stage (host-staged)"),
                            "l2": "inputs larger than L2, no flush"},
                 "lsh_build_s": lsh_s,
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
