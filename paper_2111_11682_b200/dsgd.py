@@ -247,9 +247,13 @@ def bench_main(args, metric, workload, rates):
     U = tr.model.U.view(M, F)
     b = tr.model.b
 
+    # per-stage work lists: own columns' block ranges, split when the block has fewer
+    # columns than the GPU has resident warps (HogwildTrainer.block_work)
+    works = [tr.block_work(segs[s], own) for s in range(D)]
+
     def stage(ep):
         def fn(s, rb):
-            tr.launch_epoch(ep, seg=segs[s], col_order=own, n_cols=own.numel())
+            tr.launch_work(ep, works[s])
         return fn
 
     for w in range(args.warmup):
@@ -275,17 +279,23 @@ def bench_main(args, metric, workload, rates):
     # e2e: every step each rank copies ITS column block's rating stream (rows,
     # values, masks) from pinned host memory, runs the epoch, reads the loss back
     lo_e, hi_e = int(d.col_ptr[cs.start].item()), int(d.col_ptr[cs.stop].item())
-    host = {"rows": d.col_rows[lo_e:hi_e].cpu().pin_memory(),
-            "vals": tr.vals32[lo_e:hi_e].cpu().pin_memory(),
-            "mask": tr.mask[lo_e * tr.MW:hi_e * tr.MW].cpu().pin_memory()}
+    r_lo, r_hi = int(tr.resid_ptr[cs.start].item()), int(tr.resid_ptr[cs.stop].item())
+    if tr.packed is not None:   # the arrays the stage kernels read: packed records, masks, residuals
+        pk = tr.packed
+        m_lo, m_hi = int(pk["mptr"][cs.start].item()) * tr.MW, int(pk["mptr"][cs.stop].item()) * tr.MW
+        dev_views = {"words": pk["words"][lo_e:hi_e], "cmask": pk["cmask"][m_lo:m_hi],
+                     "resid": tr.resid[r_lo:r_hi]}
+    else:
+        dev_views = {"rows": d.col_rows[lo_e:hi_e], "vals": tr.vals32[lo_e:hi_e],
+                     "mask": tr.mask[lo_e * tr.MW:hi_e * tr.MW], "resid": tr.resid[r_lo:r_hi]}
+    host = {k: v.cpu().pin_memory() for k, v in dev_views.items()}
     e_steps = max(1, min(args.steps, 3))
     torch.cuda.synchronize()
     dist.barrier()
     w0 = time.perf_counter()
     for s in range(e_steps):
-        d.col_rows[lo_e:hi_e].copy_(host["rows"], non_blocking=True)
-        tr.vals32[lo_e:hi_e].copy_(host["vals"], non_blocking=True)
-        tr.mask[lo_e * tr.MW:hi_e * tr.MW].copy_(host["mask"], non_blocking=True)
+        for k, v in dev_views.items():
+            v.copy_(host[k], non_blocking=True)
         tr.loss.zero_()
         run_epoch(plan, rank, stage(args.warmup + args.steps + s), [U, b])
         float(tr.loss.item())

@@ -190,6 +190,50 @@ class HogwildTrainer:
                 "seg": nat.to_dev(seg.astype(np.int64), np.int64), "cap": int(cap),
                 "split_cols": int((nseg > 1).sum())}
 
+    def block_work(self, seg, cols) -> dict:
+        """Per-ticket work list of one DSGD block (multi-GPU stage): column j of ``cols``
+        runs entries [seg[2j], seg[2j+1]).  When the block has fewer columns than the GPU has
+        resident warps (D = 8 at C3: 2,221 columns for 4,736 warps), each column's range is
+        cut into S segments of about total / warps entries, merged like the work segments of
+        _build_work_list (1/S-averaged column parameters), so the stage fills the GPU;
+        otherwise S = 1 everywhere.  Launched with launch_work (packed stream when built)."""
+        t = nat.torch()
+        cols_h = nat.to_host(cols).astype(np.int64)
+        seg_h = nat.to_host(seg).astype(np.int64).reshape(-1, 2)[cols_h]
+        lo, hi = seg_h[:, 0], seg_h[:, 1]
+        cnt = hi - lo
+        warps = 32 * t.cuda.get_device_properties(nat.device()).multi_processor_count
+        if len(cols_h) >= warps or cnt.sum() == 0:
+            nseg = np.ones(len(cols_h), np.int64)
+        else:
+            L = max(64, -(-int(cnt.sum()) // warps))
+            nseg = np.maximum(1, -(-cnt // L))
+        idx = np.repeat(np.arange(len(cols_h)), nseg)
+        first = np.repeat(np.cumsum(nseg) - nseg, nseg)
+        part = np.arange(len(idx)) - first
+        ns = nseg[idx]
+        s_lo = lo[idx] + (cnt[idx] * part) // ns
+        s_hi = lo[idx] + (cnt[idx] * (part + 1)) // ns
+        order = np.argsort(-(s_hi - s_lo), kind="stable")   # longest first
+        sg = np.stack([s_lo[order], s_hi[order] | (ns[order] << 40)], axis=1).reshape(-1)
+        return {"n": int(len(order)), "col": nat.to_dev(cols_h[idx][order].astype(np.int32), np.int32),
+                "seg": nat.to_dev(sg.astype(np.int64), np.int64), "split_cols": int((nseg > 1).sum())}
+
+    def launch_work(self, t_epoch: int, work: dict) -> None:
+        """Enqueue one block_work list (no host synchronisation)."""
+        rates = self._rates(t_epoch)
+        if self.packed is not None:
+            self._launch_packed(work["n"], self._stream_buffers(resident=True), work["col"], rates, self.loss,
+                                work["seg"])
+            return
+        d = self.dev
+        nat.call("culsh_sgd_hogwild_epoch", work["n"], nat.ptr(d.col_ptr), nat.ptr(work["seg"]),
+                 nat.ptr(d.col_rows), nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
+                 nat.ptr(self.resid), nat.ptr(work["col"]), ctypes.byref(self.model.struct),
+                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0) | 8,
+                 int(self.max_warps), nat.ptr(self.ticket), nat.ptr(self.loss), nat.ptr(self.status),
+                 nat.stream_ptr())
+
     def _rates(self, t_epoch: int):
         """Epoch t's rates (factorization.py:99); with train_biases False the two bias
         rates are 0, so b and b_hat keep their values (basic MF without biases)."""

@@ -959,7 +959,8 @@ def test_hogwild_shapes_c1(P, c1, F, K):
     assert abs(hog - exact) <= REF_TOL_RMSE, (F, K, hog, exact)
 
 
-def test_hogwild_dsgd_stages_c1(P, c1):
+@pytest.mark.parametrize("work", [False, True])
+def test_hogwild_dsgd_stages_c1(P, c1, work):
     """The multi-GPU DSGD performance path (dsgd.bench_main): each stage runs the Hogwild
     kernel on (row block, column block) entry ranges from culsh_pass_plan.  Here one process
     runs every rank's block of a stage in one launch; the D stages cover every rating once
@@ -993,9 +994,15 @@ def test_hogwild_dsgd_stages_c1(P, c1):
     covered = sum(sh(sg)[1::2].astype(np.int64) - sh(sg)[0::2] for sg in segs)
     assert np.array_equal(covered, np.diff(sh(d.col_ptr)))          # every rating once per epoch
     cols = torch.arange(N, dtype=torch.int32, device="cuda")
+    if work:   # block_work lists (packed stream; C1 has fewer columns than warps: split)
+        works = [ht.block_work(sg, cols) for sg in segs]
+        assert all(w["split_cols"] > 0 for w in works)
     for ep in range(cfg.epochs):
         for s in range(D):
-            ht.launch_epoch(ep, seg=segs[s], col_order=cols, n_cols=N)
+            if work:
+                ht.launch_work(ep, works[s])
+            else:
+                ht.launch_epoch(ep, seg=segs[s], col_order=cols, n_cols=N)
     assert int(ht.status.item()) == 0
     hog = P.rmse(ht.to_params(), te, tr)
     assert abs(hog - exact) <= REF_TOL_RMSE, (hog, exact)
