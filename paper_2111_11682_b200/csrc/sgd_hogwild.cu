@@ -279,6 +279,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         int rrel2 = 0;   // residual offset (relative to the column base) at position lo
         if (PACK && lo > c_lo) {   // work segment: mask cursor and residual offset at lo
             int h = 0, dsum = 0;
+#pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = c_lo + lane; x < lo; x += 32) {
                 if constexpr (P16) {
                     const uint32_t w16 = __ldg(p16 + x);
@@ -291,6 +292,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             h = warp_sum(h);
             if constexpr (P16) carry += warp_sum(dsum);
             int skip = 0;
+#pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = mrun2 + lane; x < mrun2 + h; x += 32)
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
@@ -299,6 +301,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             rrel2 = warp_sum(skip);
         } else if (lo > c_lo) {   // DSGD block: skip the residuals of the column's earlier row blocks
             int skip = 0;
+#pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = c_lo + lane; x < lo; x += 32)
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
@@ -307,10 +310,12 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         int rrel1 = rrel2;   // ... at position lo + rot
         if (PACK && rot > 0) {
             int h = 0;
+#pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = lo + lane; x < lo + rot; x += 32)
                 h += (int)(__ldg(reinterpret_cast<const uint32_t *>(rows) + x) >> 31);
             h = warp_sum(h);
             int skip = 0;
+#pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = mrun2 + lane; x < mrun2 + h; x += 32)
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
@@ -318,6 +323,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             rrel1 += warp_sum(skip);
         } else if (rot > 0) {
             int skip = 0;
+#pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = lo + lane; x < lo + rot; x += 32)
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) skip += __popc(mask[x * KPL + q]);
