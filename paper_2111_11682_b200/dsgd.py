@@ -60,6 +60,13 @@ class RingPlan:
     def cols(self, cb: int) -> slice:
         return slice(int(self.col_bounds[cb]), int(self.col_bounds[cb + 1]))
 
+    def sub_rows(self, rb: int, part: int, parts: int) -> slice:
+        """Part `part` of row block rb cut into `parts`: block rb*parts + part of the
+        D*parts-way partition (whose bounds contain the D-way bounds: (k*M)//D ==
+        (k*parts*M)//(D*parts))."""
+        k, n = rb * parts + part, self.D * parts
+        return slice((k * self.M) // n, ((k + 1) * self.M) // n)
+
 
 def _host_staging() -> bool:
     """Gloo has no CUDA send/recv: stage device tensors through host memory."""
@@ -100,11 +107,68 @@ def ring_shift(plan: RingPlan, rank: int, stage: int, tensors, group=None) -> No
             view.copy_(buf)
 
 
-def run_epoch(plan: RingPlan, rank: int, stage_fn, row_tensors, group=None) -> None:
-    """One DSGD epoch: D stages, each followed by the ring shift."""
+def _shift_part(plan: RingPlan, rank: int, stage: int, part: int, parts: int, tensors, group=None):
+    """Start the ring shift of one row sub-block: send part `part` of the block trained at
+    `stage` to rank-1, receive the same part of the next stage's block from rank+1.
+    Returns a finisher.  With NCCL the requests run on NCCL's stream, which waits only for
+    the work enqueued before this call (the sub-block's stage kernel), so the transfer
+    overlaps the next sub-block's kernel; finishing makes the current stream wait for it."""
+    import torch.distributed as dist
+    send_rows = plan.sub_rows(plan.row_block(rank, stage), part, parts)
+    recv_rows = plan.sub_rows(plan.row_block(rank, stage + 1), part, parts)
+    dst, src = plan.send_peer(rank), plan.recv_peer(rank)
+    stage_host = _host_staging()
+    ops, recv_bufs = [], []
+    for t in tensors:
+        out = t[send_rows].contiguous()
+        if stage_host and out.is_cuda:
+            out = out.cpu()
+        ops.append(dist.P2POp(dist.isend, out, dst, group))
+    for t in tensors:
+        buf = t[recv_rows]
+        if stage_host and buf.is_cuda:
+            buf = buf.cpu()
+        elif not buf.is_contiguous():
+            buf = buf.contiguous()
+        recv_bufs.append(buf)
+        ops.append(dist.P2POp(dist.irecv, buf, src, group))
+    reqs = dist.batch_isend_irecv(ops)
+
+    def finish():
+        for req in reqs:
+            req.wait()
+        for t, buf in zip(tensors, recv_bufs):
+            view = t[recv_rows]
+            if view.data_ptr() != buf.data_ptr():
+                view.copy_(buf)
+    return finish
+
+
+def run_epoch(plan: RingPlan, rank: int, stage_fn, row_tensors, group=None, parts: int = 1) -> None:
+    """One DSGD epoch: D stages, each followed by the ring shift.
+
+    parts > 1 pipelines the shift: each stage runs as `parts` row sub-blocks
+    (stage_fn(s, rb, part)), and a sub-block is sent as soon as its kernel is enqueued,
+    while the next sub-block trains; a stage's sub-block waits only for its own part to
+    arrive.  Each column still sees its entries of the block in row order and each row
+    its columns in ascending order, so with the exact stage kernel the result is the
+    same as parts = 1 (and parallel_train) bit for bit."""
+    if parts == 1:
+        for s in range(plan.D):
+            stage_fn(s, plan.row_block(rank, s))
+            ring_shift(plan, rank, s, row_tensors, group)
+        return
+    pending = {}
     for s in range(plan.D):
-        stage_fn(s, plan.row_block(rank, s))
-        ring_shift(plan, rank, s, row_tensors, group)
+        rb = plan.row_block(rank, s)
+        for h in range(parts):
+            if h in pending:
+                pending.pop(h)()
+            stage_fn(s, rb, h)
+            if plan.D > 1:
+                pending[h] = _shift_part(plan, rank, s, h, parts, row_tensors, group)
+    for h in sorted(pending):
+        pending.pop(h)()
 
 
 def allgather_blocks(t, bounds: np.ndarray, rank: int, D: int, group=None):
@@ -228,36 +292,41 @@ def bench_main(args, metric, workload, rates):
     del params
     plan = RingPlan(D, M, N)
     d = dm.dev
-    # per-stage plans: entry ranges of (row block, own column block) + own columns longest-first
-    rb_t = nat.to_dev(plan.row_bounds)
-    bp = nat.empty((N * (D + 1),), "int64")
-    nat.call("culsh_block_pointers", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), N, nat.ptr(rb_t), D + 1,
+    # per-(stage, row sub-block) work lists of the own column block: entry ranges from the
+    # block pointers of the D*parts-way row partition, split when the block has fewer
+    # columns than the GPU has resident warps (HogwildTrainer.block_work); the ring shift
+    # of each sub-block overlaps the next sub-block's kernel (run_epoch parts)
+    parts = int(os.environ.get("CULSH_DSGD_PARTS", "2")) if D > 1 else 1
+    nb = D * parts + 1
+    fine = np.array([(k * M) // (D * parts) for k in range(nb)], np.int64)
+    bp = nat.empty((N * nb,), "int64")
+    nat.call("culsh_block_pointers", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), N, nat.ptr(nat.to_dev(fine)), nb,
              nat.ptr(bp), nat.stream_ptr())
-    cbt = nat.to_dev(plan.col_bounds)
-    segs = []
-    for s in range(D):
-        seg = nat.zeros((2 * N,), "int64")
-        chain = nat.zeros((N,), "int32")
-        nat.call("culsh_pass_plan", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), N, 1, 0, N, 0, M,
-                 nat.ptr(bp), nat.ptr(cbt), D, s, nat.ptr(seg), nat.ptr(chain), nat.stream_ptr())
-        segs.append(seg)
+    bp_h = nat.to_host(bp).reshape(N, nb)
     cs = plan.cols(rank)
     counts = (d.col_ptr[1:] - d.col_ptr[:-1])[cs]
     own = (torch.argsort(counts, descending=True, stable=True) + cs.start).to(torch.int32)
     U = tr.model.U.view(M, F)
     b = tr.model.b
-
-    # per-stage work lists: own columns' block ranges, split when the block has fewer
-    # columns than the GPU has resident warps (HogwildTrainer.block_work)
-    works = [tr.block_work(segs[s], own) for s in range(D)]
+    works = {}
+    for s in range(D):
+        rb = plan.row_block(rank, s)
+        for h in range(parts):
+            k = rb * parts + h
+            seg = np.zeros((N, 2), np.int64)
+            seg[cs, 0], seg[cs, 1] = bp_h[cs, k], bp_h[cs, k + 1]
+            works[(s, h)] = tr.block_work(nat.to_dev(seg.reshape(-1)), own)
 
     def stage(ep):
-        def fn(s, rb):
-            tr.launch_work(ep, works[s])
+        def fn(s, rb, h=0):
+            tr.launch_work(ep, works[(s, h)])
         return fn
 
+    def epoch(ep):
+        run_epoch(plan, rank, stage(ep), [U, b], parts=parts)
+
     for w in range(args.warmup):
-        run_epoch(plan, rank, stage(w), [U, b])
+        epoch(w)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -268,7 +337,7 @@ def bench_main(args, metric, workload, rates):
     with clk:
         t0.record()
         for s in range(args.steps):
-            run_epoch(plan, rank, stage(args.warmup + s), [U, b])
+            epoch(args.warmup + s)
         t1.record()
         torch.cuda.synchronize()
     dist.barrier()
@@ -297,7 +366,7 @@ def bench_main(args, metric, workload, rates):
         for k, v in dev_views.items():
             v.copy_(host[k], non_blocking=True)
         tr.loss.zero_()
-        run_epoch(plan, rank, stage(args.warmup + args.steps + s), [U, b])
+        epoch(args.warmup + args.steps + s)
         float(tr.loss.item())
     torch.cuda.synchronize()
     e_dt = _max_over_ranks(time.perf_counter() - w0)
@@ -311,9 +380,10 @@ def bench_main(args, metric, workload, rates):
                 "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
                 "data": "synthetic (random_sparse distribution generated in HBM)",
-                "config": {"workload": workload[args.config], "parallelism": f"dsgd{D}",
-                           "exchange": ("NCCL send/recv ring shift of u/b row blocks per stage" if backend == "nccl" else
-                                        f"{backend} ring shift of u/b row blocks per stage (host-staged)"),
+                "config": {"workload": workload[args.config], "parallelism": f"dsgd{D}", "ring_parts": parts,
+                           "exchange": ("NCCL send/recv ring shift of u/b row sub-blocks, each overlapping the next "
+                                        "sub-block's kernel" if backend == "nccl" else
+                                        f"{backend} ring shift of u/b row sub-blocks (host-staged)"),
                            "l2": "inputs larger than L2, no flush"},
                 "lsh_build_s": lsh_s,
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",

@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, out_q):
+def _worker(rank, world, port, case, out_q, parts=1):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -41,15 +41,19 @@ def _worker(rank, world, port, case, out_q):
     plan = RingPlan(world, d.M, d.N)
     _, col_bounds, bp = orc.partition(d, world)
     assert np.array_equal(col_bounds, plan.col_bounds)
+    bp_fine = orc.partition(d, world * parts)[2]   # row sub-blocks of the pipelined shift
     U, b = torch.from_numpy(m.U), torch.from_numpy(m.b)
     for t in range(epochs):
         rates = orc.make_rates(tuple(a / (1.0 + 0.3 * t ** 1.5)
                                      for a in (0.035, 0.035, 0.035, 0.035, 0.002, 0.002)), REGS)
         cs = plan.cols(rank)
 
-        def stage(s, rb):
-            assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb, bp) == 0
-        run_epoch(plan, rank, stage, [U, b])
+        def stage(s, rb, h=None):
+            if h is None:
+                assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb, bp) == 0
+            else:
+                assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb * parts + h, bp_fine) == 0
+        run_epoch(plan, rank, stage, [U, b], parts=parts)
     # after D stages per epoch every rank holds row block `rank` again
     allgather_blocks(U, plan.row_bounds, rank, world)
     allgather_blocks(b, plan.row_bounds, rank, world)
@@ -61,15 +65,17 @@ def _worker(rank, world, port, case, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,case", [(2, 0), (3, 0), (2, 1), (3, 3)])
-def test_dsgd_ring_equals_reference_parallel_train(world, case):
+@pytest.mark.parametrize("world,case,parts", [(2, 0, 1), (3, 0, 1), (2, 1, 1), (3, 3, 1), (2, 0, 2), (3, 3, 3)])
+def test_dsgd_ring_equals_reference_parallel_train(world, case, parts):
+    """parts > 1: the pipelined ring (row sub-blocks shifted while the next one trains)
+    gives the same bytes as parallel_train(D)."""
     z = load_golden("sgd_small.npz")
     if world not in (2, 3):
         pytest.skip()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, parts)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=120)
@@ -94,3 +100,8 @@ def test_ring_plan_covers_every_block():
             for r in range(D):   # the block rank r trains next is the one its recv peer trained now
                 assert p.row_block(r, s + 1) == p.row_block(p.recv_peer(r), s)
         assert len(seen) == D * D
+        for parts in (1, 2, 3):   # sub-blocks tile each row block
+            for rb in range(D):
+                sl = [p.sub_rows(rb, h, parts) for h in range(parts)]
+                assert sl[0].start == p.rows(rb).start and sl[-1].stop == p.rows(rb).stop
+                assert all(sl[h].stop == sl[h + 1].start for h in range(parts - 1))
