@@ -169,9 +169,9 @@ class HogwildTrainer:
         t = nat.torch()
         if cap is None:
             warps = 32 * t.cuda.get_device_properties(nat.device()).multi_processor_count
-            # a lone warp runs a chain ~3-4x faster than a fully loaded SM does, so a column
-            # up to 2x the mean per-warp work still finishes within the epoch
-            cap = max(1024, 2 * -(-d.nnz // warps))
+            # cap = the mean per-warp work: on the skewed C3-shape data 1x gives 9.7 ms/epoch
+            # against 15.3 ms at 2x, with the same held-out RMSE (tools/skew_cap_sweep.py)
+            cap = max(1024, -(-d.nnz // warps))
         col_ptr = nat.to_host(d.col_ptr).astype(np.int64)
         cnt = np.diff(col_ptr)
         if cnt.max() <= cap:
