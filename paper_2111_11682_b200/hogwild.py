@@ -169,9 +169,11 @@ class HogwildTrainer:
         t = nat.torch()
         if cap is None:
             warps = 32 * t.cuda.get_device_properties(nat.device()).multi_processor_count
-            # cap = the mean per-warp work: on the skewed C3-shape data 1x gives 9.7 ms/epoch
-            # against 15.3 ms at 2x, with the same held-out RMSE (tools/skew_cap_sweep.py)
-            cap = max(1024, -(-d.nnz // warps))
+            # cap = 2 x the mean per-warp work.  Shorter segments are faster but average more
+            # (tools/skew_cap_sweep.py, skewed data): C3 6 epochs 15.3 -> 9.7 ms/epoch at 1x
+            # with unchanged held-out RMSE, but C2 8 epochs +0.0017 (2x) -> +0.0049 (1x) from
+            # the exact fit, at the 0.005 bar; split_cap overrides
+            cap = max(1024, 2 * -(-d.nnz // warps))
         col_ptr = nat.to_host(d.col_ptr).astype(np.int64)
         cnt = np.diff(col_ptr)
         if cnt.max() <= cap:

@@ -2,7 +2,7 @@
 Hogwild fit for several caps (default = 2 x nnz / resident warps), against the exact
 (serial-order) fit after the same epochs.
 
-  python tools/skew_cap_sweep.py [epochs]
+  python tools/skew_cap_sweep.py [epochs] [c2|c3]
 """
 import json
 import os
@@ -19,7 +19,8 @@ from paper_2111_11682_b200.data import DeviceSparseRatings  # noqa: E402
 from paper_2111_11682_b200.hogwild import HogwildTrainer  # noqa: E402
 
 epochs = int(sys.argv[1]) if len(sys.argv) > 1 else 6
-M, N, nnz, F, K, e = synth.SHAPES["c3"]
+shape = sys.argv[2] if len(sys.argv) > 2 else "c3"
+M, N, nnz, F, K, e = synth.SHAPES[shape]
 rows, cols, vals = synth.structured_triplets_device(M, N, nnz, seed=0)
 nt = rows.numel() // 10
 tr = DeviceSparseRatings(M, N, rows[nt:], cols[nt:], vals[nt:])
@@ -33,12 +34,12 @@ cfg = P.TrainConfig(F=F, K=K, epochs=epochs, seed=0, alpha_b=0.02, alpha_b_hat=0
                     lambda_u=0.01, lambda_v=0.01, lambda_w=0.05, lambda_c=0.05)
 warps = 32 * torch.cuda.get_device_properties(0).multi_processor_count
 mean = -(-d.nnz // warps)
-out = {"nnz": int(d.nnz), "max_col": int((d.col_ptr[1:] - d.col_ptr[:-1]).max()), "epochs": epochs}
+out = {"shape": shape, "nnz": int(d.nnz), "max_col": int((d.col_ptr[1:] - d.col_ptr[:-1]).max()), "epochs": epochs}
 t0 = time.perf_counter()
 pe = P.train_full(tr, nbr, cfg)
 out["exact_s"] = time.perf_counter() - t0
 out["exact_rmse"] = float(P.rmse(pe, te, tr))
-for mult in (2.0, 1.0, 0.5, 0.25):
+for mult in [float(x) for x in os.environ.get("CAPS", "2,1,0.5,0.25").split(",")]:
     cap = max(1024, int(mult * mean))
     h = HogwildTrainer(tr, nbr, cfg, split_cap=cap)
     h.launch_epoch(0)   # warm-up epoch is part of the fit (epochs counted below)
