@@ -360,8 +360,11 @@ constexpr int kHsRing = 4;        // 16-row groups in flight per CTA (64 row rec
 // the next groups into a shared-memory ring with the bulk-copy engine
 // (cp.async.bulk + mbarrier transaction counts); every thread then reads its own
 // 32-bit word of each record from shared memory and runs the CSA tree.
+// (128, 7): 72 registers instead of 96 (a few bytes of spill) so 7 CTAs fit per SM instead
+// of 6 — the kernel is gather-latency-bound — with the shared-memory carveout at its maximum:
+// 7.84 -> 7.13 ms at C3 (A/B, tools/gpu_ab_lsh.sh)
 template <bool kTma>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 7)
 hash_count_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows_by_class,
                   const int32_t *__restrict__ class_off, int NC, const int *__restrict__ class_psi,
                   int64_t col_begin, const uint8_t *__restrict__ table, int stride, int W4, int qp, int p,
@@ -610,6 +613,7 @@ extern "C" int culsh_hash_count(const int64_t *col_ptr, const int32_t *rows_by_c
     if (!attr) {
         cudaFuncSetAttribute(hash_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(hash_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(hash_count_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
     const bool use_tma = variant == 0;
