@@ -212,56 +212,72 @@ constexpr int kHsMaxClasses = 16;
 constexpr int kHsChunk = 1024;   // multiple of 16
 
 // Per column: entries grouped by value class (order inside a class is irrelevant to
-// integer counts).  One warp per column, two passes over the column.
+// integer counts).  One warp per column, two passes over the column; per-class counts
+// and running offsets live in lanes 0..NC-1 (ballots + shuffles, no shared atomics).
 __global__ void class_partition_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ col_rows,
                                        const double *__restrict__ col_vals, int64_t N,
                                        const double *__restrict__ class_vals, int NC,
                                        int32_t *__restrict__ rows_by_class, int32_t *__restrict__ class_off) {
-    __shared__ int s_cnt[8][kHsMaxClasses];
     const int w = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     const int64_t j = blockIdx.x * 8LL + w;
     if (j >= N) return;
     const int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
-    if (lane < kHsMaxClasses) s_cnt[w][lane] = 0;
-    __syncwarp();
-    for (int64_t x = lo + lane; x < hi; x += 32) {
-        const double v = col_vals[x];
-        int c = 0;
-        while (c < NC - 1 && class_vals[c] != v) ++c;
-        atomicAdd(&s_cnt[w][c], 1);
-    }
-    __syncwarp();
-    if (lane == 0) {
-        int run = 0;
-        for (int c = 0; c < NC; ++c) {
-            const int n = s_cnt[w][c];
-            class_off[j * (NC + 1) + c] = run;
-            s_cnt[w][c] = run;
-            run += n;
+    const unsigned lt = (1u << lane) - 1u;
+    int cnt = 0;   // lane c: entries of class c
+    constexpr int U = 4;   // 4 x 32 entries per step: their loads are in flight together
+    for (int64_t b0 = lo; b0 < hi; b0 += 32 * U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t x = b0 + 32 * u + lane;
+            v[u] = x < hi ? col_vals[x] : 0.0;
         }
-        class_off[j * (NC + 1) + NC] = run;
-    }
-    __syncwarp();
-    // stable within each class (rows stay ascending): per 32-entry step, lanes of
-    // class c take consecutive slots in lane order
-    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
-        const int64_t x = b0 + lane;
-        const bool have = x < hi;
-        int c = -1;
-        if (have) {
-            const double v = col_vals[x];
-            c = 0;
-            while (c < NC - 1 && class_vals[c] != v) ++c;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int c = -1;
+            if (b0 + 32 * u + lane < hi) {
+                c = 0;
+                while (c < NC - 1 && __ldg(class_vals + c) != v[u]) ++c;
+            }
+            for (int cc = 0; cc < NC; ++cc) {
+                const unsigned bal = __ballot_sync(0xffffffffu, c == cc);
+                if ((int)lane == cc) cnt += __popc(bal);
+            }
         }
-        for (int cc = 0; cc < NC; ++cc) {
-            const unsigned bal = __ballot_sync(0xffffffffu, c == cc);
-            if (!bal) continue;
-            const int base = s_cnt[w][cc];
-            if (c == cc) rows_by_class[lo + base + __popc(bal & ((1u << lane) - 1u))] = col_rows[x];
-            __syncwarp();
-            if (lane == 0) s_cnt[w][cc] = base + __popc(bal);
-            __syncwarp();
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += y;
+    }
+    int run = incl - cnt;   // lane c: next slot of class c (rows stay ascending within a class)
+    if ((int)lane < NC) class_off[j * (NC + 1) + lane] = run;
+    if ((int)lane == NC - 1) class_off[j * (NC + 1) + NC] = incl;
+    for (int64_t b0 = lo; b0 < hi; b0 += 32 * U) {
+        double v[U];
+        int32_t rw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t x = b0 + 32 * u + lane;
+            v[u] = x < hi ? col_vals[x] : 0.0;
+            rw[u] = x < hi ? col_rows[x] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int c = -1;
+            if (b0 + 32 * u + lane < hi) {
+                c = 0;
+                while (c < NC - 1 && __ldg(class_vals + c) != v[u]) ++c;
+            }
+            for (int cc = 0; cc < NC; ++cc) {
+                const unsigned bal = __ballot_sync(0xffffffffu, c == cc);
+                if (!bal) continue;
+                const int base = __shfl_sync(0xffffffffu, run, cc);
+                if (c == cc) rows_by_class[lo + base + __popc(bal & lt)] = rw[u];
+                if ((int)lane == cc) run += __popc(bal);
+            }
         }
     }
 }

@@ -1,3 +1,7 @@
+"""Per-entry-point GPU time of one C3 simLSH top-K build (CUDA events around every C call).
+
+  python tools/lsh_breakdown.py
+"""
 import sys, json, collections
 sys.path.insert(0, ".")
 import torch
@@ -15,6 +19,9 @@ def timed_call(name, *a):
     s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(); r = orig(name, *a); t.record(); evs.append((name, s, t)); return r
 nat.call = timed_call
+for attr in ("_value_classes", "_class_part"):   # time the data-dependent prep too (as bench.py)
+    if hasattr(dm.dev, attr):
+        delattr(dm.dev, attr)
 import time
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize(); t0 = time.perf_counter(); a.record()
