@@ -295,7 +295,12 @@ __global__ void value_set_kernel(const double *__restrict__ vals, int64_t n, dou
     if (threadIdx.x < kHsMaxClasses) s_set[threadIdx.x] = EMPTY;
     if (threadIdx.x == 0) s_over = 0;
     __syncthreads();
+    // each thread first collects its own distinct values in registers (compares only, no
+    // shared-memory round trips per element), then merges them into the block set once
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long own[kHsMaxClasses];
+    int n_own = 0;
+    bool over = false;
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += 4 * step) {
         unsigned long long v4[4];
 #pragma unroll
@@ -306,18 +311,36 @@ __global__ void value_set_kernel(const double *__restrict__ vals, int64_t n, dou
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const unsigned long long v = v4[u];
-            if (v == EMPTY) continue;
-            bool found = false;
-            for (int k = 0; k < kHsMaxClasses && !found; ++k)
-                found = ((volatile unsigned long long *)s_set)[k] == v;
-            if (found) continue;
-            int k = 0;
-            for (; k < kHsMaxClasses; ++k) {
-                const unsigned long long old = atomicCAS(&s_set[k], EMPTY, v);
-                if (old == EMPTY || old == v) break;
+            bool found = v == EMPTY;
+#pragma unroll
+            for (int k = 0; k < kHsMaxClasses; ++k) found |= (k < n_own) && own[k] == v;
+            if (!found) {
+                if (n_own == kHsMaxClasses) {
+                    over = true;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kHsMaxClasses; ++k)
+                        if (k == n_own) own[k] = v;
+                    ++n_own;
+                }
             }
-            if (k == kHsMaxClasses) s_over = 1;
         }
+    }
+    if (over) s_over = 1;
+#pragma unroll
+    for (int q = 0; q < kHsMaxClasses; ++q) {
+        if (q >= n_own) break;
+        const unsigned long long v = own[q];
+        bool found = false;
+        for (int k = 0; k < kHsMaxClasses && !found; ++k)
+            found = ((volatile unsigned long long *)s_set)[k] == v;
+        if (found) continue;
+        int k = 0;
+        for (; k < kHsMaxClasses; ++k) {
+            const unsigned long long old = atomicCAS(&s_set[k], EMPTY, v);
+            if (old == EMPTY || old == v) break;
+        }
+        if (k == kHsMaxClasses) s_over = 1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
