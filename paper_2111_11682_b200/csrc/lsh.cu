@@ -218,12 +218,22 @@ __global__ void class_partition_kernel(const int64_t *__restrict__ col_ptr, cons
                                        const double *__restrict__ col_vals, int64_t N,
                                        const double *__restrict__ class_vals, int NC,
                                        int32_t *__restrict__ rows_by_class, int32_t *__restrict__ class_off) {
+    __shared__ double s_cv[kHsMaxClasses];
+    if (threadIdx.x < NC) s_cv[threadIdx.x] = class_vals[threadIdx.x];
+    __syncthreads();
     const int w = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     const int64_t j = blockIdx.x * 8LL + w;
     if (j >= N) return;
     const int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
     const unsigned lt = (1u << lane) - 1u;
+    // class of a value: its first match among class_vals[0..NC-2], else NC-1 (a uniform
+    // NC-1-step loop over a shared copy: no divergent search, no global loads)
+    auto cls = [&](double v) {
+        int c = NC - 1;
+        for (int k = NC - 2; k >= 0; --k) c = s_cv[k] == v ? k : c;
+        return c;
+    };
     int cnt = 0;   // lane c: entries of class c
     constexpr int U = 4;   // 4 x 32 entries per step: their loads are in flight together
     for (int64_t b0 = lo; b0 < hi; b0 += 32 * U) {
@@ -235,11 +245,7 @@ __global__ void class_partition_kernel(const int64_t *__restrict__ col_ptr, cons
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            int c = -1;
-            if (b0 + 32 * u + lane < hi) {
-                c = 0;
-                while (c < NC - 1 && __ldg(class_vals + c) != v[u]) ++c;
-            }
+            const int c = b0 + 32 * u + lane < hi ? cls(v[u]) : -1;
             for (int cc = 0; cc < NC; ++cc) {
                 const unsigned bal = __ballot_sync(0xffffffffu, c == cc);
                 if ((int)lane == cc) cnt += __popc(bal);
@@ -266,11 +272,7 @@ __global__ void class_partition_kernel(const int64_t *__restrict__ col_ptr, cons
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            int c = -1;
-            if (b0 + 32 * u + lane < hi) {
-                c = 0;
-                while (c < NC - 1 && __ldg(class_vals + c) != v[u]) ++c;
-            }
+            const int c = b0 + 32 * u + lane < hi ? cls(v[u]) : -1;
             for (int cc = 0; cc < NC; ++cc) {
                 const unsigned bal = __ballot_sync(0xffffffffu, c == cc);
                 if (!bal) continue;
