@@ -1,5 +1,6 @@
 # round-end evidence: full GPU suite, smoke, default bench (+CPU baseline), reference arm,
-# C4 online bench, launch list, one ncu --set full capture of the epoch kernel
+# C4 online bench, launch list, one ncu --set full capture of the epoch kernel, C5 bench,
+# DSGD per-GPU stage times, and the N = 2 bench path with ranks sharing the GPU over gloo
 python -m pytest tests -m gpu -q --durations=10 > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 python bench.py > gpurun_out/bench_c3.log 2>&1; echo bench=$?
