@@ -158,21 +158,25 @@ struct HwCoef {
 };
 
 constexpr int kHwWarps = 8;      // warps per CTA
-constexpr int kHwDepth = 4;      // u_i prefetch depth (updates in flight per warp; 4 beat 8: C3 -1 %, C5 -8 %)
+// u_i prefetch depth (ring slots per warp): 4 for K <= 32, 2 for K > 32 (A/B: C3 11.8 ms at 4
+// vs 12.4 at 2 and 12.0 at 8; C5 (K = 64) 35.1 ms at 2 vs 37.2 at 4 and 40.5 at 8 -- the
+// smaller ring leaves more of the SM's shared/L1 split to L1)
+template <int KPL>
+constexpr int hw_depth() { return KPL == 2 ? 2 : 4; }
 
 template <int FV, int KPL>
 constexpr int hw_smem_per_warp() {
     // metadata window, mask word 1, u-row ring, b_i and deferred b updates of the window,
     // start values of a work segment
-    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + kHwDepth * 32 * FV * 4 + 2 * 64 * 4 + 32 * (FV + 2 * KPL + 1) * 4;
+    return 64 * 16 + (KPL == 2 ? 64 * 4 : 0) + hw_depth<KPL>() * 32 * FV * 4 + 2 * 64 * 4 + 32 * (FV + 2 * KPL + 1) * 4;
 }
 
 // FV floats per lane; F == 32*FV (vector path) or F < 32 with FV == 1 (masked).
 //
 // Per warp, shared memory holds (a) the column's next 64 entries' metadata
 // {row, value, mask, residual offset} refilled 32 at a time, read with one
-// broadcast LDS.128 per update (+ b_i of each entry), and (b) a ring of kHwDepth u-rows that
-// cp.async fills kHwDepth-1 updates ahead, so the HBM/L2 latency of the row
+// broadcast LDS.128 per update (+ b_i of each entry), and (b) a ring of hw_depth u-rows that
+// cp.async fills hw_depth-1 updates ahead, so the HBM/L2 latency of the row
 // gather is off the update's critical path.  Each lane copies and later reads
 // only its own FV floats of every row, so the ring needs no warp barrier.
 //
@@ -198,7 +202,7 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
                int *__restrict__ status, const float *__restrict__ lut, const int64_t *__restrict__ mptr,
                const int32_t *__restrict__ first_row) {
     extern __shared__ __align__(16) unsigned char s_raw[];
-    constexpr int P = kHwDepth;
+    constexpr int P = hw_depth<KPL>();
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;
     unsigned char *wbase = s_raw + (size_t)warp * hw_smem_per_warp<FV, KPL>();
