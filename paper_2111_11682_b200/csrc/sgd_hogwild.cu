@@ -577,11 +577,17 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
             if (FV <= 4 && cnt == 32) {
                 // whole chunk: P-update groups with compile-time ring slots (base % 32 == 0);
                 // FV == 8 keeps the rolled loop (register budget of 4 CTAs per SM)
-                static_assert(32 % P == 0, "ring depth must divide the chunk");
-                for (int k = 0; k < 32; k += P) {
-                    const int g0 = (base + k) & 63, g1 = (base + k + P) & 63;
+                // updates per unrolled group (a multiple of P): P for K <= 32; 8 for K > 32
+                // (2-deep ring), where it measured 34.6 -> 33.6 ms at C5 (and 4 -> 8 at C3: slower)
+                constexpr int GS = KPL == 2 ? 8 : P;
+                static_assert(32 % GS == 0 && GS % P == 0, "group must divide the chunk, ring the group");
+                for (int k = 0; k < 32; k += GS) {
+                    const int g0 = (base + k) & 63, g1 = (base + k + GS) & 63;
 #pragma unroll
-                    for (int s = 0; s < P; ++s) step(g0 + s, s == 0 ? g0 + P - 1 : g1 + s - 1, s, (s + P - 1) % P);
+                    for (int s = 0; s < GS; ++s) {
+                        const int t = s + P - 1;   // prefetch offset inside / past the group
+                        step(g0 + s, t < GS ? g0 + t : g1 + (t - GS), s % P, t % P);
+                    }
                 }
             } else {
                 for (int k = 0; k < cnt; ++k) {
