@@ -57,8 +57,17 @@ class BaselineStats:
     b_hat: np.ndarray
 
 
+_HOST_VIEWS = ("entry_rows", "entry_cols", "entry_values", "row_ptr", "row_cols", "row_vals",
+               "col_ptr", "col_rows", "col_vals")
+
+
 class SparseRatings:
-    """Dual-indexed sparse matrix, immutable after construction (data.py:166-207)."""
+    """Dual-indexed sparse matrix, immutable after construction (data.py:166-207).
+
+    Built from host triplets (the reference's constructor: two lexsorts), or -- by
+    ``extend_ratings`` and other device producers -- directly in HBM
+    (``_from_device``); the host views of a device-built matrix (entry arrays, CSR,
+    CSC) are downloaded on first access, read-only like the reference's."""
 
     def __init__(self, M: int, N: int, rows: np.ndarray, cols: np.ndarray, values: np.ndarray,
                  row_ids: list | None = None, col_ids: list | None = None):
@@ -72,6 +81,7 @@ class SparseRatings:
         nnz = len(self.entry_rows)
         if len(self.entry_cols) != nnz or len(self.entry_values) != nnz:
             raise ValueError("triplet arrays must have equal length")
+        self._nnz = nnz
         order = np.lexsort((self.entry_cols, self.entry_rows))
         self.row_ptr = np.zeros(self.M + 1, dtype=np.int64)
         np.cumsum(np.bincount(self.entry_rows, minlength=self.M), out=self.row_ptr[1:])
@@ -84,17 +94,56 @@ class SparseRatings:
         self.col_vals = self.entry_values[order]
         self._baselines = None
         self._dev = None
+        self._dev_entries = None
         for arr in (self.entry_rows, self.entry_cols, self.entry_values, self.row_ptr,
                     self.row_cols, self.row_vals, self.col_ptr, self.col_rows, self.col_vals):
             arr.flags.writeable = False
 
+    @classmethod
+    def _from_device(cls, dev: "DeviceRatings", entries, row_ids=None, col_ids=None,
+                     baselines: "BaselineStats | None" = None) -> "SparseRatings":
+        """A matrix whose index views already live in HBM (``dev``) together with its
+        entry-order triplets ``entries`` = (rows i32, cols i32, values f64) tensors."""
+        self = cls.__new__(cls)
+        self.M, self.N, self._nnz = dev.M, dev.N, dev.nnz
+        self.row_ids, self.col_ids = row_ids, col_ids
+        self._dev = dev
+        self._dev_entries = entries
+        self._baselines = baselines
+        return self
+
+    def __getattr__(self, name):
+        # host views of a device-built matrix, materialised on first access
+        if name in _HOST_VIEWS and self.__dict__.get("_dev") is not None:
+            d, (er, ec, ev) = self._dev, self._dev_entries
+            n = self._nnz
+            src = {"entry_rows": (er, n), "entry_cols": (ec, n), "entry_values": (ev, n),
+                   "row_ptr": (d.row_ptr, self.M + 1), "row_cols": (d.row_cols, n),
+                   "row_vals": (d.row_vals, n), "col_ptr": (d.col_ptr, self.N + 1),
+                   "col_rows": (d.col_rows, n), "col_vals": (d.col_vals, n)}[name]
+            a = np.ascontiguousarray(nat.to_host(src[0])[:src[1]])
+            a.flags.writeable = False
+            self.__dict__[name] = a
+            return a
+        raise AttributeError(name)
+
     @property
     def nnz(self) -> int:
-        return len(self.entry_rows)
+        return self._nnz
 
     def triplets(self) -> Triplets:
-        return Triplets(self.entry_rows, self.entry_cols, self.entry_values, self.row_ids,
-                        self.col_ids)
+        t = Triplets(self.entry_rows, self.entry_cols, self.entry_values, self.row_ids,
+                     self.col_ids)
+        t._source = self        # rmse() evaluates the training set on its device copy
+        return t
+
+    def device_entries(self):
+        """The entry-order triplets (rows i32, cols i32, values f64) in HBM (cached;
+        the matrix is immutable)."""
+        if self._dev_entries is None:
+            self._dev_entries = (nat.to_dev(self.entry_rows, np.int32), nat.to_dev(self.entry_cols, np.int32),
+                                 nat.to_dev(self.entry_values, np.float64))
+        return self._dev_entries
 
     def row_slice(self, i: int):
         lo, hi = self.row_ptr[i], self.row_ptr[i + 1]
@@ -292,6 +341,17 @@ class DeviceRatings:
         return nat.CulshData(self.M, self.N, self.nnz, p(self.col_ptr), p(self.col_rows),
                              p(self.col_vals), p(self.row_ptr), p(self.row_cols), p(self.row_vals),
                              p(self.csc2csr), p(self.base_b), p(self.base_bhat))
+
+    def integer_valued(self) -> bool:
+        """Whether every rating is an integer (then every baseline sum is exact and
+        device-side statistics equal the reference's bit for bit).  Cached."""
+        v = self.__dict__.get("_integer_valued")
+        if v is None:
+            t = nat.torch()
+            vals = self.col_vals[:self.nnz]
+            v = bool(t.all(vals == t.round(vals)).item()) if self.nnz else True
+            self._integer_valued = v
+        return v
 
     def set_baselines(self, mu: float, b: np.ndarray, b_hat: np.ndarray) -> None:
         self.mu = float(mu)

@@ -98,34 +98,130 @@ def _rates_struct(rates, regs) -> nat.CulshRates:
     return nat.CulshRates(*[float(x) for x in tuple(rates) + tuple(regs)])
 
 
-@dataclass
-class ModelParams:
-    """All trainable state plus the neighbour table (factorization.py:105-185)."""
+_FIELDS = ("b", "b_hat", "U", "V", "W", "C")
 
-    mu: float
-    b: np.ndarray
-    b_hat: np.ndarray
-    U: np.ndarray
-    V: np.ndarray
-    W: np.ndarray
-    C: np.ndarray
-    neighbors: NeighborTable | None = None
+
+class ModelParams:
+    """All trainable state plus the neighbour table (factorization.py:105-185).
+
+    Same fields as the reference dataclass (mu, b, b_hat, U, V, W, C, neighbors), with
+    one addition: the arrays may live in HBM.  A model produced by training (or by
+    ``extend_params``) is backed by its device copy and each host array is materialised
+    only when it is first read, so an epoch callback that only calls ``rmse``/``predict``
+    never moves the model across PCIe.  Per array the newest copy is tracked:
+
+    * ``D`` -- the device copy is newer (host array absent or stale);
+    * ``S`` -- both copies are equal and the host array was only read internally;
+    * ``H`` -- the host array is the truth: it was passed in, assigned, or handed out by an
+      attribute read (the caller may edit it in place, as with the reference's live
+      arrays), so every device use uploads it first.
+    """
+
+    def __init__(self, mu: float, b: np.ndarray, b_hat: np.ndarray, U: np.ndarray,
+                 V: np.ndarray, W: np.ndarray, C: np.ndarray,
+                 neighbors: NeighborTable | None = None):
+        self.mu = mu
+        self.neighbors = neighbors
+        self._h = {"b": b, "b_hat": b_hat, "U": U, "V": V, "W": W, "C": C}
+        self._state = dict.fromkeys(_FIELDS, "H")
+        self._dims = (len(b), len(b_hat), int(np.shape(U)[1]), int(np.shape(W)[1]))
+        self._dev = None
+
+    @classmethod
+    def _from_device(cls, mu: float, dev, M: int, N: int, neighbors: NeighborTable | None):
+        """A model whose only copy is the device model ``dev`` (DeviceModel64/32)."""
+        self = cls.__new__(cls)
+        self.mu = float(mu)
+        self.neighbors = neighbors
+        self._h = dict.fromkeys(_FIELDS)
+        self._state = dict.fromkeys(_FIELDS, "D")
+        self._dims = (int(M), int(N), int(dev.F), int(dev.K))
+        self._dev = dev
+        return self
+
+    # -- host views ----------------------------------------------------------
+    def _peek(self, name: str) -> np.ndarray:
+        """Current host value of one array for an internal read-only use."""
+        if self._state[name] == "D":
+            self._h[name] = self._dev.download(name, self._h[name])
+            self._state[name] = "S"
+        return self._h[name]
+
+    def _get(self, name: str) -> np.ndarray:
+        a = self._peek(name)
+        self._state[name] = "H"
+        return a
+
+    def _set(self, name: str, value) -> None:
+        self._h[name] = value
+        self._state[name] = "H"
+        if name in ("b", "b_hat", "U", "W"):
+            M, N, F, K = self._dims
+            sh = np.shape(value)
+            self._dims = {"b": (sh[0], N, F, K), "b_hat": (M, sh[0], F, K),
+                          "U": (M, N, sh[1], K), "W": (M, N, F, sh[1])}[name]
+
+    b = property(lambda s: s._get("b"), lambda s, v: s._set("b", v))
+    b_hat = property(lambda s: s._get("b_hat"), lambda s, v: s._set("b_hat", v))
+    U = property(lambda s: s._get("U"), lambda s, v: s._set("U", v))
+    V = property(lambda s: s._get("V"), lambda s, v: s._set("V", v))
+    W = property(lambda s: s._get("W"), lambda s, v: s._set("W", v))
+    C = property(lambda s: s._get("C"), lambda s, v: s._set("C", v))
+
+    # -- device copy ---------------------------------------------------------
+    def _device(self, precision: int = 64):
+        """The device model with every array current (host-truth arrays uploaded first).
+
+        precision=0 returns the backing as it is (DeviceModel64, or the fp32 DeviceModel32
+        of a Hogwild fit); precision=64 always returns a DeviceModel64 -- for an fp32
+        backing a widened temporary copy (the backing itself stays the trainer's)."""
+        if self._dev is None:
+            self._dev = DeviceModel64(self)
+        else:
+            for n in _FIELDS:
+                if self._state[n] == "H":
+                    self._dev.upload(n, self._h[n])
+        dev = self._dev
+        nbr = self.nbr_entries_device()
+        if dev.nbr is not nbr:
+            dev.nbr = nbr
+            dev._restruct()
+        if precision == 64 and not isinstance(dev, DeviceModel64):
+            return dev.widen()
+        return dev
+
+    def _own(self) -> None:
+        """Mark host arrays created internally (never seen by a caller) as synced, so
+        they are not re-uploaded on every device use."""
+        for n in _FIELDS:
+            if self._state[n] == "H":
+                self._state[n] = "S"
+
+    def _device_updated(self) -> None:
+        """Kernels changed the device copy: it is now the newest for every array."""
+        for n in _FIELDS:
+            self._state[n] = "D"
+
+    def nbr_entries_device(self):
+        if self.neighbors is None or self.K == 0:
+            return nat.zeros((1,), "int32")
+        return self.neighbors.device_entries()
 
     @property
     def M(self) -> int:
-        return len(self.b)
+        return self._dims[0]
 
     @property
     def N(self) -> int:
-        return len(self.b_hat)
+        return self._dims[1]
 
     @property
     def F(self) -> int:
-        return self.U.shape[1]
+        return self._dims[2]
 
     @property
     def K(self) -> int:
-        return self.W.shape[1]
+        return self._dims[3]
 
     def nbr_entries(self) -> np.ndarray:
         if self.neighbors is None:
@@ -136,22 +232,22 @@ class ModelParams:
         nbr = None
         if self.neighbors is not None:
             nbr = NeighborTable(self.neighbors.N, self.neighbors.K, self.neighbors.entries.copy())
-        return ModelParams(self.mu, self.b.copy(), self.b_hat.copy(), self.U.copy(),
-                           self.V.copy(), self.W.copy(), self.C.copy(), nbr)
+        return ModelParams(self.mu, *[self._peek(n).copy() for n in _FIELDS], nbr)
 
     def all_finite(self) -> bool:
-        return bool(np.isfinite(self.mu)
-                    and np.isfinite(self.b).all() and np.isfinite(self.b_hat).all()
-                    and np.isfinite(self.U).all() and np.isfinite(self.V).all()
-                    and np.isfinite(self.W).all() and np.isfinite(self.C).all())
+        if not np.isfinite(self.mu):
+            return False
+        if self._dev is not None and all(s != "H" for s in self._state.values()):
+            return self._dev.all_finite(self.M, self.N)
+        return all(bool(np.isfinite(self._peek(n)).all()) for n in _FIELDS)
 
     def save(self, path) -> None:
         with open(path, "wb") as fh:
             fh.write(f"{MODEL_MAGIC} {MODEL_VERSION} {self.M} {self.N} "
                      f"{self.F} {self.K}\n".encode())
             fh.write(struct.pack("<d", self.mu))
-            for arr in (self.b, self.b_hat, self.U, self.V, self.W, self.C):
-                fh.write(np.ascontiguousarray(arr, dtype="<f8").tobytes())
+            for n in _FIELDS:
+                fh.write(np.ascontiguousarray(self._peek(n), dtype="<f8").tobytes())
             fh.write(np.ascontiguousarray(self.nbr_entries(), dtype="<u4").tobytes())
 
     @classmethod
@@ -201,35 +297,66 @@ def init_params(M: int, N: int, F: int, K: int, neighbors: NeighborTable | None,
 
 # ------------------------------------------------------------ device model ---
 
+_DEV_NAME = {"b": "b", "b_hat": "bhat", "U": "U", "V": "V", "W": "W", "C": "C"}
+
+
 class DeviceModel64:
     """fp64 ModelParams resident in HBM, exposed to the C ABI as CulshModel64."""
 
-    def __init__(self, p: ModelParams):
-        self.mu = float(p.mu)
-        self.F, self.K = p.F, p.K
-        self.b = nat.to_dev(p.b, np.float64)
-        self.bhat = nat.to_dev(p.b_hat, np.float64)
-        self.U = nat.to_dev(p.U.reshape(-1) if p.U.size else np.zeros(1), np.float64)
-        self.V = nat.to_dev(p.V.reshape(-1) if p.V.size else np.zeros(1), np.float64)
-        self.W = nat.to_dev(p.W.reshape(-1) if p.W.size else np.zeros(1), np.float64)
-        self.C = nat.to_dev(p.C.reshape(-1) if p.C.size else np.zeros(1), np.float64)
-        ent = p.nbr_entries()
-        self.nbr = nat.to_dev(ent.reshape(-1) if ent.size else np.zeros(1, np.int32), np.int32)
+    def __init__(self, p: ModelParams | None = None, *, arrays: dict | None = None,
+                 mu: float = 0.0, M: int = 0, N: int = 0, F: int = 0, K: int = 0, nbr=None):
+        if p is not None:
+            mu, M, N, F, K = float(p.mu), p.M, p.N, p.F, p.K
+            arrays = {}
+            for n in _FIELDS:
+                a = p._peek(n)
+                arrays[n] = nat.to_dev(a.reshape(-1) if a.size else np.zeros(1), np.float64)
+            nbr = p.nbr_entries_device()
+        self.mu = float(mu)
+        self.M, self.N, self.F, self.K = M, N, F, K
+        for n, a in arrays.items():
+            setattr(self, _DEV_NAME[n], a)
+        self.nbr = nbr if nbr is not None else nat.zeros((1,), "int32")
+        self._restruct()
+
+    def _restruct(self) -> None:
         self.struct = nat.CulshModel64(self.mu, nat.ptr(self.b), nat.ptr(self.bhat), nat.ptr(self.U),
                                        nat.ptr(self.V), nat.ptr(self.W), nat.ptr(self.C),
                                        nat.ptr(self.nbr), self.F, self.K)
 
-    def download(self, p: ModelParams) -> None:
-        """Copy the device state back into p's numpy arrays (in place)."""
-        p.b[...] = nat.to_host(self.b)[:p.M]
-        p.b_hat[...] = nat.to_host(self.bhat)[:p.N]
-        if p.U.size:
-            p.U[...] = nat.to_host(self.U).reshape(p.U.shape)
-        if p.V.size:
-            p.V[...] = nat.to_host(self.V).reshape(p.V.shape)
-        if p.W.size:
-            p.W[...] = nat.to_host(self.W).reshape(p.W.shape)
-            p.C[...] = nat.to_host(self.C).reshape(p.C.shape)
+    def _shape(self, name: str, M: int, N: int):
+        return {"b": (M,), "b_hat": (N,), "U": (M, self.F), "V": (N, self.F),
+                "W": (N, self.K), "C": (N, self.K)}[name]
+
+    def download(self, name, out=None):
+        """Host fp64 copy of one array (``name`` a ModelParams field); with the legacy
+        form ``download(params)`` every array is copied into params (in place)."""
+        if isinstance(name, ModelParams):
+            p = name
+            for n in _FIELDS:
+                p._h[n] = self.download(n, p._h[n])
+                p._state[n] = "H"
+            return None
+        d = getattr(self, _DEV_NAME[name])
+        shape = self._shape(name, self.M, self.N)
+        n = int(np.prod(shape))
+        host = nat.to_host(d)[:n].reshape(shape) if n else np.zeros(shape)
+        if out is not None and out.shape == shape and out.dtype == np.float64 and out.flags.writeable:
+            out[...] = host
+            return out
+        return np.array(host, dtype=np.float64)
+
+    def upload(self, name: str, host: np.ndarray) -> None:
+        d = getattr(self, _DEV_NAME[name])
+        a = np.ascontiguousarray(host, dtype=np.float64).reshape(-1)
+        if a.size:
+            d[:a.size].copy_(nat.torch().from_numpy(a))
+
+    def all_finite(self, M: int, N: int) -> bool:
+        t = nat.torch()
+        F, K = self.F, self.K
+        parts = [self.b[:M], self.bhat[:N], self.U[:M * F], self.V[:N * F], self.W[:N * K], self.C[:N * K]]
+        return all(bool(t.isfinite(x).all().item()) for x in parts if x.numel())
 
 
 class _Scratch:
@@ -323,7 +450,7 @@ def split_neighbors(i: int, j: int, neighbors: NeighborTable,
 
 def _predict_pairs(params: ModelParams, ratings: SparseRatings, rows, cols) -> np.ndarray:
     dev = ratings.device()
-    dm = DeviceModel64(params)
+    dm = params._device(64)
     rows = nat.to_dev(np.asarray(rows, np.int32).reshape(-1))
     cols = nat.to_dev(np.asarray(cols, np.int32).reshape(-1))
     n = rows.numel()
@@ -354,7 +481,9 @@ def sgd_update(i: int, j: int, params: ModelParams, rates: tuple, regs: tuple,
     _check_model_dims(params.F, params.K)
     e = r - float(_predict_pairs(params, ratings, [i], [j])[0])
     dev = ratings.device()
-    dm = DeviceModel64(params)
+    dm = params._device(0)
+    if not isinstance(dm, DeviceModel64):   # an fp32 (Hogwild) backing: update in fp64
+        params._dev = dm = params._device(64)
     sc = _Scratch(ratings.M, ratings.N)
     lo = int(ratings.col_ptr[j])
     idx = lo + int(np.searchsorted(ratings.col_slice(j)[0], i))
@@ -365,7 +494,7 @@ def sgd_update(i: int, j: int, params: ModelParams, rates: tuple, regs: tuple,
     chain[j] = j                      # the pass holds this one sample: no row predecessor
     sc.chain = nat.to_dev(chain)
     _colpass(dev, dm, sc, _rates_struct(rates, regs), j, j + 1, 1)
-    dm.download(params)
+    params._device_updated()
     if not np.isfinite(e) or sc.status_value():
         raise TrainingDivergedError(epoch=0)
     return float(e)
@@ -478,7 +607,13 @@ def train_full(ratings: SparseRatings, neighbors: NeighborTable | None,
                config: TrainConfig, epoch_callback=None, mode: str = "exact") -> ModelParams:
     """Full neighbourhood model, column-major SGD over all six parameter classes
     (factorization.py:530-556).  mode="exact" is bit-identical to the reference;
-    mode="hogwild" is the fp32 performance mode (see hogwild.py)."""
+    mode="hogwild" is the fp32 performance mode (see hogwild.py).
+
+    The model stays in HBM for the whole fit: ``epoch_callback(t, params)`` receives the
+    live ModelParams backed by the device copy, so ``rmse``/``predict`` inside it run on
+    the resident model, host arrays are copied down only if the callback reads them,
+    and edits it makes to them are uploaded before the next epoch (the reference passes
+    its live arrays)."""
     config.validate()
     K = neighbors.K if neighbors is not None else 0
     if K != config.K:
@@ -486,11 +621,14 @@ def train_full(ratings: SparseRatings, neighbors: NeighborTable | None,
     if mode == "hogwild":
         from .hogwild import HogwildTrainer
         tr = HogwildTrainer(ratings, neighbors, config)
+        params = ModelParams._from_device(tr.model.mu, tr.model, ratings.M, ratings.N, neighbors)
         for t in range(config.epochs):
             tr.epoch(t)
+            params._device_updated()
             if epoch_callback is not None:
-                epoch_callback(t, tr.to_params())
-        return tr.to_params()
+                epoch_callback(t, params)
+                params._device(0)        # upload whatever the callback edited
+        return params
     if mode != "exact":
         raise ValueError(f"unknown mode {mode!r}")
     stats = ratings.baselines()
@@ -499,35 +637,52 @@ def train_full(ratings: SparseRatings, neighbors: NeighborTable | None,
         return params
     _check_model_dims(config.F, K)
     dev = ratings.device()
-    dm = DeviceModel64(params)
+    dm = params._device(64)
+    params._own()
     sc = _Scratch(ratings.M, ratings.N)
     _plan_full(dev, sc, 0, ratings.N, 0, ratings.M)
     pre = _exact_lookups(dev, dm, 0, ratings.N, 0.25)   # once per fit, reused every epoch
     for t in range(config.epochs):
         _colpass(dev, dm, sc, _rates_struct(config.rates_at(t), config.regs), 0, ratings.N, 1, pre=pre)
+        params._device_updated()
         if sc.status_value():
-            dm.download(params)
             raise TrainingDivergedError(epoch=t)
         if epoch_callback is not None:
-            dm.download(params)
             epoch_callback(t, params)
-            dm = DeviceModel64(params)   # the callback may have edited params
-    dm.download(params)
+            dm = params._device(64)      # uploads whatever the callback edited
     return params
+
+
+def _test_device(testset: Triplets, ratings: SparseRatings):
+    """Device (rows, cols, values) of a test set.  The training set itself
+    (``ratings.triplets()``) and split_holdout's test sets are immutable and keep one
+    device copy; any other Triplets is uploaded per call."""
+    src = getattr(testset, "_source", None)
+    if src is not None and src is ratings:
+        return ratings.device_entries()
+    cache = getattr(testset, "_dev", None)
+    if cache is not None:
+        return cache
+    dev = (nat.to_dev(np.asarray(testset.rows, np.int32)), nat.to_dev(np.asarray(testset.cols, np.int32)),
+           nat.to_dev(np.asarray(testset.values, np.float64)))
+    if all(not np.asarray(a).flags.writeable for a in (testset.rows, testset.cols, testset.values)):
+        testset._dev = dev
+    return dev
 
 
 def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
          unscale: float | None = None, clamp: tuple[float, float] | None = None) -> float:
-    """Root-mean-square error over held-out triplets (factorization.py:559-579)."""
+    """Root-mean-square error over held-out triplets (factorization.py:559-579).
+
+    Runs on the resident model (no host copy of the parameters) and, for the training
+    set or an immutable test set, on device-resident triplets."""
     if len(testset) == 0:
         raise ValueError("empty test set")
     _check_model_dims(max(params.F, 1), params.K)
     dev = ratings.device()
-    dm = DeviceModel64(params)
+    dm = params._device(64)
     n = len(testset)
-    tr = nat.to_dev(np.asarray(testset.rows, np.int32))
-    tc = nat.to_dev(np.asarray(testset.cols, np.int32))
-    tv = nat.to_dev(np.asarray(testset.values, np.float64))
+    tr, tc, tv = _test_device(testset, ratings)
     scratch = nat.empty((n + 256,), "float64")
     out = nat.empty((1,), "float64")
     lo, hi = clamp if clamp is not None else (0.0, 0.0)
@@ -544,10 +699,10 @@ def objective_value(params: ModelParams, ratings: SparseRatings, regs: tuple) ->
     d = ratings.entry_values - pred
     total = float(np.add.accumulate(d * d)[-1]) if len(d) else 0.0
     lb, lbh, lu, lv, lw, lc = regs
-    total += lb * float(np.sum(params.b ** 2))
-    total += lbh * float(np.sum(params.b_hat ** 2))
-    total += lu * float(np.sum(params.U ** 2))
-    total += lv * float(np.sum(params.V ** 2))
-    total += lw * float(np.sum(params.W ** 2))
-    total += lc * float(np.sum(params.C ** 2))
+    total += lb * float(np.sum(params._peek("b") ** 2))
+    total += lbh * float(np.sum(params._peek("b_hat") ** 2))
+    total += lu * float(np.sum(params._peek("U") ** 2))
+    total += lv * float(np.sum(params._peek("V") ** 2))
+    total += lw * float(np.sum(params._peek("W") ** 2))
+    total += lc * float(np.sum(params._peek("C") ** 2))
     return total

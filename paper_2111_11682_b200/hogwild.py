@@ -24,29 +24,72 @@ from .factorization import (ModelParams, TrainConfig, TrainingDivergedError, _ra
 from .similarity import NeighborTable
 
 
+_DEV_NAME = {"b": "b", "b_hat": "bhat", "U": "U", "V": "V", "W": "W", "C": "C"}
+
+
 class DeviceModel32:
+    """fp32 model of a Hogwild fit in HBM (CulshModel32); also the device backing of
+    the ModelParams that train_full(mode="hogwild") returns (host views widened to
+    fp64 on first read)."""
+
     def __init__(self, p: ModelParams):
         t = nat.torch()
         dev = nat.device()
         f32 = lambda a: t.from_numpy(np.ascontiguousarray(a, np.float32).reshape(-1)).to(dev)
-        self.F, self.K = p.F, p.K
+        self.M, self.N, self.F, self.K = p.M, p.N, p.F, p.K
         self.mu = float(p.mu)
-        self.b = f32(p.b)
-        self.bhat = f32(p.b_hat)
-        self.U = f32(p.U)
-        self.V = f32(p.V)
-        self.W = f32(p.W) if p.W.size else nat.zeros((1,), "float32")
-        self.C = f32(p.C) if p.C.size else nat.zeros((1,), "float32")
+        self.b = f32(p._peek("b"))
+        self.bhat = f32(p._peek("b_hat"))
+        self.U = f32(p._peek("U"))
+        self.V = f32(p._peek("V"))
+        W, C = p._peek("W"), p._peek("C")
+        self.W = f32(W) if W.size else nat.zeros((1,), "float32")
+        self.C = f32(C) if C.size else nat.zeros((1,), "float32")
+        self.nbr = p.nbr_entries_device()
+        self._restruct()
+
+    def _restruct(self) -> None:
         self.struct = nat.CulshModel32(self.mu, nat.ptr(self.b), nat.ptr(self.bhat), nat.ptr(self.U),
                                        nat.ptr(self.V), nat.ptr(self.W), nat.ptr(self.C), self.F,
                                        self.K)
 
+    def _shape(self, name: str):
+        M, N, F, K = self.M, self.N, self.F, self.K
+        return {"b": (M,), "b_hat": (N,), "U": (M, F), "V": (N, F), "W": (N, K), "C": (N, K)}[name]
+
+    def download(self, name: str, out=None) -> np.ndarray:
+        shape = self._shape(name)
+        n = int(np.prod(shape))
+        host = (nat.to_host(getattr(self, _DEV_NAME[name]))[:n].astype(np.float64).reshape(shape)
+                if n else np.zeros(shape))
+        if out is not None and out.shape == shape and out.dtype == np.float64 and out.flags.writeable:
+            out[...] = host
+            return out
+        return host
+
+    def upload(self, name: str, host: np.ndarray) -> None:
+        a = np.ascontiguousarray(host, dtype=np.float32).reshape(-1)
+        if a.size:
+            getattr(self, _DEV_NAME[name])[:a.size].copy_(nat.torch().from_numpy(a))
+
+    def all_finite(self, M: int, N: int) -> bool:
+        t = nat.torch()
+        F, K = self.F, self.K
+        parts = [self.b[:M], self.bhat[:N], self.U[:M * F], self.V[:N * F], self.W[:N * K], self.C[:N * K]]
+        return all(bool(t.isfinite(x).all().item()) for x in parts if x.numel())
+
+    def widen(self):
+        """An fp64 DeviceModel64 copy (device-side conversion)."""
+        from .factorization import DeviceModel64
+        t = nat.torch()
+        arrays = {n: getattr(self, _DEV_NAME[n]).to(t.float64) for n in _DEV_NAME}
+        return DeviceModel64(arrays=arrays, mu=self.mu, M=self.M, N=self.N, F=self.F, K=self.K,
+                             nbr=self.nbr)
+
     def to_params(self, neighbors: NeighborTable | None, M: int, N: int) -> ModelParams:
-        h = lambda x, shape: nat.to_host(x).astype(np.float64)[:int(np.prod(shape))].reshape(shape)
-        return ModelParams(mu=self.mu, b=h(self.b, (M,)), b_hat=h(self.bhat, (N,)),
-                           U=h(self.U, (M, self.F)), V=h(self.V, (N, self.F)),
-                           W=h(self.W, (N, self.K)), C=h(self.C, (N, self.K)),
-                           neighbors=neighbors)
+        h = lambda n: self.download(n)
+        return ModelParams(mu=self.mu, b=h("b"), b_hat=h("b_hat"), U=h("U"), V=h("V"), W=h("W"),
+                           C=h("C"), neighbors=neighbors)
 
 
 def hogwild_supported(F: int, K: int) -> bool:
@@ -89,8 +132,8 @@ class HogwildTrainer:
         MW = 1 if K <= 32 else 2
         self.MW = MW
         # explicit-neighbour stream (data + J^K only; once per fit)
-        self.nbr = (nat.to_dev(neighbors.entries.reshape(-1), np.int32) if K
-                    else nat.zeros((1,), "int32"))
+        self.nbr = neighbors.device_entries() if K else nat.zeros((1,), "int32")
+        self.model.nbr = self.nbr
         self.mask = nat.zeros((max(d.nnz * MW, 1),), "int32")
         nexpl = nat.zeros((max(d.N, 1),), "int64")
         self.resid_ptr = nat.zeros((d.N + 1,), "int64")

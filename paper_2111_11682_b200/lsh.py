@@ -129,9 +129,17 @@ def assign_row_hashes(M: int, config: LshConfig) -> RowHashes:
 class HashState:
     """Per-column signed accumulators and signatures (lsh.py:186-228).
 
-    ``acc`` (N, q, p, G) float64 and ``sig`` (N, q, p, G) uint8 are numpy
-    arrays materialised on first access; the device copies (and the packed
-    group keys (q, N) uint64) stay resident for the online path.
+    ``acc`` (N, q, p, G) float64 and ``sig`` (N, q, p, G) uint8.  One side is the
+    source of truth:
+
+    * a state built by the device pipeline (``simlsh_topk``, ``update_hashes_incremental``)
+      keeps acc / sig / the packed group keys (q, N) u64 resident on the device; the host
+      arrays are read-only copies materialised on first access, so an in-place edit of
+      them fails loudly instead of silently diverging from the device copy;
+    * a state built from host arrays (the constructor, ``load``, or assigning ``.acc`` /
+      ``.sig``) is owned by the host, as in the reference dataclass: every device use
+      re-reads those arrays (acc uploaded, group keys packed from ``sig``, as
+      ``_state_group_keys`` does at lsh.py:417-423), so edits made to them are seen.
     """
 
     def __init__(self, acc: np.ndarray | None = None, sig: np.ndarray | None = None,
@@ -143,6 +151,7 @@ class HashState:
         self._dev_acc = _dev_acc
         self._dev_sig = _dev_sig
         self._dev_keys = _dev_keys
+        self._host_truth = _dev_acc is None
         self._shape = tuple(_shape) if _shape is not None else tuple(np.shape(acc))
 
     def __eq__(self, other):
@@ -151,32 +160,47 @@ class HashState:
         return (self.config == other.config and np.array_equal(self.acc, other.acc)
                 and np.array_equal(self.sig, other.sig))
 
+    @staticmethod
+    def _readonly(a: np.ndarray) -> np.ndarray:
+        a.flags.writeable = False
+        return a
+
     @property
     def acc(self) -> np.ndarray:
         if self._acc is None:
-            self._acc = nat.to_host(self._dev_acc).reshape(self._shape)
+            self._acc = self._readonly(nat.to_host(self._dev_acc).reshape(self._shape))
         return self._acc
 
     @acc.setter
     def acc(self, value):
+        self._to_host_truth()
         self._acc = value
-        self._dev_acc = None
-        self._dev_keys = None
         self._shape = tuple(np.shape(value))
 
     @property
     def sig(self) -> np.ndarray:
         if self._sig is None:
             if self._dev_sig is not None:
-                self._sig = nat.to_host(self._dev_sig).reshape(self._shape)
+                self._sig = self._readonly(nat.to_host(self._dev_sig).reshape(self._shape))
             else:
                 self._sig = (self.acc >= 0.0).astype(np.uint8)
+                if not self._host_truth:
+                    self._readonly(self._sig)
         return self._sig
 
     @sig.setter
     def sig(self, value):
+        self._to_host_truth()
         self._sig = value
-        self._dev_sig = None
+
+    def _to_host_truth(self) -> None:
+        """Switch ownership to the host arrays (materialising the other one first)."""
+        if not self._host_truth:
+            acc, sig = self.acc, self.sig
+            self._acc = np.array(acc)
+            self._sig = np.array(sig)
+        self._host_truth = True
+        self._dev_acc = self._dev_sig = self._dev_keys = None
 
     @property
     def N(self) -> int:
@@ -189,21 +213,32 @@ class HashState:
         return self.sig[:, g, m, :]
 
     def device_acc(self):
-        if self._dev_acc is None:
-            self._dev_acc = nat.to_dev(np.ascontiguousarray(self._acc, dtype=np.float64).reshape(-1)
-                                       if np.size(self._acc) else np.zeros(1))
+        """acc (N*q*p*G,) f64 on the device: the resident copy, or a fresh upload of the
+        host array when the host owns the state."""
+        if self._host_truth:
+            return nat.to_dev(np.ascontiguousarray(self._acc, dtype=np.float64).reshape(-1)
+                              if np.size(self._acc) else np.zeros(1))
         return self._dev_acc
 
     def device_keys(self):
-        """(q, N) uint64 group keys on the device (recomputed from acc if absent)."""
-        if self._dev_keys is None:
-            c = self.config
-            N = self.N
-            keys = nat.empty((c.q * max(N, 1),), "uint64")
-            if N:
-                _keys_from_acc(self.device_acc(), N, c, keys)
+        """(q, N) uint64 group keys on the device: resident, or packed from the host
+        ``sig`` when the host owns the state (lsh.py:417-423 derives keys from sig)."""
+        if not self._host_truth and self._dev_keys is not None:
+            return self._dev_keys
+        c = self.config
+        N = self.N
+        keys = nat.empty((c.q * max(N, 1),), "uint64")
+        if N:
+            if self._host_truth:
+                sig = self._sig if self._sig is not None else (self._acc >= 0.0)
+                sig_dev = nat.to_dev(np.ascontiguousarray(sig, dtype=np.uint8).reshape(-1))
+                nat.call("culsh_pack_keys", nat.ptr(sig_dev), N, c.q, c.p, c.G, nat.ptr(keys),
+                         nat.stream_ptr())
+            else:
+                _keys_from_acc(self._dev_acc, N, c, keys)
+        if not self._host_truth:
             self._dev_keys = keys
-        return self._dev_keys
+        return keys
 
     def save(self, path) -> None:
         c = self.config

@@ -30,23 +30,7 @@ from .data import DeviceRatings
 from .factorization import (DeviceModel64, ModelParams, TrainConfig, TrainingDivergedError,
                             _Scratch, _colpass, _exact_lookups, _plan_full, _rates_struct)
 from .lsh import HashState, LshConfig, RowHashes, _ns, _table_alloc, _topk_device
-from .online import IncrementBatch, device_segments
-
-
-def _device_baselines(M: int, N: int, col_ptr, col_vals, row_ptr, row_vals, nnz: int):
-    """compute_baselines (data.py:289-309) from the two views' segment sums."""
-    t = nat.torch()
-    cs = nat.empty((max(N, 1),), "float64")
-    rs = nat.empty((max(M, 1),), "float64")
-    nat.call("culsh_segment_sums", N, nat.ptr(col_ptr), nat.ptr(col_vals), nat.ptr(cs), nat.stream_ptr())
-    nat.call("culsh_segment_sums", M, nat.ptr(row_ptr), nat.ptr(row_vals), nat.ptr(rs), nat.stream_ptr())
-    cs, rs = cs[:N], rs[:M]
-    mu = float(cs.sum().item()) / max(nnz, 1)
-    cnt_c = (col_ptr[1:] - col_ptr[:-1]).to(t.float64)
-    rc = (row_ptr[1:] - row_ptr[:-1]).to(t.float64)
-    bb = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
-    bh = t.where(cnt_c > 0, cs / cnt_c.clamp(min=1) - mu, t.zeros_like(cs))
-    return mu, bb, bh
+from .online import IncrementBatch, append_device
 
 
 class _Reserve:
@@ -168,31 +152,11 @@ class OnlineSession:
         br = nat.to_dev(np.asarray(batch.rows, np.int32))
         bcl = nat.to_dev(np.asarray(batch.cols, np.int32))
         bv = nat.to_dev(np.asarray(batch.values, np.float64))
-        cptr_d, crow_d, cval_d = device_segments(N_hat, bcl, br, bv)
-        rptr_d, rcol_d, rval_d = device_segments(M_hat, br, bcl, bv)
-        nnz_hat = d.nnz + len(batch.rows)
         self._cur ^= 1
-        sizes = {"N1": N_hat + 1, "M1": M_hat + 1, "nnz": nnz_hat}
-        out = {f: self._sets[self._cur][f].view(sizes[k]) for f, _, k in _VIEW_FIELDS}
-        new_col_ptr, new_col_rows, new_col_vals = out["col_ptr"], out["col_rows"], out["col_vals"]
-        new_row_ptr, new_row_cols, new_row_vals = out["row_ptr"], out["row_cols"], out["row_vals"]
-        nat.call("culsh_append_segments", N_old, N_hat, nat.ptr(d.col_ptr), nat.ptr(d.col_rows),
-                 nat.ptr(d.col_vals), nat.ptr(cptr_d), nat.ptr(crow_d), nat.ptr(cval_d),
-                 nat.ptr(new_col_ptr), nat.ptr(new_col_rows), nat.ptr(new_col_vals), nat.stream_ptr())
-        nat.call("culsh_append_segments", M_old, M_hat, nat.ptr(d.row_ptr), nat.ptr(d.row_cols),
-                 nat.ptr(d.row_vals), nat.ptr(rptr_d), nat.ptr(rcol_d), nat.ptr(rval_d),
-                 nat.ptr(new_row_ptr), nat.ptr(new_row_cols), nat.ptr(new_row_vals), nat.stream_ptr())
-        mu_x, bb, bh = _device_baselines(M_hat, N_hat, new_col_ptr, new_col_vals, new_row_ptr,
-                                         new_row_vals, nnz_hat)
-
-        def merged_map(nd):
-            nat.call("culsh_append_csc2csr", ctypes.byref(nd.struct), N_old, nat.ptr(d.col_ptr),
-                     nat.ptr(d.csc2csr), nat.ptr(rptr_d), M_old, nat.ptr(nd.csc2csr), nat.stream_ptr())
-
-        self.dev = DeviceRatings.from_device(M_hat, N_hat, new_col_ptr, new_col_rows[:nnz_hat],
-                                             new_col_vals[:nnz_hat], new_row_ptr, new_row_cols[:nnz_hat],
-                                             new_row_vals[:nnz_hat], mu_x, bb, bh, csc2csr=merged_map,
-                                             map_out=out["csc2csr"])
+        sets = self._sets[self._cur]
+        d._integer_valued = True          # checked at construction and per batch
+        self.dev, (rptr_d, rval_d, cptr_d, cval_d) = append_device(
+            d, M_hat, N_hat, br, bcl, bv, alloc=lambda f, dt, n: sets[f].view(n))
         t0 = mark("extend_ratings", t0)
         # (5) extend the model (online.py:187-227), same PCG64 stream as the reference
         cfg = self.config

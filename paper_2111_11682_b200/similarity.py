@@ -49,6 +49,17 @@ class NeighborTable:
             if bad.any():
                 raise ValueError(f"neighbor index out of range in row {int(np.flatnonzero(bad)[0])}")
 
+    def device_entries(self):
+        """(N*K,) int32 copy of ``entries`` in HBM.  Cached against a host snapshot, so an
+        in-place edit of ``entries`` (a plain array, as in the reference) is picked up."""
+        e = np.ascontiguousarray(self.entries, dtype=np.int32)
+        cache = self.__dict__.get("_dev_cache")
+        if cache is not None and cache[1].shape == e.shape and np.array_equal(cache[1], e):
+            return cache[0]
+        dev = nat.to_dev(e.reshape(-1) if e.size else np.zeros(1, np.int32), np.int32)
+        self.__dict__["_dev_cache"] = (dev, e.copy())
+        return dev
+
     def write_csv(self, path) -> None:
         with open(path, "w") as fh:
             fh.write("j,rank,neighbor\n")

@@ -1,0 +1,168 @@
+"""GPU: the drop-in API on device-resident objects -- live device-backed ModelParams in
+epoch callbacks, rmse/predict on the resident model, and the online step
+(extend_ratings / extend_params / train_incremental / absorb_increment) built in HBM --
+all bit-identical to the oracle / the reference-written fixtures."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2111_11682_b200 as p
+    return p
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle
+    return oracle
+
+
+def _case(P, seed=0, M=120, N=60, dens=0.15, integer=True):
+    rng = np.random.default_rng(seed)
+    rows, cols = np.nonzero(rng.random((M, N)) < dens)
+    vals = (rng.integers(1, 6, len(rows)).astype(np.float64) if integer
+            else np.round(rng.random(len(rows)) * 5, 3))
+    return P.SparseRatings(M, N, rows, cols, vals), rows, cols, vals
+
+
+def test_callback_gets_live_device_params(P, orc):
+    """The callback's rmse runs on the resident model; the fit equals the oracle's."""
+    r, rows, cols, vals = _case(P)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 6)
+    cfg = P.TrainConfig(F=8, K=6, epochs=4, seed=1)
+    seen, ids = [], []
+
+    def cb(t, p):
+        ids.append(id(p))
+        seen.append(P.rmse(p, r.triplets(), r))
+        assert all(s == "D" for s in p._state.values())     # nothing copied to the host
+
+    p = P.train_full(r, tbl, cfg, epoch_callback=cb)
+    assert len(set(ids)) == 1 and ids[0] == id(p)            # the live object, as in the reference
+    d, mu = orc.build_csr(r.M, r.N, rows, cols, vals)
+    ref_rmse = []
+    m = orc.train_full(d, mu, tbl.entries, 8, 6, 4, 1, cfg.rates_at, cfg.regs,
+                       callback=lambda t, mm: ref_rmse.append(
+                           orc.rmse(d, mm, r.entry_rows, r.entry_cols, r.entry_values)))
+    assert p.U.tobytes() == m.U.tobytes() and p.W.tobytes() == m.W.tobytes()
+    assert np.array_equal(np.array(seen), np.array(ref_rmse))
+
+
+def test_callback_edits_reach_the_device(P, orc):
+    """Edits the callback makes to the host arrays are trained on (reference: live arrays)."""
+    r, rows, cols, vals = _case(P, seed=2)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 5)
+    cfg = P.TrainConfig(F=8, K=5, epochs=3, seed=4)
+
+    def edit(U, W):
+        U[3] *= 2.0
+        W[:, 0] = 0.25
+
+    def cb(t, p):
+        if t == 0:
+            edit(p.U, p.W)
+
+    p = P.train_full(r, tbl, cfg, epoch_callback=cb)
+    d, mu = orc.build_csr(r.M, r.N, rows, cols, vals)
+    m = orc.train_full(d, mu, tbl.entries, 8, 5, 3, 4, cfg.rates_at, cfg.regs,
+                       callback=lambda t, mm: edit(mm.U, mm.W) if t == 0 else None)
+    for a, b in ((p.U, m.U), (p.V, m.V), (p.W, m.W), (p.C, m.C), (p.b, m.b), (p.b_hat, m.bhat)):
+        assert a.tobytes() == b.tobytes()
+
+
+def test_hogwild_callback_edit_applied(P):
+    r, *_ = _case(P, seed=5, M=300, N=80)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 4)
+    cfg = P.TrainConfig(F=16, K=4, epochs=2, seed=0)
+    seen = []
+
+    def cb(t, p):
+        seen.append(P.rmse(p, r.triplets(), r))
+        if t == 0:
+            p.U[:] = 0.0            # an edit the next epoch must start from
+            p.V[:] = 0.0
+    p = P.train_full(r, tbl, cfg, epoch_callback=cb, mode="hogwild")
+    # with u = v = 0 every u/v gradient is 0: they stay exactly 0 through epoch 1
+    assert not p.U.any() and not p.V.any()
+    assert np.isfinite(seen).all()
+
+
+def test_rmse_predict_reuse_resident_model(P, orc):
+    r, rows, cols, vals = _case(P, seed=6)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 6)
+    cfg = P.TrainConfig(F=8, K=6, epochs=2, seed=1)
+    p = P.train_full(r, tbl, cfg)
+    dev = p._dev
+    x = P.rmse(p, r.triplets(), r)
+    y = P.predict(3, int(r.entry_cols[r.entry_rows == 3][0]), p, r)
+    assert p._dev is dev and all(s == "D" for s in p._state.values())
+    d, mu = orc.build_csr(r.M, r.N, rows, cols, vals)
+    m = orc.train_full(d, mu, tbl.entries, 8, 6, 2, 1, cfg.rates_at, cfg.regs)
+    assert x == orc.rmse(d, m, r.entry_rows, r.entry_cols, r.entry_values)
+    # a host edit after the fit is seen by the next evaluation
+    p.U[:] = 0.0
+    m.U[:] = 0.0
+    assert P.rmse(p, r.triplets(), r) == orc.rmse(d, m, r.entry_rows, r.entry_cols, r.entry_values)
+    assert np.isfinite(y)
+
+
+@pytest.mark.parametrize("integer", [True, False])
+def test_extend_ratings_on_device_equals_rebuild(P, integer):
+    """Device append == the reference's full rebuild: entries, CSR, CSC and baselines."""
+    full, *_ = _case(P, seed=8, M=90, N=50, dens=0.3, integer=integer)
+    orig, batch, _, _ = P.holdback_variables(full, 7, 5, seed=1)
+    ext = P.extend_ratings(orig, batch)
+    ref = P.SparseRatings(batch.M_hat, batch.N_hat, np.concatenate([orig.entry_rows, batch.rows]),
+                          np.concatenate([orig.entry_cols, batch.cols]),
+                          np.concatenate([orig.entry_values, batch.values]))
+    for name in ("entry_rows", "entry_cols", "entry_values", "row_ptr", "row_cols", "row_vals",
+                 "col_ptr", "col_rows", "col_vals"):
+        assert getattr(ext, name).tobytes() == getattr(ref, name).tobytes(), name
+    a, b = ext.baselines(), ref.baselines()
+    assert a.mu == b.mu and a.b.tobytes() == b.b.tobytes() and a.b_hat.tobytes() == b.b_hat.tobytes()
+    d = ext.device()
+    from paper_2111_11682_b200 import _native as nat
+    assert nat.to_host(d.base_b)[:ext.M].tobytes() == b.b.tobytes()
+    assert nat.to_host(d.csc2csr)[:ext.nnz].tobytes() == nat.to_host(ref.device().csc2csr)[:ext.nnz].tobytes()
+
+
+def test_absorb_increment_chain_matches_oracle(P, orc):
+    """Three increments through the public API, each bit-identical to the oracle."""
+    full, *_ = _case(P, seed=11, M=160, N=70, dens=0.2)
+    lc = P.LshConfig(G=4, p=2, q=10, psi_exponent=2, seed=2)
+    cfg = P.TrainConfig(F=8, K=5, epochs=2, seed=3)
+    orig, b3, _, _ = P.holdback_variables(full, 12, 6, seed=0)
+    tbl, state = P.simlsh_topk(orig, lc, 5)
+    params = P.train_full(orig, tbl, cfg)
+    ratings = orig
+    # split the held-back variables into three successive batches
+    M0, N0 = orig.M, orig.N
+    m_, c_ = [M0, M0 + 4, M0 + 8, M0 + 12], [N0, N0 + 2, N0 + 4, N0 + 6]
+    d0, mu0 = orc.build_csr(orig.M, orig.N, orig.entry_rows, orig.entry_cols, orig.entry_values)
+    m = orc.train_full(d0, mu0, tbl.entries, 8, 5, 2, 3, cfg.rates_at, cfg.regs)
+    acc = state.acc.copy()
+    trip = (orig.entry_rows, orig.entry_cols, orig.entry_values)
+    for k in range(3):
+        sel = ((b3.rows < m_[k + 1]) & (b3.cols < c_[k + 1])) & ~((b3.rows < m_[k]) & (b3.cols < c_[k]))
+        batch = P.IncrementBatch(m_[k], c_[k], m_[k + 1] - m_[k], c_[k + 1] - c_[k],
+                                 b3.rows[sel], b3.cols[sel], b3.values[sel])
+        params, state, ratings, tbl = P.absorb_increment(params, state, ratings, batch, cfg)
+        m, acc, ent, _ = orc.absorb_increment(
+            m, acc, (lc.G, lc.p, lc.q, lc.psi_exponent, lc.seed), None, trip,
+            (batch.base_M, batch.base_N, batch.new_row_count, batch.new_col_count, batch.rows,
+             batch.cols, batch.values), 8, 5, 2, 3, cfg.rates_at, cfg.regs)
+        trip = tuple(np.concatenate([a, b]) for a, b in zip(trip, (batch.rows, batch.cols, batch.values)))
+        assert state.acc.tobytes() == acc.tobytes(), k
+        assert tbl.entries.tobytes() == ent.tobytes(), k
+        for a, b in ((params.U, m.U), (params.V, m.V), (params.W, m.W), (params.C, m.C),
+                     (params.b, m.b), (params.b_hat, m.bhat)):
+            assert a.tobytes() == b.tobytes(), k
