@@ -297,6 +297,23 @@ int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int32_t *nbr,
                  const int32_t *t_rows, const int32_t *t_cols, const double *t_vals, int64_t n,
                  double *sqerr_scratch, double *rmse_out, void *stream);
 
+/* Lookup cache of the training set for culsh_rmse_train: the explicit-neighbour mask of
+ * every CSC entry (culsh_explicit_stream) is turned into the CSC position of each
+ * explicit pair r(i, J[j, k]).  Call with group_count != NULL to get the number of pairs
+ * per 32-entry group, then (after an exclusive scan into group_base) with
+ * group_count == NULL to fill pos (int32, CSC order). */
+int culsh_train_lookup(const CulshData *d, const int32_t *nbr, int K, const uint32_t *mask,
+                       int64_t *group_count, const int64_t *group_base, int32_t *pos, void *stream);
+
+/* factorization.py:559-579 rmse over the TRAINING set itself (cli.py:204-210 calls it
+ * every epoch): the CSC entries of d, neighbour values from the lookup cache, the squared
+ * error of CSC position c stored at entry index perm[c] (NULL: identity) so the sum runs
+ * in the reference's entry order (sequential for nnz <= 2^22, else the fixed tree). */
+int culsh_rmse_train(const CulshData *d, const CulshModel64 *m, const uint32_t *mask,
+                     const int64_t *group_base, const int32_t *pos, const int64_t *perm, int do_clamp,
+                     double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
+                     double *rmse_out, void *stream);
+
 /* factorization.py:235-263 _predict_one for n (i, j) pairs -> out (n) f64. */
 int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows,
                   const int32_t *cols, int64_t n, double *out, void *stream);
@@ -367,6 +384,16 @@ int culsh_pair_similarity(const int64_t *col_ptr, const int32_t *col_rows, const
  * entry.  in_test: nnz bytes (0/1).  Returns the number taken, or a negative error. */
 int64_t culsh_split_holdout(const int32_t *entry_rows, const int32_t *entry_cols, int64_t nnz, int64_t M,
                             int64_t N, const int64_t *perm, int64_t n_test, uint8_t *in_test);
+
+/* --------------------------------------------------------------- init --- */
+
+/* factorization.py:196-211 init_params / online.py:187-227 extend_params draws:
+ * out[k] = 0.0 + scale * u_{skip+k} for k < n, u_t the t-th double of numpy's PCG64
+ * stream seeded to (state, inc) = default_rng(seed).bit_generator.state (128-bit
+ * halves), i.e. rng.uniform(0, scale, ...) bit for bit.  fp32 != 0 stores the fp64
+ * value rounded to float (the Hogwild model).  Replaces the host numpy draw. */
+int culsh_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                        uint64_t skip, int64_t n, double scale, int fp32, void *out, void *stream);
 
 #ifdef __cplusplus
 }

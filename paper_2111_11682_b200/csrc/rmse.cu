@@ -1,8 +1,8 @@
 // Evaluation: exact fp64 prediction and RMSE.
-// predict_one restates factorization.py:235-263 in its exact operation order
-// (compiled with -fmad=false); the RMSE sum is sequential (bit-identical to
-// factorization.py:394-409) when `sequential` is set, otherwise a fixed
-// pairwise tree (deterministic, within a few ulp of the sequential sum).
+// pred_tile_kernel restates factorization.py:235-263 _predict_one in its exact operation
+// order (explicit _rn intrinsics; the TU is also compiled with -fmad=false); the RMSE sum
+// is sequential (bit-identical to factorization.py:394-409) when `sequential` is set,
+// otherwise a fixed pairwise tree (deterministic, within a few ulp of the sequential sum).
 #include "common.cuh"
 
 namespace culsh {
@@ -19,57 +19,35 @@ __device__ __forceinline__ bool lookup_rv(const int64_t *row_ptr, const int32_t 
     return false;
 }
 
-template <typename P>
-__device__ double predict_one(const CulshData &d, double mu, const P *b, const P *bhat, const P *U,
-                              const P *V, const P *W, const P *C, const int32_t *nbr, int F, int K,
-                              int64_t i, int64_t j) {
-    double pred = mu + (double)b[i] + (double)bhat[j];
-    double dot = 0.0;
-    for (int f = 0; f < F; ++f) dot = dot + (double)U[i * F + f] * (double)V[j * F + f];
-    pred = pred + dot;
-    if (K > 0) {
-        int nr = 0, nn = 0;
-        double sw = 0.0, sc = 0.0;
-        for (int k = 0; k < K; ++k) {
-            const int32_t j1 = nbr[j * K + k];
-            double rv;
-            if (lookup_rv(d.row_ptr, d.row_cols, d.row_vals, i, j1, &rv)) {
-                ++nr;
-                sw = sw + (rv - (mu + d.base_b[i] + d.base_bhat[j1])) * (double)W[j * K + k];
-            } else {
-                ++nn;
-                sc = sc + (double)C[j * K + k];
-            }
-        }
-        if (nr > 0) pred = pred + sw / sqrt((double)nr);
-        if (nn > 0) pred = pred + sc / sqrt((double)nn);
-    }
-    return pred;
-}
-
-template <typename P>
-__global__ void sqerr_kernel(CulshData d, double mu, const P *b, const P *bhat, const P *U, const P *V,
-                             const P *W, const P *C, const int32_t *nbr, int F, int K,
-                             const int32_t *t_rows, const int32_t *t_cols, const double *t_vals,
-                             int64_t n, int do_clamp, double lo, double hi, double unscale,
-                             double *out, int mode) {
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-         x += (int64_t)gridDim.x * blockDim.x) {
-        double pred = predict_one<P>(d, mu, b, bhat, U, V, W, C, nbr, F, K, t_rows[x], t_cols[x]);
-        if (mode == 1) { out[x] = pred; continue; }
-        if (do_clamp) {
-            if (pred < lo) pred = lo;
-            else if (pred > hi) pred = hi;
-        }
-        const double dd = (pred - t_vals[x]) * unscale;
-        out[x] = dd * dd;
-    }
-}
-
-__global__ void seq_sum_kernel(const double *x, int64_t n, double *out) {
+// Sequential sum in index order (the reference's serial loop, bit-exact).  The chain of
+// dependent adds cannot be parallelised, but its operands can be staged: warps 1..31
+// copy the next 2048-element chunk into shared memory while lane 0 of warp 0 adds the
+// current one, so the loop runs at add latency instead of global-load latency.
+__global__ void __launch_bounds__(1024) seq_sum_kernel(const double *__restrict__ x, int64_t n,
+                                                       double *out) {
+    constexpr int CH = 2048;
+    __shared__ double buf[2][CH];
+    const int tid = threadIdx.x;
     double total = 0.0;
-    for (int64_t k = 0; k < n; ++k) total = total + x[k];
-    *out = sqrt(total / (double)n);
+    const int64_t nch = (n + CH - 1) / CH;
+    for (int k = tid; k < CH; k += blockDim.x) buf[0][k] = k < n ? x[k] : 0.0;
+    __syncthreads();
+    for (int64_t c = 0; c < nch; ++c) {
+        const int cur = (int)(c & 1);
+        if (tid >= 32) {
+            const int64_t base = (c + 1) * CH;
+            if (base < n)
+                for (int k = tid - 32; k < CH; k += blockDim.x - 32)
+                    buf[cur ^ 1][k] = base + k < n ? x[base + k] : 0.0;
+        } else if (tid == 0) {
+            const int m = (int)min64(CH, n - c * CH);
+            const double *b = buf[cur];
+#pragma unroll 8
+            for (int k = 0; k < m; ++k) total = __dadd_rn(total, b[k]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *out = sqrt(total / (double)n);
 }
 
 // fixed-shape pairwise tree: 1024-wide blocks, then one block over the partials
@@ -92,10 +70,224 @@ __global__ void finish_kernel(const double *partial, int np, int64_t n, double *
     *out = sqrt(t / (double)n);
 }
 
+// ---- warp-tiled prediction ---------------------------------------------------------
+// A warp evaluates 32 ratings at once, lane l owning rating l.  The dot product's
+// operands are read cooperatively (for each rating r of the group, lane f loads U[i_r, f]
+// and V[j_r, f]: one coalesced row segment instead of 32 scattered per-lane walks), the
+// products go through a per-warp 32x33 shared tile, and lane l then adds its rating's
+// products in f order -- the reference's sequential fp64 sum, so predictions are
+// bit-identical to predict_one.  The neighbour part is lane-local: rating values either
+// by binary search in the CSR row (any triplets) or from the per-fit lookup cache of the
+// training set (PRE: explicit-neighbour mask + CSC positions of the rated neighbours).
+struct PreLookup {
+    const uint32_t *mask;        // (nnz * MW) explicit-neighbour bits per CSC entry
+    const int64_t *group_base;   // first pos index of each 32-entry group
+    const int32_t *pos;          // CSC position of r(i, J[j, k]) per explicit pair, CSC order
+    const int64_t *perm;         // entry index of each CSC position (nullptr: identity)
+    int MW;
+};
+
+__device__ __forceinline__ int64_t column_of(const int64_t *col_ptr, int64_t N, int64_t e) {
+    int64_t lo = 0, hi = N;   // last j with col_ptr[j] <= e
+    while (hi - lo > 1) {
+        const int64_t m = (lo + hi) >> 1;
+        if (__ldg(col_ptr + m) <= e) lo = m; else hi = m;
+    }
+    return lo;
+}
+
+constexpr int kTileLd = 33;
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// WARPS per block; PRE: training set (CSC entries, V rows mostly shared by the group ->
+// read directly), else any triplets (V rows staged like U's).
+template <typename P, bool PRE>
+__global__ void __launch_bounds__(PRE ? 128 : 64) pred_tile_kernel(CulshData d, double mu, const P *__restrict__ b,
+                                                        const P *__restrict__ bhat, const P *__restrict__ U,
+                                                        const P *__restrict__ V, const P *__restrict__ W,
+                                                        const P *__restrict__ C, const int32_t *__restrict__ nbr,
+                                                        int F, int K, const int32_t *__restrict__ t_rows,
+                                                        const int32_t *__restrict__ t_cols,
+                                                        const double *__restrict__ t_vals, int64_t n, PreLookup pre,
+                                                        int mode, int do_clamp, double lo, double hi,
+                                                        double unscale, double *__restrict__ out) {
+    constexpr int WPB = PRE ? 4 : 2;
+    constexpr int NT = PRE ? 1 : 2;
+    __shared__ P tiles[WPB][NT][32 * kTileLd];
+    P *ut = tiles[threadIdx.x >> 5][0];
+    P *vt = tiles[threadIdx.x >> 5][NT - 1];
+    const int lane = (int)lane_id();
+    const int64_t warps = (int64_t)gridDim.x * WPB;
+    for (int64_t g = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5); g * 32 < n; g += warps) {
+        const int64_t e = g * 32 + lane;
+        const bool valid = e < n;
+        int64_t i = 0, j = 0;
+        if (valid) {
+            if (PRE) {
+                i = d.col_rows[e];
+                j = column_of(d.col_ptr, d.N, e);
+            } else {
+                i = t_rows[e];
+                j = t_cols[e];
+            }
+        }
+        double pred = valid ? __dadd_rn(__dadd_rn(mu, (double)b[i]), (double)bhat[j]) : 0.0;
+        double dot = 0.0;
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        for (int f0 = 0; f0 < F; f0 += 32) {
+            const int f = f0 + lane;
+            // stage this f-chunk of the group's U (and V) rows: all 32 row segments in flight
+            // at once (cp.async, no register staging); lane f fills column f of the tile
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+                if (!((vmask >> r) & 1u)) continue;          // warp-uniform
+                const int64_t ir = __shfl_sync(0xffffffffu, i, r);
+                const int64_t jr = PRE ? 0 : __shfl_sync(0xffffffffu, j, r);
+                if (f < F) {
+                    cp_async<sizeof(P)>(ut + lane * kTileLd + r, U + ir * F + f);
+                    if (!PRE) cp_async<sizeof(P)>(vt + lane * kTileLd + r, V + jr * F + f);
+                }
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            const int fe = F - f0 < 32 ? F - f0 : 32;
+            if (valid) {
+                for (int q = 0; q < fe; ++q) {
+                    const double v = PRE ? (double)__ldg(V + j * F + f0 + q) : (double)vt[q * kTileLd + lane];
+                    dot = __dadd_rn(dot, __dmul_rn((double)ut[q * kTileLd + lane], v));
+                }
+            }
+            __syncwarp();
+        }
+        pred = __dadd_rn(pred, dot);
+        int nr = 0, nn = 0;
+        double sw = 0.0, sc = 0.0;
+        int64_t cur = 0;
+        uint32_t mw0 = 0u, mw1 = 0u;
+        if (PRE) {
+            int pc = 0;
+            if (valid && K > 0) {
+                mw0 = pre.mask[e * pre.MW];
+                if (pre.MW == 2) mw1 = pre.mask[e * pre.MW + 1];
+                pc = __popc(mw0) + __popc(mw1);
+            }
+            int incl = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            cur = (K > 0 ? pre.group_base[g] : 0) + incl - pc;
+        }
+        if (valid && K > 0) {
+            const double bb = d.base_b[i];
+            for (int k = 0; k < K; ++k) {
+                const int32_t j1 = nbr[j * K + k];
+                double rv;
+                bool found;
+                if (PRE) {
+                    found = (((k < 32 ? mw0 : mw1) >> (k & 31)) & 1u) != 0;
+                    if (found) rv = d.col_vals[pre.pos[cur++]];
+                } else {
+                    found = lookup_rv(d.row_ptr, d.row_cols, d.row_vals, i, j1, &rv);
+                }
+                if (found) {
+                    ++nr;
+                    sw = __dadd_rn(sw, __dmul_rn(__dsub_rn(rv, __dadd_rn(__dadd_rn(mu, bb), d.base_bhat[j1])),
+                                                 (double)W[j * K + k]));
+                } else {
+                    ++nn;
+                    sc = __dadd_rn(sc, (double)C[j * K + k]);
+                }
+            }
+            if (nr > 0) pred = __dadd_rn(pred, __ddiv_rn(sw, __dsqrt_rn((double)nr)));
+            if (nn > 0) pred = __dadd_rn(pred, __ddiv_rn(sc, __dsqrt_rn((double)nn)));
+        }
+        if (!valid) continue;
+        if (mode == 1) {
+            out[e] = pred;
+            continue;
+        }
+        if (do_clamp) {
+            if (pred < lo) pred = lo;
+            else if (pred > hi) pred = hi;
+        }
+        const double val = PRE ? d.col_vals[e] : t_vals[e];
+        const double dd = __dmul_rn(__dsub_rn(pred, val), unscale);
+        out[PRE && pre.perm ? pre.perm[e] : e] = __dmul_rn(dd, dd);
+    }
+}
+
+// Lookup cache of the training set: per 32-entry group of CSC entries, the number of
+// explicit (i, J[j, k]) pairs, then their CSC positions (warp scan per group).
+__global__ void lookup_count_kernel(int64_t nnz, const uint32_t *__restrict__ mask, int MW,
+                                    int64_t *__restrict__ group_count) {
+    const int lane = (int)lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g * 32 < nnz; g += warps) {
+        const int64_t e = g * 32 + lane;
+        int pc = 0;
+        if (e < nnz) {
+            pc = __popc(mask[e * MW]);
+            if (MW == 2) pc += __popc(mask[e * MW + 1]);
+        }
+        pc = warp_sum(pc);
+        if (lane == 0) group_count[g] = pc;
+    }
+}
+
+__global__ void lookup_fill_kernel(CulshData d, const int32_t *__restrict__ nbr, int K, const uint32_t *__restrict__ mask,
+                                   int MW, const int64_t *__restrict__ group_base, int32_t *__restrict__ pos) {
+    const int lane = (int)lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g * 32 < d.nnz; g += warps) {
+        const int64_t e = g * 32 + lane;
+        uint32_t m0 = 0u, m1 = 0u;
+        if (e < d.nnz) {
+            m0 = mask[e * MW];
+            if (MW == 2) m1 = mask[e * MW + 1];
+        }
+        const int pc = __popc(m0) + __popc(m1);
+        int incl = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (!pc) continue;
+        int64_t cur = group_base[g] + incl - pc;
+        const int64_t j = column_of(d.col_ptr, d.N, e);
+        const int32_t i = d.col_rows[e];
+        for (int q = 0; q < MW; ++q) {
+            uint32_t m = q == 0 ? m0 : m1;
+            while (m) {
+                const int k = 32 * q + __ffs(m) - 1;
+                m &= m - 1u;
+                const int32_t j1 = nbr[j * K + k];
+                int64_t lo2 = d.col_ptr[j1], hi2 = d.col_ptr[j1 + 1];
+                while (lo2 < hi2) {   // the row is present (the mask says so)
+                    const int64_t mid = (lo2 + hi2) >> 1;
+                    if (__ldg(d.col_rows + mid) < i) lo2 = mid + 1; else hi2 = mid;
+                }
+                pos[cur++] = (int32_t)lo2;
+            }
+        }
+    }
+}
+
 int reduce_rmse(const double *sq, int64_t n, double *out, double *scratch_partials, bool sequential,
                 cudaStream_t st) {
     if (sequential) {
-        seq_sum_kernel<<<1, 1, 0, st>>>(sq, n, out);
+        seq_sum_kernel<<<1, 1024, 0, st>>>(sq, n, out);
     } else {
         const int np = 256;
         tree_sum_kernel<<<np, 1024, 0, st>>>(sq, n, scratch_partials);
@@ -115,10 +307,43 @@ extern "C" int culsh_rmse(const CulshData *d, const CulshModel64 *m, const int32
                           double *rmse_out, void *stream) {
     CULSH_REQUIRE(n > 0, "empty test set");
     cudaStream_t st = (cudaStream_t)stream;
-    const int blocks = (int)min64((n + 127) / 128, (int64_t)num_sms() * 16);
-    sqerr_kernel<double><<<blocks, 128, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->nbr,
-                                                 m->F, m->K, t_rows, t_cols, t_vals, n, do_clamp, clamp_lo,
-                                                 clamp_hi, unscale, sqerr_scratch, 0);
+    const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
+    pred_tile_kernel<double, false><<<blocks, 64, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
+                                                            m->nbr, m->F, m->K, t_rows, t_cols, t_vals, n,
+                                                            PreLookup{}, 0, do_clamp, clamp_lo, clamp_hi, unscale,
+                                                            sqerr_scratch);
+    CULSH_LAUNCH_CHECK();
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+}
+
+extern "C" int culsh_train_lookup(const CulshData *d, const int32_t *nbr, int K, const uint32_t *mask,
+                                  int64_t *group_count, const int64_t *group_base, int32_t *pos, void *stream) {
+    CULSH_REQUIRE(K >= 1 && K <= 64, "K must be in [1, 64]");
+    if (d->nnz <= 0) return CULSH_OK;
+    const int MW = K <= 32 ? 1 : 2;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = num_sms() * 16;
+    if (group_count)
+        lookup_count_kernel<<<blocks, 256, 0, st>>>(d->nnz, mask, MW, group_count);
+    else
+        lookup_fill_kernel<<<blocks, 256, 0, st>>>(*d, nbr, K, mask, MW, group_base, pos);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_rmse_train(const CulshData *d, const CulshModel64 *m, const uint32_t *mask,
+                                const int64_t *group_base, const int32_t *pos, const int64_t *perm, int do_clamp,
+                                double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
+                                double *rmse_out, void *stream) {
+    const int64_t n = d->nnz;
+    CULSH_REQUIRE(n > 0, "empty training set");
+    CULSH_REQUIRE(m->K == 0 || (mask && group_base && pos), "lookup cache missing");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = (int)min64((n + 127) / 128, (int64_t)num_sms() * 12);
+    PreLookup pre{mask, group_base, pos, perm, m->K <= 32 ? 1 : 2};
+    pred_tile_kernel<double, true><<<blocks, 128, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
+                                                           m->nbr, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
+                                                           do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
     return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
 }
@@ -128,10 +353,10 @@ extern "C" int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int
                             double *sqerr_scratch, double *rmse_out, void *stream) {
     CULSH_REQUIRE(n > 0, "empty test set");
     cudaStream_t st = (cudaStream_t)stream;
-    const int blocks = (int)min64((n + 127) / 128, (int64_t)num_sms() * 16);
-    sqerr_kernel<float><<<blocks, 128, 0, st>>>(*d, (double)m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
-                                                nbr, m->F, m->K, t_rows, t_cols, t_vals, n, 0, 0.0, 0.0, 1.0,
-                                                sqerr_scratch, 0);
+    const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
+    pred_tile_kernel<float, false><<<blocks, 64, 0, st>>>(*d, (double)m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
+                                                           nbr, m->F, m->K, t_rows, t_cols, t_vals, n, PreLookup{},
+                                                           0, 0, 0.0, 0.0, 1.0, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
     return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, false, st);
 }
@@ -140,9 +365,10 @@ extern "C" int culsh_predict(const CulshData *d, const CulshModel64 *m, const in
                              const int32_t *cols, int64_t n, double *out, void *stream) {
     if (n <= 0) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const int blocks = (int)min64((n + 127) / 128, (int64_t)num_sms() * 16);
-    sqerr_kernel<double><<<blocks, 128, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->nbr,
-                                                 m->F, m->K, rows, cols, nullptr, n, 0, 0.0, 0.0, 1.0, out, 1);
+    const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
+    pred_tile_kernel<double, false><<<blocks, 64, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
+                                                            m->nbr, m->F, m->K, rows, cols, nullptr, n, PreLookup{},
+                                                            1, 0, 0.0, 0.0, 1.0, out);
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }

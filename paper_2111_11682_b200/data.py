@@ -145,6 +145,22 @@ class SparseRatings:
                                  nat.to_dev(self.entry_values, np.float64))
         return self._dev_entries
 
+    def csc_entry_perm(self):
+        """Entry index of every CSC position (int64, device), or None when the entries
+        are already in CSC order.  The CSC is sorted by (col, row) and (row, col) pairs
+        are unique, so this is the argsort of col * M + row (cached)."""
+        if self.__dict__.get("_csc_perm_done"):
+            return self._csc_perm
+        t = nat.torch()
+        er, ec, _ = self.device_entries()
+        n = self._nnz
+        key = ec[:n].to(t.int64) * self.M + er[:n].to(t.int64)
+        perm = t.argsort(key)
+        ident = bool(t.equal(perm, t.arange(n, device=perm.device))) if n else True
+        self._csc_perm = None if ident else perm
+        self._csc_perm_done = True
+        return self._csc_perm
+
     def row_slice(self, i: int):
         lo, hi = self.row_ptr[i], self.row_ptr[i + 1]
         return self.row_cols[lo:hi], self.row_vals[lo:hi]
@@ -162,7 +178,13 @@ class SparseRatings:
 
     def baselines(self) -> BaselineStats:
         if self._baselines is None:
-            self._baselines = compute_baselines(self)
+            d = self._dev
+            if d is not None and getattr(d, "exact_baselines", False):
+                # integer-valued data: the device sums are exact, hence the reference's bytes
+                self._baselines = BaselineStats(d.mu, nat.to_host(d.base_b)[:self.M].copy(),
+                                                nat.to_host(d.base_bhat)[:self.N].copy())
+            else:
+                self._baselines = compute_baselines(self)
         return self._baselines
 
     def device(self) -> "DeviceRatings":
@@ -323,7 +345,13 @@ class DeviceRatings:
         self.row_cols = nat.to_dev(r.row_cols, np.int32)
         self.row_vals = nat.to_dev(r.row_vals, np.float64)
         self.csc2csr = nat.empty((max(r.nnz, 1),), "int32")
-        if r.nnz and with_baselines:
+        self.exact_baselines = False
+        if r.nnz and with_baselines and r._baselines is None and self.integer_valued():
+            # every sum exact: device statistics are the reference's bytes (data.py:289-309)
+            self.mu, self.base_b, self.base_bhat = device_baselines(
+                r.M, r.N, self.col_ptr, self.col_vals, self.row_ptr, self.row_vals, r.nnz)
+            self.exact_baselines = True
+        elif r.nnz and with_baselines:
             st = r.baselines()
             self.mu = st.mu
             self.base_b = nat.to_dev(st.b, np.float64)
@@ -358,6 +386,23 @@ class DeviceRatings:
         self.base_b = nat.to_dev(b, np.float64)
         self.base_bhat = nat.to_dev(b_hat, np.float64)
         self.struct = self._make_struct()
+
+
+def device_baselines(M: int, N: int, col_ptr, col_vals, row_ptr, row_vals, nnz: int):
+    """compute_baselines (data.py:289-309) from the two views' segment sums (exact,
+    hence bit-identical, for integer-valued ratings)."""
+    t = nat.torch()
+    cs = nat.empty((max(N, 1),), "float64")
+    rs = nat.empty((max(M, 1),), "float64")
+    nat.call("culsh_segment_sums", N, nat.ptr(col_ptr), nat.ptr(col_vals), nat.ptr(cs), nat.stream_ptr())
+    nat.call("culsh_segment_sums", M, nat.ptr(row_ptr), nat.ptr(row_vals), nat.ptr(rs), nat.stream_ptr())
+    cs, rs = cs[:N], rs[:M]
+    mu = float(cs.sum().item()) / max(nnz, 1)
+    cnt_c = (col_ptr[1:] - col_ptr[:-1]).to(t.float64)
+    rc = (row_ptr[1:] - row_ptr[:-1]).to(t.float64)
+    bb = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
+    bh = t.where(cnt_c > 0, cs / cnt_c.clamp(min=1) - mu, t.zeros_like(cs))
+    return mu, bb, bh
 
 
 def transform_ratings(triplets: Triplets, zero_floor: float | None = None,

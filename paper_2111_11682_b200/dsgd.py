@@ -286,10 +286,7 @@ def bench_main(args, metric, workload, rates):
     nbr = NeighborTable(N, K, nat.to_host(ent)[:N * K].reshape(N, K).astype(np.int32))
 
     cfg = TrainConfig(F=F, K=K, epochs=args.warmup + args.steps, seed=0, **rates)
-    stats = BaselineStats(dm.dev.mu, nat.to_host(dm.dev.base_b), nat.to_host(dm.dev.base_bhat))
-    params = init_params(M, N, F, K, nbr, stats, cfg)
-    tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev, params=params)
-    del params
+    tr = HogwildTrainer(None, nbr, cfg, dev=dm.dev)
     plan = RingPlan(D, M, N)
     d = dm.dev
     # per-(stage, row sub-block) work lists of the own column block: entry ranges from the

@@ -282,17 +282,52 @@ class NeighborSplit:
     implicit: np.ndarray
 
 
+_M64 = (1 << 64) - 1
+
+
+def pcg64_uniform_device(seed, skip: int, n: int, scale: float, dtype: str = "float64"):
+    """``np.random.default_rng(seed).uniform(0, scale, skip + n)[skip:]`` generated in
+    HBM (csrc/init.cu: the PCG64 stream jumped ahead per thread), bit for bit."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    out = nat.empty((max(int(n), 1),), dtype)
+    nat.call("culsh_pcg64_uniform", s >> 64, s & _M64, inc >> 64, inc & _M64, int(skip), int(n),
+             float(scale), int(dtype == "float32"), nat.ptr(out), nat.stream_ptr())
+    return out
+
+
+def _dev_bias(a, n: int, dtype: str):
+    """A device copy of a baseline vector (host array or device tensor)."""
+    t = nat.torch()
+    if isinstance(a, t.Tensor):
+        v = a[:n].to(getattr(t, dtype)).clone()
+    else:
+        v = nat.to_dev(np.asarray(a, np.float64)[:n]).to(getattr(t, dtype))
+    return v if n else nat.zeros((1,), dtype)
+
+
 def init_params(M: int, N: int, F: int, K: int, neighbors: NeighborTable | None,
-                baselines: BaselineStats, config: TrainConfig) -> ModelParams:
-    """Biases from the baselines, U/V uniform in [0, init_scale], W/C zero (factorization.py:196-211)."""
+                baselines: BaselineStats, config: TrainConfig, *, _dtype: str = "float64",
+                _dev_baselines=None) -> ModelParams:
+    """Biases from the baselines, U/V uniform in [0, init_scale], W/C zero
+    (factorization.py:196-211).  Generated in HBM: U and V are the reference's
+    ``default_rng(seed).uniform`` draws in the same order (U's M*F values, then V's),
+    bit for bit (csrc/init.cu); the host arrays are materialised on first read."""
     if neighbors is not None and (neighbors.N != N or neighbors.K != K):
         raise ValueError("neighbor table does not match N, K")
-    rng = np.random.default_rng(config.seed)
     scale = config.effective_init_scale
-    U = rng.uniform(0.0, scale, size=(M, F))
-    V = rng.uniform(0.0, scale, size=(N, F))
-    return ModelParams(mu=baselines.mu, b=baselines.b.copy(), b_hat=baselines.b_hat.copy(),
-                       U=U, V=V, W=np.zeros((N, K)), C=np.zeros((N, K)), neighbors=neighbors)
+    U = pcg64_uniform_device(config.seed, 0, M * F, scale, _dtype)
+    V = pcg64_uniform_device(config.seed, M * F, N * F, scale, _dtype)
+    bb, bh = (_dev_baselines if _dev_baselines is not None else (baselines.b, baselines.b_hat))
+    arrays = {"b": _dev_bias(bb, M, _dtype), "b_hat": _dev_bias(bh, N, _dtype), "U": U, "V": V,
+              "W": nat.zeros((max(N * K, 1),), _dtype), "C": nat.zeros((max(N * K, 1),), _dtype)}
+    nbr = neighbors.device_entries() if (neighbors is not None and K) else None
+    if _dtype == "float32":
+        from .hogwild import DeviceModel32
+        dm = DeviceModel32.from_arrays(arrays, baselines.mu, M, N, F, K, nbr)
+    else:
+        dm = DeviceModel64(arrays=arrays, mu=baselines.mu, M=M, N=N, F=F, K=K, nbr=nbr)
+    return ModelParams._from_device(baselines.mu, dm, M, N, neighbors)
 
 
 # ------------------------------------------------------------ device model ---
@@ -631,14 +666,15 @@ def train_full(ratings: SparseRatings, neighbors: NeighborTable | None,
         return params
     if mode != "exact":
         raise ValueError(f"unknown mode {mode!r}")
-    stats = ratings.baselines()
-    params = init_params(ratings.M, ratings.N, config.F, K, neighbors, stats, config)
-    if config.epochs == 0 or ratings.nnz == 0:
+    if ratings.nnz == 0:
+        return init_params(ratings.M, ratings.N, config.F, K, neighbors, ratings.baselines(), config)
+    dev = ratings.device()
+    params = init_params(ratings.M, ratings.N, config.F, K, neighbors, BaselineStats(dev.mu, None, None),
+                         config, _dev_baselines=(dev.base_b, dev.base_bhat))
+    if config.epochs == 0:
         return params
     _check_model_dims(config.F, K)
-    dev = ratings.device()
     dm = params._device(64)
-    params._own()
     sc = _Scratch(ratings.M, ratings.N)
     _plan_full(dev, sc, 0, ratings.N, 0, ratings.M)
     pre = _exact_lookups(dev, dm, 0, ratings.N, 0.25)   # once per fit, reused every epoch
@@ -670,26 +706,69 @@ def _test_device(testset: Triplets, ratings: SparseRatings):
     return dev
 
 
+def _train_lookup(dev, nbr, K: int):
+    """Per-(ratings, J^K) lookup cache for rmse over the training set: the explicit-
+    neighbour mask of every CSC entry and the CSC position of each explicit pair (built
+    once with the Hogwild stream's intersection kernel, ~0.5 GB at C3; cached on the
+    device ratings, keyed by the neighbour table's device copy)."""
+    key = (nbr.data_ptr(), K)
+    cache = dev.__dict__.setdefault("_train_lookup", {})
+    if key in cache and cache[key][0] is nbr:
+        return cache[key][1:]
+    cache.clear()
+    t = nat.torch()
+    MW = 1 if K <= 32 else 2
+    mask = nat.zeros((max(dev.nnz * MW, 1),), "int32")
+    nexpl = nat.zeros((max(dev.N, 1),), "int64")
+    nat.call("culsh_explicit_stream", ctypes.byref(dev.struct), float(dev.mu), nat.ptr(nbr), K,
+             nat.ptr(mask), nat.ptr(nexpl), None, None, nat.stream_ptr())
+    ng = (dev.nnz + 31) // 32
+    cnt = nat.zeros((max(ng, 1),), "int64")
+    nat.call("culsh_train_lookup", ctypes.byref(dev.struct), nat.ptr(nbr), K, nat.ptr(mask), nat.ptr(cnt),
+             None, None, nat.stream_ptr())
+    base = t.zeros(max(ng, 1), dtype=t.int64, device=cnt.device)
+    if ng > 1:
+        t.cumsum(cnt[:ng - 1], 0, out=base[1:ng])
+    total = int((base[ng - 1] + cnt[ng - 1]).item()) if ng else 0
+    pos = nat.empty((max(total, 1),), "int32")
+    nat.call("culsh_train_lookup", ctypes.byref(dev.struct), nat.ptr(nbr), K, nat.ptr(mask), None,
+             nat.ptr(base), nat.ptr(pos), nat.stream_ptr())
+    cache[key] = (nbr, mask, base, pos)
+    return mask, base, pos
+
+
 def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
          unscale: float | None = None, clamp: tuple[float, float] | None = None) -> float:
     """Root-mean-square error over held-out triplets (factorization.py:559-579).
 
-    Runs on the resident model (no host copy of the parameters) and, for the training
-    set or an immutable test set, on device-resident triplets."""
+    Runs on the resident model (no host copy of the parameters).  When ``testset`` is the
+    training set itself (``ratings.triplets()``, as the CLI's per-epoch callback passes
+    it, cli.py:204-210) the ratings' device views and a cached neighbour-lookup table are
+    used; other test sets are uploaded and their neighbour values binary-searched."""
     if len(testset) == 0:
         raise ValueError("empty test set")
     _check_model_dims(max(params.F, 1), params.K)
     dev = ratings.device()
     dm = params._device(64)
     n = len(testset)
-    tr, tc, tv = _test_device(testset, ratings)
     scratch = nat.empty((n + 256,), "float64")
     out = nat.empty((1,), "float64")
     lo, hi = clamp if clamp is not None else (0.0, 0.0)
+    us = 1.0 if unscale is None else float(unscale)
+    if getattr(testset, "_source", None) is ratings and n == dev.nnz:
+        K = dm.K
+        mask = base = pos = None
+        if K:
+            mask, base, pos = _train_lookup(dev, dm.nbr, K)
+        perm = ratings.csc_entry_perm()
+        nat.call("culsh_rmse_train", ctypes.byref(dev.struct), ctypes.byref(dm.struct), nat.ptr(mask),
+                 nat.ptr(base), nat.ptr(pos), nat.ptr(perm), int(clamp is not None), float(lo), float(hi),
+                 us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
+        return float(out.item())
+    tr, tc, tv = _test_device(testset, ratings)
     nat.call("culsh_rmse", ctypes.byref(dev.struct), ctypes.byref(dm.struct), nat.ptr(tr),
-             nat.ptr(tc), nat.ptr(tv), n, int(clamp is not None), float(lo), float(hi),
-             1.0 if unscale is None else float(unscale), nat.ptr(scratch), nat.ptr(out),
-             nat.stream_ptr())
+             nat.ptr(tc), nat.ptr(tv), n, int(clamp is not None), float(lo), float(hi), us,
+             nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
     return float(out.item())
 
 

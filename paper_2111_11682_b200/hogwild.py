@@ -19,6 +19,7 @@ import ctypes
 import numpy as np
 
 from . import _native as nat
+from .data import BaselineStats
 from .factorization import (ModelParams, TrainConfig, TrainingDivergedError, _rates_struct,
                             init_params)
 from .similarity import NeighborTable
@@ -47,6 +48,30 @@ class DeviceModel32:
         self.C = f32(C) if C.size else nat.zeros((1,), "float32")
         self.nbr = p.nbr_entries_device()
         self._restruct()
+
+    @classmethod
+    def from_arrays(cls, arrays: dict, mu: float, M: int, N: int, F: int, K: int, nbr=None):
+        self = cls.__new__(cls)
+        self.M, self.N, self.F, self.K, self.mu = M, N, F, K, float(mu)
+        for n, a in arrays.items():
+            setattr(self, _DEV_NAME[n], a)
+        self.nbr = nbr if nbr is not None else nat.zeros((1,), "int32")
+        self._restruct()
+        return self
+
+    @classmethod
+    def from_params(cls, p: ModelParams):
+        """fp32 copy of a ModelParams: converted on the device when p is device-backed
+        and current there, else from the host arrays."""
+        dev = p._dev
+        if dev is not None and all(s != "H" for s in p._state.values()):
+            t = nat.torch()
+            if isinstance(dev, cls):
+                arrays = {n: getattr(dev, _DEV_NAME[n]).clone() for n in _DEV_NAME}
+            else:
+                arrays = {n: getattr(dev, _DEV_NAME[n]).to(t.float32) for n in _DEV_NAME}
+            return cls.from_arrays(arrays, p.mu, p.M, p.N, p.F, p.K, p.nbr_entries_device())
+        return cls(p)
 
     def _restruct(self) -> None:
         self.struct = nat.CulshModel32(self.mu, nat.ptr(self.b), nat.ptr(self.bhat), nat.ptr(self.U),
@@ -124,10 +149,13 @@ class HogwildTrainer:
         # Hogwild staleness grows with (concurrently updated columns) / (rows): keep at
         # most one active column warp per `rows_per_warp` rows (no cap at C2/C3 scale).
         self.max_warps = max(32, d.M // 16) if max_warps is None else max_warps
-        if params is None:
-            stats = ratings.baselines()
-            params = init_params(d.M, d.N, config.F, K, neighbors, stats, config)
-        self.model = DeviceModel32(params)
+        if params is None:   # the reference's initial values, drawn directly as fp32 in HBM
+            stats = BaselineStats(d.mu, None, None)
+            params = init_params(d.M, d.N, config.F, K, neighbors, stats, config, _dtype="float32",
+                                 _dev_baselines=(d.base_b, d.base_bhat))
+            self.model = params._dev
+        else:
+            self.model = DeviceModel32.from_params(params)
         self.K = K
         MW = 1 if K <= 32 else 2
         self.MW = MW

@@ -76,7 +76,21 @@ def random_sparse_device(M: int, N: int, nnz_target: int, seed: int = 0) -> Devi
     del col
     dev = DeviceRatings.from_device(M, N, col_ptr, row.contiguous(), vals, row_ptr, row_cols,
                                     row_vals, mu, base_b, base_bhat)
+    dev.exact_baselines = True            # integer stars: every sum above is exact
+    dev._integer_valued = True
     return DeviceMatrix(dev, M, N, nnz)
+
+
+def random_sparse_ratings(M: int, N: int, nnz_target: int, seed: int = 0):
+    """The same matrix as a drop-in ``SparseRatings`` (device-built; entry order = column
+    major), for driving the public API at full scale without a host build."""
+    from .data import SparseRatings
+    t = nat.torch()
+    dm = random_sparse_device(M, N, nnz_target, seed)
+    d = dm.dev
+    cols = t.repeat_interleave(t.arange(N, device=d.col_ptr.device, dtype=t.int32),
+                               d.col_ptr[1:] - d.col_ptr[:-1])
+    return SparseRatings._from_device(d, (d.col_rows, cols, d.col_vals))
 
 
 def structured_triplets_device(M: int, N: int, nnz_target: int, seed: int = 0, rank: int = 6):

@@ -166,3 +166,72 @@ def test_absorb_increment_chain_matches_oracle(P, orc):
         for a, b in ((params.U, m.U), (params.V, m.V), (params.W, m.W), (params.C, m.C),
                      (params.b, m.b), (params.b_hat, m.bhat)):
             assert a.tobytes() == b.tobytes(), k
+
+
+@pytest.mark.parametrize("seed", [0, 7, (3, 0x0B1)])
+def test_pcg64_device_draws_equal_numpy(P, seed):
+    """init_params' U then V (and extend_params' stream) drawn in HBM == numpy's PCG64."""
+    from paper_2111_11682_b200 import _native as nat
+    from paper_2111_11682_b200.factorization import pcg64_uniform_device
+    n, skip, scale = 200_003, 12_345, 1.0 / np.sqrt(128)
+    ref = np.random.default_rng(seed).uniform(0.0, scale, skip + n)[skip:]
+    assert nat.to_host(pcg64_uniform_device(seed, skip, n, scale))[:n].tobytes() == ref.tobytes()
+    assert (nat.to_host(pcg64_uniform_device(seed, skip, n, scale, "float32"))[:n].tobytes()
+            == ref.astype(np.float32).tobytes())
+
+
+def test_init_params_equals_reference_draws(P):
+    r, *_ = _case(P, seed=3, M=700, N=300)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 6)
+    cfg = P.TrainConfig(F=24, K=6, epochs=0, seed=9)
+    p = P.init_params(r.M, r.N, 24, 6, tbl, r.baselines(), cfg)
+    rng = np.random.default_rng(9)
+    sc = 1.0 / np.sqrt(24)
+    assert p.U.tobytes() == rng.uniform(0.0, sc, (r.M, 24)).tobytes()
+    assert p.V.tobytes() == rng.uniform(0.0, sc, (r.N, 24)).tobytes()
+    st = r.baselines()
+    assert p.b.tobytes() == st.b.tobytes() and p.b_hat.tobytes() == st.b_hat.tobytes()
+    assert not p.W.any() and p.W.shape == (r.N, 6)
+    # the Hogwild trainer's fp32 model holds the same draws rounded to float
+    from paper_2111_11682_b200.hogwild import HogwildTrainer
+    tr = HogwildTrainer(r, tbl, P.TrainConfig(F=32, K=6, epochs=1, seed=9))
+    rng = np.random.default_rng(9)
+    sc = 1.0 / np.sqrt(32)
+    U = rng.uniform(0.0, sc, (r.M, 32))
+    assert tr.model.download("U").astype(np.float32).tobytes() == U.astype(np.float32).tobytes()
+
+
+@pytest.mark.parametrize("K", [0, 7, 40])
+def test_train_set_rmse_path_equals_generic(P, orc, K):
+    """rmse(params, ratings.triplets(), ratings) -- the cached-lookup training-set path --
+    equals the generic path on a copy of the same triplets and the oracle (sequential sum)."""
+    r, rows, cols, vals = _case(P, seed=12, M=400, N=90, dens=0.3)
+    if K:
+        tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=6, seed=1), K)
+    else:
+        tbl = None
+    p = P.train_full(r, tbl, P.TrainConfig(F=40, K=K, epochs=2, seed=2))
+    a = P.rmse(p, r.triplets(), r, clamp=(1.0, 5.0))
+    t = r.triplets()
+    b = P.rmse(p, P.Triplets(t.rows.copy(), t.cols.copy(), t.values.copy()), r, clamp=(1.0, 5.0))
+    d, mu = orc.build_csr(r.M, r.N, rows, cols, vals)
+    m = orc.Model(p.mu, p.b, p.b_hat, p.U, p.V, p.W, p.C,
+                  tbl.entries if K else np.zeros((r.N, 0), np.int32))
+    ref = orc.rmse(d, m, r.entry_rows, r.entry_cols, r.entry_values, clamp=(1.0, 5.0))
+    assert a == b == ref
+
+
+def test_train_set_rmse_large_tree_sum(P):
+    """Above 2^22 ratings both paths use the same fixed tree over entry order."""
+    rng = np.random.default_rng(3)
+    M, N = 60_000, 700
+    rows, cols = np.nonzero(rng.random((M, N)) < 0.11)
+    perm = rng.permutation(len(rows))          # entry order != CSC order
+    r = P.SparseRatings(M, N, rows[perm], cols[perm], rng.integers(1, 6, len(rows)).astype(float))
+    assert r.nnz > (1 << 22)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=6, seed=1), 16)
+    p = P.train_full(r, tbl, P.TrainConfig(F=32, K=16, epochs=1, seed=2), mode="hogwild")
+    t = r.triplets()
+    a = P.rmse(p, t, r)
+    b = P.rmse(p, P.Triplets(t.rows.copy(), t.cols.copy(), t.values.copy()), r)
+    assert a == b and np.isfinite(a)

@@ -1,0 +1,129 @@
+"""Cost of whole calls through the drop-in API at full scale (C3 / C4), one B200.
+
+  fit      train_full(mode="hogwild"), 20 epochs, device-resident ratings, parameters
+           returned to host numpy (U, V, W, C, b, b_hat read) -- the per-fit work the
+           epoch-only bench line excludes (init, explicit-neighbour stream, D2H);
+           also with the CLI's per-epoch callback (train + test RMSE, cli.py:204-210)
+  exact    train_full(mode="exact") per-epoch cost without / with the same callback
+  online   C4 through the public absorb_increment (not OnlineSession): 10 increments of
+           1 % new rows + 1 % new columns into a 90 % fit, seconds per increment
+
+  python tools/api_costs.py [fit] [exact] [online]
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2111_11682_b200 as P  # noqa: E402
+from paper_2111_11682_b200 import _native as nat, synth  # noqa: E402
+
+RATES = dict(alpha_b=0.02, alpha_b_hat=0.02, alpha_u=0.02, alpha_v=0.02, alpha_w=0.001, alpha_c=0.001,
+             lambda_b=0.01, lambda_b_hat=0.01, lambda_u=0.01, lambda_v=0.01, lambda_w=0.05, lambda_c=0.05,
+             beta=0.3)
+
+
+def sync_time(fn):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, time.perf_counter() - t0
+
+
+def materialise(p):
+    return sum(int(getattr(p, n).nbytes) for n in ("b", "b_hat", "U", "V", "W", "C"))
+
+
+def main():
+    what = set(sys.argv[1:]) or {"fit", "exact", "online"}
+    torch.cuda.set_device(0)
+    M, N, nnz, F, K, e = synth.SHAPES["c3"]
+    r = synth.random_sparse_ratings(M, N, nnz, seed=0)
+    out = {"config": "C3", "nnz": r.nnz}
+    lc = P.LshConfig(psi_exponent=e)
+    (tbl, _), out["simlsh_topk_api_s_first"] = sync_time(lambda: P.simlsh_topk(r, lc, K))
+    _, out["simlsh_topk_api_s"] = sync_time(lambda: P.simlsh_topk(r, lc, K))
+    # CLI-style test set: 1 % of the entries as host triplets (uploaded per rmse call)
+    rng = np.random.default_rng(1)
+    er, ec, ev = (nat.to_host(x) for x in r.device_entries())
+    sel = np.sort(rng.choice(r.nnz, r.nnz // 100, replace=False))
+    test = P.Triplets(er[sel].copy(), ec[sel].copy(), ev[sel].copy())
+    train_t = r.triplets()
+    curve = []
+
+    def cb(t, p):
+        curve.append((t, P.rmse(p, train_t, r), P.rmse(p, test, r)))
+
+    if "fit" in what:
+        cfg = P.TrainConfig(F=F, K=K, epochs=20, seed=0, **RATES)
+        P.train_full(r, tbl, P.TrainConfig(F=F, K=K, epochs=1, seed=0, **RATES), mode="hogwild")  # warm
+        for tag, kw in (("fit_s", {}), ("fit_with_rmse_callback_s", {"epoch_callback": cb})):
+            curve.clear()
+            def run():
+                p = P.train_full(r, tbl, cfg, mode="hogwild", **kw)
+                return p, materialise(p)
+            (p, nb), out[tag] = sync_time(run)
+            out["fit_d2h_bytes"] = nb
+        out["fit_rmse_curve_last"] = curve[-1] if curve else None
+        # component: one train RMSE and one test RMSE on the resident fp32 model
+        _, out["rmse_train_s"] = sync_time(lambda: P.rmse(p, train_t, r))
+        _, out["rmse_test_1pct_s"] = sync_time(lambda: P.rmse(p, test, r))
+    if "exact" in what:
+        for tag, kw in (("exact", {}), ("exact_with_rmse_callback", {"epoch_callback": cb})):
+            ts = {}
+            for ep in (1, 3):
+                cfg = P.TrainConfig(F=F, K=K, epochs=ep, seed=0, **RATES)
+                _, ts[ep] = sync_time(lambda: P.train_full(r, tbl, cfg, **kw))
+            out[tag + "_s_per_epoch"] = (ts[3] - ts[1]) / 2
+            out[tag + "_first_call_s"] = ts[1]
+        out["exact_callback_ratio"] = out["exact_with_rmse_callback_s_per_epoch"] / out["exact_s_per_epoch"]
+    if "online" in what:
+        out.update(online_public())
+    print(json.dumps(out), flush=True)
+
+
+def online_public():
+    """C4 as bench.py --config c4 builds it, absorbed through P.absorb_increment."""
+    t = torch
+    M, N, nnz_t, F, K, e = synth.SHAPES["c3"]
+    dm = synth.random_sparse_device(M, N, nnz_t, seed=0)
+    d = dm.dev
+    col = t.repeat_interleave(t.arange(N, device="cuda"), d.col_ptr[1:] - d.col_ptr[:-1]).to(t.int32)
+    row = d.col_rows
+    M0, N0 = int(M * 0.9), int(N * 0.9)
+    dM, dN = (M - M0) // 10, (N - N0) // 10
+    br = t.where(row >= M0, (row - M0) // dM, t.full_like(row, -1)).clamp(max=9)
+    bc = t.where(col >= N0, (col - N0) // dN, t.full_like(col, -1)).clamp(max=9)
+    bidx = t.maximum(br, bc)
+    init = bidx < 0
+    base = P.DeviceSparseRatings(M0, N0, row[init], col[init], d.col_vals[init])
+    ratings = P.SparseRatings._from_device(base.device(), (row[init].contiguous(), col[init].contiguous(),
+                                                           d.col_vals[init].contiguous()))
+    ratings.device().exact_baselines = True
+    lc = P.LshConfig(psi_exponent=e)
+    tbl, state = P.simlsh_topk(ratings, lc, K)
+    cfg = P.TrainConfig(F=F, K=K, epochs=1, seed=0, **RATES)
+    params = P.train_full(ratings, tbl, P.TrainConfig(F=F, K=K, epochs=3, seed=0, **RATES), mode="hogwild")
+    times = []
+    Mb, Nb = M0, N0
+    for b in range(10):
+        sel = bidx == b
+        nr_ = dM if b < 9 else M - (M0 + 9 * dM)
+        nc_ = dN if b < 9 else N - (N0 + 9 * dN)
+        batch = P.IncrementBatch(Mb, Nb, nr_, nc_, nat.to_host(row[sel]), nat.to_host(col[sel]),
+                                 nat.to_host(d.col_vals[sel]))
+        (params, state, ratings, tbl), dt = sync_time(
+            lambda: P.absorb_increment(params, state, ratings, batch, cfg))
+        times.append(dt)
+        Mb, Nb = Mb + nr_, Nb + nc_
+    return {"online_public_absorb_s_per_batch_median": float(np.median(times[1:])),
+            "online_public_absorb_s": times, "online_final_finite": params.all_finite()}
+
+
+if __name__ == "__main__":
+    main()
