@@ -395,6 +395,15 @@ int64_t culsh_split_holdout(const int32_t *entry_rows, const int32_t *entry_cols
 int culsh_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                         uint64_t skip, int64_t n, double scale, int fp32, void *out, void *stream);
 
+/* Synthetic workload (bench and tests only, not a reference seam): the entries
+ * [col_ptr[col_lo], col_ptr[col_hi]) of a random_sparse-shaped matrix
+ * (datasets.py:147-164 distribution: distinct uniform rows per column, stars 1..5),
+ * column j's rows a keyed permutation of [0, M) -- any column range is generated
+ * independently, identically on every rank.  rows/vals are relative to col_ptr[col_lo];
+ * rows are NOT sorted within a column. */
+int culsh_synth_columns(int64_t M, int64_t col_lo, int64_t col_hi, const int64_t *col_ptr, uint64_t seed,
+                        int32_t *rows, double *vals, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,7 @@ _SIGS = {
     "culsh_split_holdout": [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp],
     "culsh_train_lookup": [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp],
     "culsh_rmse_train": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f64, _f64, _f64, _vp, _vp, _vp],
+    "culsh_synth_columns": [_i64, _i64, _i64, _vp, _u64, _vp, _vp, _vp],
     "culsh_pcg64_uniform": [_u64, _u64, _u64, _u64, _u64, _i64, _f64, _i32, _vp, _vp],
     "culsh_pack16": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     "culsh_sgd_hogwild_epoch_packed16": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

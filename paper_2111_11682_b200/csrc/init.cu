@@ -78,3 +78,64 @@ extern "C" int culsh_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }
+
+// ---- synthetic workload generator (bench / tests; not a reference path) ------------
+// Column j of a random_sparse-shaped matrix (datasets.py:147-164: per-column counts,
+// distinct uniform rows, stars 1..5) without a host build and without duplicates: its
+// c_j rows are the first c_j values of a keyed pseudo-random permutation of [0, M)
+// (a 4-round Feistel network on 2^b >= M, cycle-walked into range), so any range of
+// columns -- one rank's column shard, or all columns filtered to a row shard -- is
+// generated independently and identically on every rank.
+namespace culsh {
+
+__device__ __forceinline__ uint64_t feistel(uint64_t x, int half, uint64_t k0, uint64_t k1, uint64_t k2,
+                                            uint64_t k3) {
+    const uint64_t mh = (1ull << half) - 1;
+    uint64_t L = x >> half, R = x & mh;
+    const uint64_t ks[4] = {k0, k1, k2, k3};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint64_t nl = R;
+        R = L ^ (splitmix64(R ^ ks[r]) & mh);
+        L = nl;
+    }
+    return (L << half) | R;
+}
+
+__global__ void synth_columns_kernel(int64_t M, int half, int64_t col_lo, int64_t col_hi, const int64_t *col_ptr,
+                                     uint64_t seed, int32_t *rows, double *vals) {
+    const int64_t base = col_ptr[col_lo];
+    const int64_t total = col_ptr[col_hi] - base;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = base + x;
+        int64_t lo = col_lo, hi = col_hi;   // column of entry e
+        while (hi - lo > 1) {
+            const int64_t m = (lo + hi) >> 1;
+            if (col_ptr[m] <= e) lo = m; else hi = m;
+        }
+        const int64_t j = lo, k = e - col_ptr[j];
+        const uint64_t kj = splitmix64(seed ^ ((uint64_t)(j + 1) * kGolden));
+        const uint64_t k0 = splitmix64(kj ^ 1), k1 = splitmix64(kj ^ 2), k2 = splitmix64(kj ^ 3),
+                       k3 = splitmix64(kj ^ 4);
+        uint64_t y = feistel((uint64_t)k, half, k0, k1, k2, k3);
+        while (y >= (uint64_t)M) y = feistel(y, half, k0, k1, k2, k3);
+        rows[x] = (int32_t)y;
+        vals[x] = (double)(1 + splitmix64(kj ^ (y * kMix1) ^ 0x5EED) % 5);
+    }
+}
+
+}  // namespace culsh
+
+extern "C" int culsh_synth_columns(int64_t M, int64_t col_lo, int64_t col_hi, const int64_t *col_ptr,
+                                   uint64_t seed, int32_t *rows, double *vals, void *stream) {
+    CULSH_REQUIRE(M >= 1 && M < (1LL << 31), "M out of range");
+    if (col_hi <= col_lo) return CULSH_OK;
+    int b = 2;
+    while ((1LL << b) < M) b += 2;
+    const int blocks = num_sms() * 8;
+    synth_columns_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(M, b / 2, col_lo, col_hi, col_ptr, seed, rows,
+                                                                   vals);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}

@@ -3,9 +3,11 @@
 The reference's ``random_sparse`` (datasets.py:147-164) draws a Binomial(M,
 density) count per column and that many distinct rows, with integer stars
 1..5.  Generating 100M ratings that way on the host takes ~100 s,
-so the bench builds the same distribution on the device: per-column Binomial
-counts (numpy, seeded), uniform rows drawn with replacement then de-duplicated
-(~0.6% duplicates at Netflix shape), stars uniform in 1..5.  Both index views
+so the bench builds the same distribution on the device: per-column counts (a
+seeded multinomial split of exactly the config's rating count), distinct rows per
+column from a keyed permutation of [0, M), stars 1..5 from a hash -- all a pure
+function of (seed, column), so every rank of a multi-GPU run generates exactly its
+own shard of the same matrix (csrc/init.cu culsh_synth_columns).  Both index views
 and the (integer-exact) baselines are built in HBM; this is setup, never timed.
 """
 
@@ -35,50 +37,86 @@ class DeviceMatrix:
     nnz: int
 
 
-def random_sparse_device(M: int, N: int, nnz_target: int, seed: int = 0) -> DeviceMatrix:
-    t = nat.torch()
-    d = nat.device()
+def column_counts(M: int, N: int, nnz_target: int, seed: int = 0) -> np.ndarray:
+    """Per-column rating counts: a multinomial split of exactly nnz_target ratings over
+    the N columns (each column ~Binomial(M, density) as in datasets.py:147-164, but the
+    total is the config's exact count), at least 1 and at most M per column."""
     rng = np.random.default_rng(seed)
-    per_col = np.maximum(rng.binomial(M, nnz_target / (M * N), size=N), 1).astype(np.int64)
-    total = int(per_col.sum())
-    g = t.Generator(device=d)
-    g.manual_seed(seed)
-    cols = t.repeat_interleave(t.arange(N, device=d, dtype=t.int64), t.from_numpy(per_col).to(d))
-    rows = t.randint(0, M, (total,), generator=g, device=d, dtype=t.int64)
-    key = cols * M + rows
-    key, _ = t.sort(key)
-    key = t.unique_consecutive(key)
-    del rows, cols
-    nnz = int(key.numel())
-    col = (key // M).to(t.int32)
-    row = (key % M).to(t.int32)
-    vals = t.randint(1, 6, (nnz,), generator=g, device=d, dtype=t.int64).to(t.float64)
+    c = rng.multinomial(nnz_target, np.full(N, 1.0 / N))
+    return np.clip(c, 1, M).astype(np.int64)
+
+
+def hashed_shard(M: int, N: int, nnz_target: int, seed: int = 0, cols: tuple | None = None,
+                 rows: tuple | None = None, chunk: int = 1 << 25):
+    """Device triplets (rows i32, cols i32, vals f64), sorted by (col, row), of the
+    synthetic matrix restricted to a column range and/or a row range; the same seed gives
+    the same matrix for any shard (csrc/init.cu culsh_synth_columns).  Also returns the
+    global column pointer (host int64)."""
+    t = nat.torch()
+    dev = nat.device()
+    cnt = column_counts(M, N, nnz_target, seed)
+    cp = np.zeros(N + 1, np.int64)
+    np.cumsum(cnt, out=cp[1:])
+    cp_d = t.from_numpy(cp).to(dev)
+    c0, c1 = cols if cols is not None else (0, N)
+    parts_r, parts_c, parts_v = [], [], []
+    j = c0
+    while j < c1:   # column chunks of ~chunk entries (bounded scratch)
+        j2 = int(np.searchsorted(cp, cp[j] + chunk, side="right")) - 1
+        j2 = min(max(j2, j + 1), c1)
+        n = int(cp[j2] - cp[j])
+        r = nat.empty((max(n, 1),), "int32")
+        v = nat.empty((max(n, 1),), "float64")
+        nat.call("culsh_synth_columns", M, j, j2, nat.ptr(cp_d), int(seed) & ((1 << 64) - 1), nat.ptr(r),
+                 nat.ptr(v), nat.stream_ptr())
+        r, v = r[:n], v[:n]
+        c = t.repeat_interleave(t.arange(j, j2, device=dev, dtype=t.int32), cp_d[j + 1:j2 + 1] - cp_d[j:j2])
+        if rows is not None:
+            keep = (r >= rows[0]) & (r < rows[1])
+            r, c, v = r[keep], c[keep], v[keep]
+        key = c.to(t.int64) * M + r.to(t.int64)
+        key, order = t.sort(key)
+        parts_r.append(r[order])
+        parts_c.append(c[order])
+        parts_v.append(v[order])
+        j = j2
+    if not parts_r:
+        z = t.zeros(0, dtype=t.int32, device=dev)
+        return z, z.clone(), t.zeros(0, dtype=t.float64, device=dev), cp
+    return t.cat(parts_r), t.cat(parts_c), t.cat(parts_v), cp
+
+
+def device_ratings_from_sorted(M: int, N: int, rows, cols, vals, baselines: bool = True):
+    """DeviceRatings from device triplets already sorted by (col, row): CSC directly, CSR by
+    a device sort; baselines from the two views' exact segment sums (integer stars)."""
+    from .data import device_baselines
+    t = nat.torch()
+    d = rows.device
+    nnz = int(rows.numel())
     col_ptr = t.zeros(N + 1, dtype=t.int64, device=d)
-    col_ptr[1:] = t.cumsum(t.bincount(col, minlength=N), 0)
-    # CSR: stable order by (row, col)
-    rkey = row.to(t.int64) * N + col.to(t.int64)
-    order = t.argsort(rkey, stable=True)
-    del rkey
-    row_cols = col[order].contiguous()
+    col_ptr[1:] = t.cumsum(t.bincount(cols, minlength=N), 0)
+    order = t.argsort(rows.to(t.int64) * N + cols.to(t.int64))
+    row_cols = cols[order].contiguous()
     row_vals = vals[order].contiguous()
     del order
     row_ptr = t.zeros(M + 1, dtype=t.int64, device=d)
-    row_cnt = t.bincount(row, minlength=M)
-    row_ptr[1:] = t.cumsum(row_cnt, 0)
-    # baselines (integer data: every summation order is exact)
-    mu = float(vals.sum().item()) / nnz
-    rs = t.zeros(M, dtype=t.float64, device=d).index_add_(0, row.to(t.int64), vals)
-    cs = t.zeros(N, dtype=t.float64, device=d).index_add_(0, col.to(t.int64), vals)
-    cc = (col_ptr[1:] - col_ptr[:-1]).to(t.float64)
-    rc = row_cnt.to(t.float64)
-    base_b = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
-    base_bhat = t.where(cc > 0, cs / cc.clamp(min=1) - mu, t.zeros_like(cs))
-    del col
-    dev = DeviceRatings.from_device(M, N, col_ptr, row.contiguous(), vals, row_ptr, row_cols,
-                                    row_vals, mu, base_b, base_bhat)
-    dev.exact_baselines = True            # integer stars: every sum above is exact
+    row_ptr[1:] = t.cumsum(t.bincount(rows, minlength=M), 0)
+    if baselines and nnz:
+        mu, bb, bh = device_baselines(M, N, col_ptr, vals, row_ptr, row_vals, nnz)
+    else:
+        mu, bb, bh = 0.0, t.zeros(M, dtype=t.float64, device=d), t.zeros(N, dtype=t.float64, device=d)
+    dev = DeviceRatings.from_device(M, N, col_ptr, rows.contiguous(), vals.contiguous(), row_ptr, row_cols,
+                                    row_vals, mu, bb, bh)
+    dev.exact_baselines = bool(baselines)
     dev._integer_valued = True
-    return DeviceMatrix(dev, M, N, nnz)
+    return dev
+
+
+def random_sparse_device(M: int, N: int, nnz_target: int, seed: int = 0) -> DeviceMatrix:
+    """The whole synthetic matrix in HBM (hashed_shard over all columns)."""
+    rows, cols, vals, _ = hashed_shard(M, N, nnz_target, seed)
+    dev = device_ratings_from_sorted(M, N, rows, cols, vals)
+    return DeviceMatrix(dev, M, N, dev.nnz)
 
 
 def random_sparse_ratings(M: int, N: int, nnz_target: int, seed: int = 0):

@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, out_q, parts=1):
+def _worker(rank, world, port, case, out_q, parts=1, side="rows"):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -38,22 +38,24 @@ def _worker(rank, world, port, case, out_q, parts=1):
     d, mu = orc.build_csr(int(z[pre + "M"]), int(z[pre + "N"]), z[pre + "rows"], z[pre + "cols"],
                           z[pre + "vals"])
     m = orc.init_model(d.M, d.N, F, K, z[pre + "nbr"], mu, d.base_b, d.base_bhat, seed)
-    plan = RingPlan(world, d.M, d.N)
+    plan = RingPlan(world, d.M, d.N, side)
     _, col_bounds, bp = orc.partition(d, world)
     assert np.array_equal(col_bounds, plan.col_bounds)
     bp_fine = orc.partition(d, world * parts)[2]   # row sub-blocks of the pipelined shift
     U, b = torch.from_numpy(m.U), torch.from_numpy(m.b)
+    moving = [U, b] if side == "rows" else [torch.from_numpy(x) for x in (m.V, m.W, m.C, m.bhat)]
     for t in range(epochs):
         rates = orc.make_rates(tuple(a / (1.0 + 0.3 * t ** 1.5)
                                      for a in (0.035, 0.035, 0.035, 0.035, 0.002, 0.002)), REGS)
-        cs = plan.cols(rank)
 
-        def stage(s, rb, h=None):
-            if h is None:
-                assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb, bp) == 0
-            else:
+        def stage(s, rb, cb, h):
+            if side == "rows":
+                cs = plan.cols(cb)
                 assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb * parts + h, bp_fine) == 0
-        run_epoch(plan, rank, stage, [U, b], parts=parts)
+            else:
+                cs = plan.sub_cols(cb, h, parts)
+                assert orc.stage_pass(d, m, rates, cs.start, cs.stop, rb, bp) == 0
+        run_epoch(plan, rank, stage, moving, parts=parts)
     # after D stages per epoch every rank holds row block `rank` again
     allgather_blocks(U, plan.row_bounds, rank, world)
     allgather_blocks(b, plan.row_bounds, rank, world)
@@ -65,17 +67,19 @@ def _worker(rank, world, port, case, out_q, parts=1):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("side", ["rows", "cols"])
 @pytest.mark.parametrize("world,case,parts", [(2, 0, 1), (3, 0, 1), (2, 1, 1), (3, 3, 1), (2, 0, 2), (3, 3, 3)])
-def test_dsgd_ring_equals_reference_parallel_train(world, case, parts):
-    """parts > 1: the pipelined ring (row sub-blocks shifted while the next one trains)
-    gives the same bytes as parallel_train(D)."""
+def test_dsgd_ring_equals_reference_parallel_train(world, case, parts, side):
+    """Both rotation sides (u/b row blocks or v/w/c/b_hat column blocks travel) give the
+    same bytes as the reference's parallel_train(D); parts > 1: the pipelined ring
+    (sub-blocks shifted while the next one trains) too."""
     z = load_golden("sgd_small.npz")
     if world not in (2, 3):
         pytest.skip()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, parts)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, parts, side)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=120)
@@ -88,20 +92,30 @@ def test_dsgd_ring_equals_reference_parallel_train(world, case, parts):
         assert res[k] == z[pre + n].tobytes(), (world, case, n)
 
 
-def test_ring_plan_covers_every_block():
+@pytest.mark.parametrize("side", ["rows", "cols"])
+def test_ring_plan_covers_every_block(side):
     from paper_2111_11682_b200.dsgd import RingPlan
     for D in (1, 2, 3, 8):
-        p = RingPlan(D, 1000, 700)
+        p = RingPlan(D, 1000, 700, side)
         seen = set()
         for s in range(D):
-            rbs = [p.row_block(r, s) for r in range(D)]
-            assert sorted(rbs) == list(range(D))
-            seen |= {(rb, r) for r, rb in enumerate(rbs)}
+            blocks = [p.stage_block(r, s) for r in range(D)]
+            # the stage's pairs are parallel_train's: worker w takes ((w + s) % D, w)
+            assert sorted(blocks) == sorted(((w + s) % D, w) for w in range(D))
+            seen |= set(blocks)
             for r in range(D):   # the block rank r trains next is the one its recv peer trained now
-                assert p.row_block(r, s + 1) == p.row_block(p.recv_peer(r), s)
+                assert p.moving_block(r, s + 1) == p.moving_block(p.recv_peer(r), s)
+                assert p.send_peer(p.recv_peer(r)) == r
         assert len(seen) == D * D
-        for parts in (1, 2, 3):   # sub-blocks tile each row block
-            for rb in range(D):
-                sl = [p.sub_rows(rb, h, parts) for h in range(parts)]
-                assert sl[0].start == p.rows(rb).start and sl[-1].stop == p.rows(rb).stop
-                assert all(sl[h].stop == sl[h + 1].start for h in range(parts - 1))
+        for parts in (1, 2, 3):   # sub-blocks tile each block
+            for blk in range(D):
+                for sub, whole in ((p.sub_rows, p.rows), (p.sub_cols, p.cols)):
+                    sl = [sub(blk, h, parts) for h in range(parts)]
+                    assert sl[0].start == whole(blk).start and sl[-1].stop == whole(blk).stop
+                    assert all(sl[h].stop == sl[h + 1].start for h in range(parts - 1))
+
+
+def test_choose_side():
+    from paper_2111_11682_b200.dsgd import choose_side
+    assert choose_side(480_189, 17_770, 128, 32) == "cols"      # Netflix: move v/w/c (1.7 MB / stage)
+    assert choose_side(1_000, 600_000, 32, 64) == "rows"
