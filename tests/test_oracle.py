@@ -162,6 +162,26 @@ class TestSgdGolden:
         assert orc.rmse(d, md, tr, tc, tv) == float(z["sgd_D4_rmse_test"])
 
 
+    def test_c1_20_epoch_curve(self, orc):
+        """The oracle reproduces the reference's whole 20-epoch learning curve (test and
+        train RMSE after every epoch, c1_ref20.npz written by the reference)."""
+        z = load_golden("c1.npz")
+        ref = load_golden("c1_ref20.npz")
+        assert ref["entries16"].tobytes() == z["lsh_entries16"].tobytes()
+        d, mu = orc.build_csr(int(z["train_M"]), int(z["train_N"]), z["train_rows"], z["train_cols"],
+                              z["train_vals"])
+        tr, tc, tv = (z["test_rows"].astype(np.int32), z["test_cols"].astype(np.int32),
+                      z["test_vals"].astype(np.float64))
+        rr, rc, rv = (z["train_rows"].astype(np.int32), z["train_cols"].astype(np.int32),
+                      z["train_vals"].astype(np.float64))
+        seen = []
+        orc.train_full(d, mu, ref["entries16"], 32, 16, 20, 0, _rates(), REGS,
+                       callback=lambda t, mm: seen.append((orc.rmse(d, mm, tr, tc, tv),
+                                                           orc.rmse(d, mm, rr, rc, rv))))
+        np.testing.assert_array_equal([a for a, _ in seen], ref["F32_rmse_test"])
+        np.testing.assert_array_equal([b for _, b in seen], ref["F32_rmse_train"])
+
+
 class TestOnlineGolden:
     def test_online_small(self, orc):
         z = load_golden("online_small.npz")
