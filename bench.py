@@ -131,7 +131,8 @@ def cpu_baseline(shape, F, K, cfg_lsh, budget_s=20.0, threads=None):
             "sample": (f"host-generated {Ms} x {N} sample (2 % of the rows at the workload's density, "
                        f"{len(rows)} ratings): oracle simLSH top-K in {lsh_sample_s:.2f}s, then "
                        f"parallel_epoch (reference parallel_train, D={D}) x {n_ep} in {sgd_s:.2f}s"),
-            "lsh_build_s_extrapolated": lsh_sample_s * nnz / max(len(rows), 1)}
+            "lsh_build_s_extrapolated": lsh_sample_s * nnz / max(len(rows), 1),
+            "calibration": cpu_calibration()}
 
 
 def run_reference(args):
@@ -153,11 +154,36 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD[args.config]},
+            "config": workload_config(args.config),
+            "sample": cb["sample"],
             "cpu_baseline": {**cb, "value": v},
             "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_config(name):
+    """The `config` both arms print (identical keys and values): the workload named by
+    BASELINE.json's configs.  Implementation details go under `impl_config`; the CPU
+    arm's bounded sample of this workload is stated in `sample` / `cpu_baseline.sample`."""
+    from paper_2111_11682_b200.synth import SHAPES
+    M, N, nnz, F, K, e = SHAPES[name]
+    return {"workload": WORKLOAD[name], "M": M, "N": N, "nnz": nnz, "F": F, "K": K,
+            "lsh": {"G": 8, "p": 3, "q": 100, "psi_exponent": e},
+            "rates": "Netflix Table 6 (alpha 0.02/0.001, lambda 0.01/0.05, beta 0.3)"}
+
+
+def cpu_calibration():
+    """profiles/r2_cpu_calibration.json (tools/calibrate_cpu_baseline.py, build container):
+    the port's time over the unmodified reference's on the same sample and threads."""
+    path = os.path.join(ROOT, "profiles", "r2_cpu_calibration.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        c = json.load(fh)
+    return {"simlsh_port_over_reference_time": c["simlsh_topk_s"]["port_over_reference_time"],
+            "dsgd_port_over_reference_time": c["dsgd_epoch_s"]["port_over_reference_time"],
+            "host_threads": c["host_threads"], "source": "profiles/r2_cpu_calibration.json"}
 
 
 WORKLOAD = {
@@ -255,7 +281,7 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_2111_11682_b200 import dsgd
-        return dsgd.bench_main(args, METRIC, WORKLOAD, NETFLIX_RATES)
+        return dsgd.bench_main(args, METRIC, workload_config(args.config), NETFLIX_RATES)
 
     torch.cuda.set_device(0)
     M, N, nnz_t, F, K, e = synth.SHAPES[args.config]
@@ -342,10 +368,11 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (random_sparse distribution generated in HBM, integer stars 1-5)",
-        "config": {"workload": WORKLOAD[args.config], "M": M, "N": N, "nnz": nnz, "F": F, "K": K,
-                   "mode": "hogwild fp32, warp per column", "stream": "packed" if tr.packed is not None else "wide",
-                   "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic),
-                   "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
+        "config": workload_config(args.config),
+        "impl_config": {"nnz_generated": nnz, "mode": "hogwild fp32, warp per column",
+                        "stream": "packed" if tr.packed is not None else "wide",
+                        "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic),
+                        "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
         "lsh_build_s": lsh_s, "lsh_build_runs_s": lsh_runs, "lsh_candidates": ncand,
         # the simLSH build's work is nnz*p*q*G signed accumulations
         "lsh_accumulations_per_s": float(nnz) * lcfg.p * lcfg.q * lcfg.G / lsh_s,

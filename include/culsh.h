@@ -358,10 +358,20 @@ int culsh_gsm_merge_topk(const int64_t *col_ptr, const int32_t *col_rows, const 
  * caller): 1 / r / r*r at (j, i - row_lo) for every rating with row_lo <= i <
  * row_hi (the caller accumulates the products over row passes).  *status |= 1 if a
  * value is not an integer in [-11, 11] (use the merge route then).  Step 2 is
- * four int8 GEMMs with int32 accumulation (cuBLASLt). */
+ * culsh_gsm_stats_tc. */
 int culsh_gsm_densify_rows(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
                            int64_t N, int64_t row_lo, int64_t row_hi, int64_t ld, int8_t *xt,
                            int8_t *rt, int8_t *qt, int *status, void *stream);
+
+/* Count route, step 2: the four statistic products of the (3, ld, w) int8 panel
+ * array (X rows 0..ld-1, R rows ld..2ld-1, Q rows 2ld..3ld-1, row stride w bytes):
+ * g_xx (+)= X X', g_rx (+)= R X', g_rr (+)= R R', g_qx (+)= Q X' (ld x ld int32,
+ * row stride ld; accumulate != 0 adds to the existing values, for row passes).  One
+ * sm_100a kernel: TMA-fed tcgen05.mma kind::i8 with TMEM accumulators, exact int32
+ * (similarity.py:57-90 statistics of every pair at once).  ld % 128 == 0,
+ * w % 64 == 0, panels 16-byte aligned. */
+int culsh_gsm_stats_tc(const int8_t *panels, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
+                       int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, void *stream);
 
 /* Count route, step 3 (after the int32 products g_xx = X'X, g_rx = R'X,
  * g_rr = R'R, g_qx = Q'X, each N x N with row stride ld): shrunk Pearson of every

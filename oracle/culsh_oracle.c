@@ -91,19 +91,22 @@ typedef struct {
     const uint8_t *bits; int64_t W; int e; double *acc;
 } acc_ctx_t;
 
+/* a - ps == a + (-ps) in IEEE arithmetic, so the select form below is the reference's
+ * if/else bit for bit; written branch-free it vectorises (numba's LLVM build of the
+ * reference does the same), and target_clones picks AVX-512 / AVX2 on the host that
+ * runs it (the .so is built in one container and run on another box). */
+__attribute__((target_clones("avx512f", "avx2", "default")))
 static void acc_body(int64_t jlo, int64_t jhi, void *p) {
     const acc_ctx_t *c = (const acc_ctx_t *)p;
     const int64_t W = c->W;
     for (int64_t j = jlo; j < jhi; ++j) {
-        double *a = c->acc + j * W;
+        double *restrict a = c->acc + j * W;
         for (int64_t w = 0; w < W; ++w) a[w] = 0.0;
         for (int64_t idx = c->col_ptr[j]; idx < c->col_ptr[j + 1]; ++idx) {
             const int64_t i = c->col_rows[idx];
-            const double ps = psi_of(c->col_vals[idx], c->e);
-            const uint8_t *b = c->bits + i * W;
-            for (int64_t w = 0; w < W; ++w) {
-                if (b[w] != 0) a[w] += ps; else a[w] -= ps;
-            }
+            const double ps = psi_of(c->col_vals[idx], c->e), ng = -ps;
+            const uint8_t *restrict b = c->bits + i * W;
+            for (int64_t w = 0; w < W; ++w) a[w] += b[w] != 0 ? ps : ng;
         }
     }
 }
@@ -134,25 +137,44 @@ void orc_accumulate_into(double *acc, const int64_t *col_ptr, const int32_t *col
 }
 
 /* lsh.py:182-183 _threshold: sig = acc >= 0 */
-void orc_threshold(const double *acc, int64_t n, uint8_t *sig) {
-    for (int64_t k = 0; k < n; ++k) sig[k] = acc[k] >= 0.0 ? 1 : 0;
+/* Host threads for the stages below (set from Python; every stage's output is
+ * independent of the thread count). */
+static int g_threads = 1;
+void orc_set_threads(int n) { g_threads = n > 0 ? n : 1; }
+
+typedef struct { const double *acc; uint8_t *sig; } thr_ctx_t;
+static void thr_body(int64_t lo, int64_t hi, void *p) {
+    const thr_ctx_t *c = (const thr_ctx_t *)p;
+    for (int64_t k = lo; k < hi; ++k) c->sig[k] = c->acc[k] >= 0.0 ? 1 : 0;
 }
 
-/* lsh.py:246-260 _pack_group_keys + lsh.py:417-423 _state_group_keys:
- * keys[g, j] bit (m*G + t) set iff sig[j, g, m, t] */
-void orc_pack_group_keys(const uint8_t *sig, int64_t N, int q, int p, int G, uint64_t *keys) {
-    for (int g = 0; g < q; ++g)
-        for (int64_t j = 0; j < N; ++j) {
+void orc_threshold(const double *acc, int64_t n, uint8_t *sig) {
+    thr_ctx_t c = {acc, sig};
+    parallel_for(n, 1 << 20, g_threads, thr_body, &c);
+}
+
+/* lsh.py:246-260 _pack_group_keys over all groups (lsh.py:417-423): bit m*G+t of
+ * group g's key is sig[j,g,m,t] */
+typedef struct { const uint8_t *sig; int64_t N; int q, p, G; uint64_t *keys; } pack_ctx_t;
+static void pack_body(int64_t jlo, int64_t jhi, void *pp) {
+    const pack_ctx_t *c = (const pack_ctx_t *)pp;
+    for (int64_t j = jlo; j < jhi; ++j)
+        for (int g = 0; g < c->q; ++g) {
             uint64_t k = 0;
             unsigned shift = 0;
-            const uint8_t *s = sig + ((j * q + g) * (int64_t)p) * G;
-            for (int m = 0; m < p; ++m)
-                for (int t = 0; t < G; ++t) {
-                    if (s[m * G + t] != 0) k |= 1ULL << shift;
+            const uint8_t *s = c->sig + ((j * c->q + g) * (int64_t)c->p) * c->G;
+            for (int m = 0; m < c->p; ++m)
+                for (int t = 0; t < c->G; ++t) {
+                    if (s[m * c->G + t] != 0) k |= 1ULL << shift;
                     shift += 1;
                 }
-            keys[(int64_t)g * N + j] = k;
+            c->keys[(int64_t)g * c->N + j] = k;
         }
+}
+
+void orc_pack_group_keys(const uint8_t *sig, int64_t N, int q, int p, int G, uint64_t *keys) {
+    pack_ctx_t c = {sig, N, q, p, G, keys};
+    parallel_for(N, 256, g_threads, pack_body, &c);
 }
 
 /* ---- bucketing: lsh.py:263-287 _group_runs (stable argsort) ---- */
@@ -237,16 +259,45 @@ static void fine_topk_one(int32_t *cand, int64_t ncand, int64_t j, int K, uint64
 /* lsh.py:401-414 _topk_from_group_keys, generalised with online.py:152-184
  * (j_base/n_cols target subset).  keys is (q, N_total).  entries is (n_cols, K).
  * Returns the total candidate count (sum over targets of bucket-1 over groups). */
+typedef struct { const uint64_t *keys; int64_t N; int64_t *order, *rs, *re; } runs_ctx_t;
+static void runs_body(int64_t glo, int64_t ghi, void *pp) {
+    const runs_ctx_t *c = (const runs_ctx_t *)pp;
+    kj_t *tmp = (kj_t *)malloc(sizeof(kj_t) * (size_t)(c->N > 0 ? c->N : 1));
+    for (int64_t g = glo; g < ghi; ++g)
+        group_runs(c->keys + g * c->N, c->N, c->order + g * c->N, c->rs + g * c->N, c->re + g * c->N, tmp);
+    free(tmp);
+}
+
+typedef struct {
+    const int64_t *order, *rs, *re, *offsets; int q; int64_t N_total, j_base; int K; uint64_t seed;
+    int32_t *cand, *entries;
+} fine_ctx_t;
+static void fine_body(int64_t lo, int64_t hi, void *pp) {
+    const fine_ctx_t *c = (const fine_ctx_t *)pp;
+    double *best_cnt = (double *)malloc(sizeof(double) * (size_t)(c->K > 0 ? c->K : 1));
+    int32_t *best_idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(c->K > 0 ? c->K : 1));
+    for (int64_t jj = lo; jj < hi; ++jj) {
+        const int64_t j = c->j_base + jj;
+        int64_t f = c->offsets[jj];
+        /* lsh.py:308-328 _fill_candidates: groups in order, bucket mates in sorted order */
+        for (int g = 0; g < c->q; ++g) {
+            const int64_t *og = c->order + (int64_t)g * c->N_total;
+            for (int64_t pos = c->rs[(int64_t)g * c->N_total + j]; pos < c->re[(int64_t)g * c->N_total + j]; ++pos)
+                if (og[pos] != j) c->cand[f++] = (int32_t)og[pos];
+        }
+        fine_topk_one(c->cand + c->offsets[jj], c->offsets[jj + 1] - c->offsets[jj], j, c->K, c->seed,
+                      c->N_total, best_cnt, best_idx, c->entries + jj * (int64_t)c->K);
+    }
+    free(best_cnt); free(best_idx);
+}
+
 int64_t orc_topk_from_group_keys(const uint64_t *keys, int q, int64_t N_total, int64_t j_base,
                                  int64_t n_cols, int K, uint64_t seed, int32_t *entries) {
     int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)q * (size_t)N_total);
     int64_t *rs = (int64_t *)malloc(sizeof(int64_t) * (size_t)q * (size_t)N_total);
     int64_t *re = (int64_t *)malloc(sizeof(int64_t) * (size_t)q * (size_t)N_total);
-    kj_t *tmp = (kj_t *)malloc(sizeof(kj_t) * (size_t)(N_total > 0 ? N_total : 1));
-    for (int g = 0; g < q; ++g)
-        group_runs(keys + (int64_t)g * N_total, N_total, order + (int64_t)g * N_total,
-                   rs + (int64_t)g * N_total, re + (int64_t)g * N_total, tmp);
-    free(tmp);
+    runs_ctx_t rc = {keys, N_total, order, rs, re};
+    parallel_for(q, 1, g_threads, runs_body, &rc);
     /* lsh.py:308-328 _fill_candidates: offsets = prefix sum of sum_g (bucket - 1) */
     int64_t *offsets = (int64_t *)calloc((size_t)n_cols + 1, sizeof(int64_t));
     for (int64_t jj = 0; jj < n_cols; ++jj) {
@@ -259,23 +310,9 @@ int64_t orc_topk_from_group_keys(const uint64_t *keys, int q, int64_t N_total, i
     }
     int64_t total = offsets[n_cols];
     int32_t *cand = (int32_t *)malloc(sizeof(int32_t) * (size_t)(total > 0 ? total : 1));
-    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_cols > 0 ? n_cols : 1));
-    for (int64_t jj = 0; jj < n_cols; ++jj) fill[jj] = offsets[jj];
-    for (int g = 0; g < q; ++g)
-        for (int64_t jj = 0; jj < n_cols; ++jj) {
-            int64_t j = j_base + jj;
-            const int64_t *og = order + (int64_t)g * N_total;
-            for (int64_t pos = rs[(int64_t)g * N_total + j]; pos < re[(int64_t)g * N_total + j]; ++pos) {
-                int64_t o = og[pos];
-                if (o != j) cand[fill[jj]++] = (int32_t)o;
-            }
-        }
-    double *best_cnt = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
-    int32_t *best_idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(K > 0 ? K : 1));
-    for (int64_t jj = 0; jj < n_cols; ++jj)
-        fine_topk_one(cand + offsets[jj], offsets[jj + 1] - offsets[jj], j_base + jj, K, seed,
-                      N_total, best_cnt, best_idx, entries + jj * (int64_t)K);
-    free(best_cnt); free(best_idx); free(cand); free(fill); free(offsets);
+    fine_ctx_t fc = {order, rs, re, offsets, q, N_total, j_base, K, seed, cand, entries};
+    parallel_for(n_cols, 64, g_threads, fine_body, &fc);
+    free(cand); free(offsets);
     free(order); free(rs); free(re);
     return total;
 }

@@ -51,6 +51,7 @@ def lib():
         for name in ("orc_full_pass_block", "orc_stage_pass", "orc_parallel_epoch",
                      "orc_online_row_pass", "orc_online_col_pass"):
             getattr(_lib, name).restype = ctypes.c_int
+        _lib.orc_set_threads(os.cpu_count() or 1)   # hash-stage threads; outputs do not depend on it
     return _lib
 
 
@@ -143,6 +144,8 @@ class HashResult:
 
 def simlsh_topk(col_ptr, col_rows, col_vals, M, G, p, q, e, seed, K, nthreads=None) -> HashResult:
     """lsh.py:426-438 composed from the stage restatements."""
+    if nthreads:
+        lib().orc_set_threads(int(nthreads))
     bits = assign_bits(seed, q, p, M, G)
     acc = accumulate_all(col_ptr, col_rows, col_vals, bits, e, nthreads)
     sig = threshold(acc)

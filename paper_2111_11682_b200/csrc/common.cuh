@@ -1,5 +1,6 @@
 // Shared device helpers for the CULSH-MF sm_100a kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -65,15 +66,24 @@ __device__ __forceinline__ int ld_volatile(const int *p) {
     return *(const volatile int *)p;
 }
 
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+// True the first time it is called for the current device (per-device bit, thread-safe):
+// for per-device state such as cudaFuncSetAttribute or the mempool threshold, which must be
+// set again after a set_device to another GPU of the same process.
+inline bool first_on_device(std::atomic<uint64_t> &done) {
+    const uint64_t bit = 1ull << (current_device() & 63);
+    return (done.fetch_or(bit) & bit) == 0;
+}
+
 inline int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
+    return n > 0 ? n : 148;
 }
 
 // Stream-ordered scratch (cudaMallocAsync) comes from the device's default pool; keep
@@ -81,16 +91,13 @@ inline int num_sms() {
 // synchronisation (release threshold 0 by default), which would re-map memory on each
 // call of a frequently called entry point.
 inline void keep_pool_memory() {
-    static bool done = false;
-    if (!done) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    static std::atomic<uint64_t> done{0};
+    if (first_on_device(done)) {
         cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
             uint64_t thr = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        done = true;
     }
 }
 

@@ -1,0 +1,326 @@
+// GSM count route, step 2 (reference similarity.py:57-90, 164-185):
+// the four co-rating statistic products of the dense int8 column panels
+//
+//     g_xx += X X',  g_rx += R X',  g_rr += R R',  g_qx += Q X'      (ld x ld, int32)
+//
+// as ONE hand-written sm_100a tensor-core kernel (tcgen05.mma kind::i8, exact int32
+// accumulation in TMEM), replacing four separate library GEMMs.  X / R / Q are rows of
+// one (3, ld, w) int8 array (row j of a panel = column j of the ratings over w rating
+// rows, i.e. K-major), so the fused kernel loads each operand tile once for all the
+// products that use it:
+//
+//   per 128 x 128 output tile (a, b) and per 64-byte K block:
+//     smem  Xa Ra Qa (A, 128 rows each) | Xb Rb (B, contiguous = one 256-row operand)
+//     TMEM  cols   0..127  D_xx += Xa . Xb'         (N = 128)
+//           cols 128..383  D_rx|D_rr += Ra . [Xb;Rb]'   (N = 256, one instruction)
+//           cols 384..511  D_qx += Qa . Xb'         (N = 128)
+//
+// 4 products share 5 tile loads (a plain GEMM pays 2 per product).  Warp-specialised,
+// persistent (one CTA per SM): warp 0 = TMA producer (cp.async.bulk.tensor, 64-byte
+// swizzle, 5-stage mbarrier ring), warp 1 = TMEM owner + single-thread MMA issuer
+// (tcgen05.commit frees a stage / publishes the accumulator), warps 2..5 = epilogue
+// (tcgen05.ld 32x32b -> int32 stores, += when accumulating over row passes).  Every
+// product entry is an exact integer (|sum| <= 121 * rows < 2^31), so the statistics --
+// and the fp64 similarities the select kernel derives from them -- are bit-identical to
+// the reference's ordered fp64 sums.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace culsh {
+namespace gsm_tc {
+
+constexpr int kBM = 128;                     // output tile rows (a) = MMA M
+constexpr int kBN = 128;                     // output tile cols (b)
+constexpr int kBK = 64;                      // K bytes per stage (64-byte swizzle rows)
+constexpr int kStages = 5;
+constexpr int kTile = kBM * kBK;             // 8 KB per 128-row operand tile
+constexpr int kStageBytes = 5 * kTile;       // Xa Ra Qa Xb Rb = 40 KB
+constexpr int kThreads = 192;                // 6 warps
+constexpr int kTmemCols = 512;
+constexpr int kGroupA = 8;                   // tile raster: 8 a-blocks per band (L2 reuse)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int32_t x, int32_t y,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// K-major operand in shared memory, 64-byte swizzle: 8-row atoms of 512 bytes, stride
+// byte offset 512, descriptor version 1 (sm_100), layout type 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFF) >> 4);          // start address
+    d |= (uint64_t)1 << 16;                          // leading byte offset (unused, swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;                 // stride byte offset
+    d |= (uint64_t)1 << 46;                          // version
+    d |= (uint64_t)4 << 61;                          // SWIZZLE_64B
+    return d;
+}
+
+// kind::i8 instruction descriptor: s32 accumulator, signed A/B, both K-major, M = 128.
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tile_of(int64_t t, int nA, int nB, int &a, int &b) {
+    const int64_t band = (int64_t)kGroupA * nB;
+    const int first = (int)(t / band) * kGroupA;
+    const int gsz = min(nA - first, kGroupA);
+    const int64_t r = t % band;
+    a = first + (int)(r % gsz);
+    b = (int)(r / gsz);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+gsm_stats_tc_kernel(const __grid_constant__ CUtensorMap panels, int64_t ld, int nk, int accumulate,
+                    int32_t *__restrict__ g_xx, int32_t *__restrict__ g_rx, int32_t *__restrict__ g_rr,
+                    int32_t *__restrict__ g_qx) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + kStages * kStageBytes);
+    uint64_t *empty = full + kStages;
+    uint64_t *tmem_full = empty + kStages;
+    uint64_t *tmem_empty = tmem_full + 1;
+    uint32_t *tmem_slot = (uint32_t *)(tmem_empty + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nA = (int)(ld / kBM), nB = (int)(ld / kBN);
+    const int64_t ntiles = (int64_t)nA * nB;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&panels) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int a, b;
+                tile_of(t, nA, nB, a, b);
+                const int ya = a * kBM, yb = b * kBN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char *st = smem + stage * kStageBytes;
+                    mbar_expect_tx(&full[stage], kStageBytes);
+                    const int x = kb * kBK;
+                    tma_load_2d(smem_u32(st + 0 * kTile), &panels, x, (int32_t)(0 * ld + ya), &full[stage]);
+                    tma_load_2d(smem_u32(st + 1 * kTile), &panels, x, (int32_t)(1 * ld + ya), &full[stage]);
+                    tma_load_2d(smem_u32(st + 2 * kTile), &panels, x, (int32_t)(2 * ld + ya), &full[stage]);
+                    tma_load_2d(smem_u32(st + 3 * kTile), &panels, x, (int32_t)(0 * ld + yb), &full[stage]);
+                    tma_load_2d(smem_u32(st + 4 * kTile), &panels, x, (int32_t)(1 * ld + yb), &full[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one thread) ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            constexpr uint32_t id128 = idesc_i8(128), id256 = idesc_i8(256);
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(tmem_empty, acc_phase ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t base = smem_u32(smem + stage * kStageBytes);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 32; ++kk) {
+                        const uint32_t off = kk * 32;
+                        const uint64_t dXa = smem_desc(base + 0 * kTile + off);
+                        const uint64_t dRa = smem_desc(base + 1 * kTile + off);
+                        const uint64_t dQa = smem_desc(base + 2 * kTile + off);
+                        const uint64_t dXb = smem_desc(base + 3 * kTile + off);   // [Xb; Rb] for N = 256
+                        const uint32_t acc = (kb | kk) ? 1u : 0u;
+                        mma_i8(tmem + 0, dXa, dXb, id128, acc);
+                        mma_i8(tmem + 128, dRa, dXb, id256, acc);
+                        mma_i8(tmem + 384, dQa, dXb, id128, acc);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(tmem_full);
+                acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ---------------- epilogue: TMEM -> global ----------------
+        const int quarter = warp & 3;            // TMEM lanes this warp may access
+        const int row_in_tile = quarter * 32 + lane;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int a, b;
+            tile_of(t, nA, nB, a, b);
+            mbar_wait(tmem_full, acc_phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t row = (int64_t)a * kBM + row_in_tile;
+            const int64_t col0 = (int64_t)b * kBN;
+#pragma unroll 1
+            for (int c = 0; c < kTmemCols; c += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c, v);
+                int32_t *g = c < 128 ? g_xx : c < 256 ? g_rx : c < 384 ? g_rr : g_qx;
+                int4 *dst = reinterpret_cast<int4 *>(g + row * ld + col0 + (c & 127));
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    int4 o = make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2], (int)v[4 * q + 3]);
+                    if (accumulate) {
+                        const int4 p = dst[q];
+                        o.x += p.x;
+                        o.y += p.y;
+                        o.z += p.z;
+                        o.w += p.w;
+                    }
+                    dst[q] = o;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tmem_empty);
+            acc_phase ^= 1;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols)
+                     : "memory");
+}
+
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 + 256;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+}  // namespace gsm_tc
+}  // namespace culsh
+
+using namespace culsh;
+
+extern "C" int culsh_gsm_stats_tc(const int8_t *panels, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
+                                  int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, void *stream) {
+    using namespace culsh::gsm_tc;
+    CULSH_REQUIRE(ld > 0 && ld % kBM == 0, "ld must be a positive multiple of 128");
+    CULSH_REQUIRE(w > 0 && w % kBK == 0, "w must be a positive multiple of 64");
+    CULSH_REQUIRE(3 * ld < (1ll << 31) && w < (1ll << 31), "panel too large for 32-bit TMA coordinates");
+    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(panels) & 15) == 0, "panels must be 16-byte aligned");
+    auto enc = encode_fn();
+    CULSH_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)(3 * ld)};
+    const cuuint64_t strides[1] = {(cuuint64_t)w};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)panels, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CULSH_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed");
+    CULSH_CHECK(cudaFuncSetAttribute(gsm_stats_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemBytes));
+    const int64_t ntiles = (ld / kBM) * (ld / kBN);
+    const int grid = (int)min64(ntiles, (int64_t)num_sms());
+    gsm_stats_tc_kernel<<<grid, kThreads, kSmemBytes, (cudaStream_t)stream>>>(
+        map, ld, (int)(w / kBK), accumulate, g_xx, g_rx, g_rr, g_qx);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}

@@ -650,12 +650,10 @@ extern "C" int culsh_hash_count(const int64_t *col_ptr, const int32_t *rows_by_c
     CULSH_REQUIRE(threads <= 128, "q*p*ceil(G/8) > 512 bytes: use culsh_hash_accumulate");
     const size_t smem = (size_t)kHsRing * 16 * stride + (size_t)((W4 * 4 + 15) & ~15) +
                         sizeof(int) * 32 * threads;
-    static bool attr = false;
-    if (!attr) {
+    {   // per device and cheap: set on every launch (a once-per-process flag breaks on a 2nd GPU)
         cudaFuncSetAttribute(hash_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(hash_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(hash_count_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
     }
     const bool use_tma = variant == 0;
     const size_t smem_k = use_tma ? smem : smem - (size_t)kHsRing * 16 * stride;

@@ -660,11 +660,9 @@ int launch_hogwild(int64_t N, const int64_t *col_ptr, const int64_t *seg, const 
                    const int64_t *mptr = nullptr, const int32_t *first_row = nullptr) {
     const int threads = kHwWarps * 32;
     const size_t smem = (size_t)kHwWarps * hw_smem_per_warp<FV, KPL>();
-    static bool attr_set = false;
-    if (!attr_set) {
+    {   // per device and cheap: set on every launch (a once-per-process flag breaks on a 2nd GPU)
         cudaFuncSetAttribute(hogwild_kernel<FV, KPL, true, PACK, P16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(hogwild_kernel<FV, KPL, false, PACK, P16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
     }
     int occ = 0;
     auto kern = (flags & 2) ? hogwild_kernel<FV, KPL, true, PACK, P16> : hogwild_kernel<FV, KPL, false, PACK, P16>;

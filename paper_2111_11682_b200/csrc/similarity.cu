@@ -270,13 +270,11 @@ extern "C" int culsh_gsm_merge_topk(const int64_t *col_ptr, const int32_t *col_r
     cudaStream_t st = (cudaStream_t)stream;
     const int smem_cap = 8192;   // j1's list in shared memory up to 8192 ratings (96 KB)
     const size_t smem = (size_t)smem_cap * 12;
-    static bool attr = false;
-    if (!attr) {
+    {   // per device and cheap: set on every launch (a once-per-process flag breaks on a 2nd GPU)
         cudaFuncSetAttribute(gsm_merge_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gsm_merge_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gsm_merge_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gsm_merge_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     const unsigned grid = (unsigned)n_rows;
     CULSH_GSM_KDISPATCH(gsm_merge_kernel, col_ptr, col_rows, col_vals, N, j_lo, K, lambda_rho, smem_cap, entries);

@@ -632,7 +632,8 @@ def bench_main(args, metric, workload, rates):
                 "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
                 "data": "synthetic (random_sparse distribution, each rank generates its own shards in HBM)",
-                "config": {"workload": workload[args.config], "nnz": nnz, "parallelism": f"dsgd{D}",
+                "config": workload,
+                "impl_config": {"nnz_generated": nnz, "parallelism": f"dsgd{D}",
                            "ring_parts": parts, "rotating_side": side,
                            "moving_bytes_per_stage_per_gpu": moving,
                            "exchange": (f"NCCL send/recv ring shift of the {side} parameter sub-blocks, each "

@@ -434,11 +434,11 @@ def _colpass(dev, dm: DeviceModel64, sc: _Scratch, rates: nat.CulshRates, col_lo
              nat.stream_ptr())
 
 
-def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fraction: float = 1.0):
+def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fraction: float = 0.5):
     """Neighbour lookups of columns [col_lo, col_hi) for _colpass's ``pre``: the K
     dependent binary searches of every update leave the update chain (which is what
     bounds a pass on long columns / hot rows).  None when K == 0, the range is empty, or
-    the arrays (entries x K x 8 B) would exceed ``mem_fraction`` of the free memory."""
+    the arrays (entries x (8K + 4 ceil(K/32)) B) would exceed ``mem_fraction`` of the free memory."""
     K = dm.struct.K
     if K == 0 or col_hi <= col_lo:
         return None
@@ -446,9 +446,9 @@ def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fractio
     base = int(cp[col_lo].item())
     n = int(cp[col_hi].item()) - base
     t = nat.torch()
-    if n * K * 8.5 > mem_fraction * t.cuda.mem_get_info()[0]:
-        return None
     kpl = 1 if K <= 32 else 2
+    if n * (8 * K + 4 * kpl) > mem_fraction * t.cuda.mem_get_info()[0]:   # rv f64 + mask words
+        return None
     mask = nat.empty((max(n * kpl, 1),), "int32")
     rv = nat.empty((max(n * K, 1),), "float64")
     nat.call("culsh_exact_lookup", ctypes.byref(dev.struct), ctypes.byref(dm.struct), col_lo, col_hi,

@@ -47,17 +47,48 @@ class DeviceModel32:
         self.W = f32(W) if W.size else nat.zeros((1,), "float32")
         self.C = f32(C) if C.size else nat.zeros((1,), "float32")
         self.nbr = p.nbr_entries_device()
+        self.Fp = self.F
+        self._pad()
         self._restruct()
 
     @classmethod
-    def from_arrays(cls, arrays: dict, mu: float, M: int, N: int, F: int, K: int, nbr=None):
+    def from_arrays(cls, arrays: dict, mu: float, M: int, N: int, F: int, K: int, nbr=None,
+                    padded: bool = False):
+        """``arrays`` hold U / V as (M, F) / (N, F) rows, or already in the padded
+        storage layout when ``padded``."""
         self = cls.__new__(cls)
         self.M, self.N, self.F, self.K, self.mu = M, N, F, K, float(mu)
         for n, a in arrays.items():
             setattr(self, _DEV_NAME[n], a)
         self.nbr = nbr if nbr is not None else nat.zeros((1,), "int32")
+        self.Fp = hogwild_width(F) if padded else F
+        self._pad()
         self._restruct()
         return self
+
+    def _pad(self) -> None:
+        """Store U / V with the kernel's row width Fp = hogwild_width(F): the extra
+        features are zero and stay zero (their update is gamma*(e*0 - lambda*0)), so
+        the model is the F-feature model; host views drop them."""
+        Fp = hogwild_width(self.F)
+        if Fp == self.Fp:
+            return
+        t = nat.torch()
+        for name, rows in (("U", self.M), ("V", self.N)):
+            old = getattr(self, name)
+            new = t.zeros((max(rows * Fp, 1),), dtype=t.float32, device=old.device)
+            if rows:
+                new[:rows * Fp].view(rows, Fp)[:, :self.F] = old[:rows * self.F].view(rows, self.F)
+            setattr(self, name, new)
+        self.Fp = Fp
+
+    def _logical(self, name: str):
+        """Device view of parameter ``name`` in the logical (unpadded) shape, flattened."""
+        a = getattr(self, _DEV_NAME[name])
+        if name in ("U", "V") and self.Fp != self.F:
+            rows = self.M if name == "U" else self.N
+            return a[:rows * self.Fp].view(rows, self.Fp)[:, :self.F].reshape(-1)
+        return a
 
     @classmethod
     def from_params(cls, p: ModelParams):
@@ -68,14 +99,15 @@ class DeviceModel32:
             t = nat.torch()
             if isinstance(dev, cls):
                 arrays = {n: getattr(dev, _DEV_NAME[n]).clone() for n in _DEV_NAME}
-            else:
-                arrays = {n: getattr(dev, _DEV_NAME[n]).to(t.float32) for n in _DEV_NAME}
+                return cls.from_arrays(arrays, p.mu, p.M, p.N, p.F, p.K, p.nbr_entries_device(),
+                                       padded=True)
+            arrays = {n: getattr(dev, _DEV_NAME[n]).to(t.float32) for n in _DEV_NAME}
             return cls.from_arrays(arrays, p.mu, p.M, p.N, p.F, p.K, p.nbr_entries_device())
         return cls(p)
 
     def _restruct(self) -> None:
         self.struct = nat.CulshModel32(self.mu, nat.ptr(self.b), nat.ptr(self.bhat), nat.ptr(self.U),
-                                       nat.ptr(self.V), nat.ptr(self.W), nat.ptr(self.C), self.F,
+                                       nat.ptr(self.V), nat.ptr(self.W), nat.ptr(self.C), self.Fp,
                                        self.K)
 
     def _shape(self, name: str):
@@ -85,7 +117,7 @@ class DeviceModel32:
     def download(self, name: str, out=None) -> np.ndarray:
         shape = self._shape(name)
         n = int(np.prod(shape))
-        host = (nat.to_host(getattr(self, _DEV_NAME[name]))[:n].astype(np.float64).reshape(shape)
+        host = (nat.to_host(self._logical(name)[:n]).astype(np.float64).reshape(shape)
                 if n else np.zeros(shape))
         if out is not None and out.shape == shape and out.dtype == np.float64 and out.flags.writeable:
             out[...] = host
@@ -95,11 +127,16 @@ class DeviceModel32:
     def upload(self, name: str, host: np.ndarray) -> None:
         a = np.ascontiguousarray(host, dtype=np.float32).reshape(-1)
         if a.size:
-            getattr(self, _DEV_NAME[name])[:a.size].copy_(nat.torch().from_numpy(a))
+            src = nat.torch().from_numpy(a)
+            if name in ("U", "V") and self.Fp != self.F:
+                rows = a.size // self.F
+                getattr(self, name)[:rows * self.Fp].view(rows, self.Fp)[:, :self.F].copy_(src.view(rows, self.F))
+            else:
+                getattr(self, _DEV_NAME[name])[:a.size].copy_(src)
 
     def all_finite(self, M: int, N: int) -> bool:
         t = nat.torch()
-        F, K = self.F, self.K
+        F, K = self.Fp, self.K
         parts = [self.b[:M], self.bhat[:N], self.U[:M * F], self.V[:N * F], self.W[:N * K], self.C[:N * K]]
         return all(bool(t.isfinite(x).all().item()) for x in parts if x.numel())
 
@@ -107,7 +144,7 @@ class DeviceModel32:
         """An fp64 DeviceModel64 copy (device-side conversion)."""
         from .factorization import DeviceModel64
         t = nat.torch()
-        arrays = {n: getattr(self, _DEV_NAME[n]).to(t.float64) for n in _DEV_NAME}
+        arrays = {n: self._logical(n).to(t.float64) for n in _DEV_NAME}
         return DeviceModel64(arrays=arrays, mu=self.mu, M=self.M, N=self.N, F=self.F, K=self.K,
                              nbr=self.nbr)
 
@@ -117,8 +154,16 @@ class DeviceModel32:
                            C=h("C"), neighbors=neighbors)
 
 
+def hogwild_width(F: int) -> int:
+    """Row width the Hogwild kernels run for F features: F itself for F <= 32 or
+    F in (64, 128, 256), else the next of 64 / 128 / 256 (zero-padded features)."""
+    if F <= 32 or F in (64, 128, 256):
+        return F
+    return 64 if F <= 64 else 128 if F <= 128 else 256
+
+
 def hogwild_supported(F: int, K: int) -> bool:
-    return (1 <= F <= 32 or F in (64, 128, 256)) and 0 <= K <= 64
+    return 1 <= F <= 256 and 0 <= K <= 64
 
 
 class HogwildTrainer:
@@ -140,8 +185,8 @@ class HogwildTrainer:
         self.neighbors = neighbors
         K = neighbors.K if neighbors is not None else 0
         if not hogwild_supported(config.F, K):
-            raise ValueError(f"Hogwild mode supports F <= 32 or F in (64, 128, 256) and K <= 64; "
-                             f"got F={config.F}, K={K}")
+            raise ValueError(f"Hogwild mode supports 1 <= F <= 256 and K <= 64 (the reference takes any "
+                             f"F and K, factorization.py:75-82); got F={config.F}, K={K}")
         t = nat.torch()
         self.dev = dev if dev is not None else ratings.device()
         d = self.dev
@@ -317,7 +362,7 @@ class HogwildTrainer:
 
     def kernel_name(self) -> str:
         """The epoch kernel a whole-matrix launch_epoch (device-resident stream) runs."""
-        F, K = self.config.F, self.K
+        F, K = hogwild_width(self.config.F), self.K
         at = str(bool(self.atomic_rows)).lower()
         fv = 1 if F <= 32 else F // 32
         return "hogwild_kernel<%d,%d,%s,%s,false>" % (fv, self.MW, at, str(self.packed is not None).lower())

@@ -118,16 +118,18 @@ _GSM_MAX_K = 128
 
 
 def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
-    """Count route; False (nothing written) when a value is not an integer in [-11, 11]."""
+    """Count route; False (nothing written) when a value is not an integer in [-11, 11].
+    The statistics of all pairs are four int8 products of dense column panels, computed
+    by one tensor-core kernel (culsh_gsm_stats_tc) per pass over rating-row chunks."""
     t = nat.torch()
     N, M = d.N, d.M
-    ld = max(32, (N + 15) // 16 * 16)
+    ld = max(128, (N + 127) // 128 * 128)
     free = t.cuda.mem_get_info()[0]
     prod_bytes = 4 * ld * ld * 4
     # rows of the dense panels per pass (int32 products accumulate exactly across passes)
     budget = max(int(0.5 * free) - prod_bytes, 3 * ld * 64)
     mc = max(64, min((M + 63) // 64 * 64, budget // (3 * ld) // 64 * 64))
-    g = [t.zeros((ld, ld), dtype=t.int32, device=nat.device()) for _ in range(4)]
+    g = t.empty((4, ld, ld), dtype=t.int32, device=nat.device())
     st = nat.zeros((1,), "int32")
     for m0 in range(0, M, mc):
         m1 = min(M, m0 + mc)
@@ -138,12 +140,9 @@ def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
                  nat.stream_ptr())
         if int(st.item()):
             return False
-        x, r, q = pan[0], pan[1], pan[2]
-        g[0] += t._int_mm(x, x.t())
-        g[1] += t._int_mm(r, x.t())
-        g[2] += t._int_mm(r, r.t())
-        g[3] += t._int_mm(q, x.t())
-        del pan, x, r, q
+        nat.call("culsh_gsm_stats_tc", nat.ptr(pan), ld, w, int(m0 > 0), nat.ptr(g[0]), nat.ptr(g[1]),
+                 nat.ptr(g[2]), nat.ptr(g[3]), nat.stream_ptr())
+        del pan
     nat.call("culsh_gsm_count_select", nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]), nat.ptr(g[3]), ld, N,
              0, N, K, float(lambda_rho), nat.ptr(entries), nat.stream_ptr())
     return True

@@ -795,6 +795,33 @@ class TestGsm:
             assert np.array_equal(P.gsm_topk(r, P.SimilarityConfig(K=32, lambda_rho=50.0), method=meth).entries,
                                   z["c1_gsm_K32_l50"]), meth
 
+    @pytest.mark.parametrize("ld,w,passes", [(128, 64, 1), (384, 1024, 1), (1664, 192, 2), (256, 4096, 3)])
+    def test_gsm_stats_tc_products(self, P, ld, w, passes):
+        """culsh_gsm_stats_tc (tcgen05 kind::i8, TMEM accumulators) == the four int32
+        products computed independently (torch integer matmul in int64), with row-pass
+        accumulation; 1664 = 13 blocks -> 169 tiles, more than one tile per CTA."""
+        import torch
+        from paper_2111_11682_b200 import _native as nat
+        gen = torch.Generator().manual_seed(ld + w)
+        g = torch.zeros((4, ld, ld), dtype=torch.int32, device="cuda")
+        want = torch.zeros((4, ld, ld), dtype=torch.int64)
+        for ps in range(passes):
+            pan = torch.randint(-11, 12, (3, ld, w), generator=gen, dtype=torch.int8)
+            pan[0] = (pan[0] > 0).to(torch.int8)           # indicator
+            pan[2] = (pan[1].to(torch.int16) ** 2).to(torch.int8)   # squares <= 121
+            x, r, q = (pan[i].to(torch.int64) for i in range(3))
+            want[0] += x @ x.T
+            want[1] += r @ x.T
+            want[2] += r @ r.T
+            want[3] += q @ x.T
+            dpan = pan.cuda()
+            nat.call("culsh_gsm_stats_tc", nat.ptr(dpan), ld, w, int(ps > 0), nat.ptr(g[0]), nat.ptr(g[1]),
+                     nat.ptr(g[2]), nat.ptr(g[3]), nat.stream_ptr())
+        torch.cuda.synchronize()
+        got = g.cpu().to(torch.int64)
+        for i, name in enumerate(("xx", "rx", "rr", "qx")):
+            assert torch.equal(got[i], want[i]), name
+
     def test_gsm_mid_scale_vs_oracle(self, P, orc):
         """20,000 x 3,000, ~600k integer ratings: count route == merge route == oracle."""
         rng = np.random.default_rng(7)
@@ -944,10 +971,11 @@ class TestApiGolden:
             assert getattr(pt, k).tobytes() == z["inc_" + k].tobytes(), k
 
 
-@pytest.mark.parametrize("F,K", [(8, 8), (32, 48), (256, 64)])
+@pytest.mark.parametrize("F,K", [(8, 8), (32, 48), (256, 64), (50, 16), (96, 32), (200, 8)])
 def test_hogwild_shapes_c1(P, c1, F, K):
     """Every Hogwild kernel instantiation family (F < 32 masked lanes, K > 32 two mask
-    words, F = 256) trains to the exact mode's test RMSE within the 0.005 bar."""
+    words, F = 256) and the zero-padded widths (F = 50 / 96 / 200 run as 64 / 128 / 256)
+    train to the exact mode's test RMSE within the 0.005 bar."""
     z, tr, te = c1
     nbr = P.NeighborTable(tr.N, 32, z["lsh_entries32"])
     if K != 32:
@@ -955,8 +983,17 @@ def test_hogwild_shapes_c1(P, c1, F, K):
         nbr = tbl
     cfg = P.TrainConfig(F=F, K=K, epochs=12, seed=0)
     exact = P.rmse(P.train_full(tr, nbr, cfg), te, tr)
-    hog = P.rmse(P.train_full(tr, nbr, cfg, mode="hogwild"), te, tr)
+    ph = P.train_full(tr, nbr, cfg, mode="hogwild")
+    hog = P.rmse(ph, te, tr)
     assert abs(hog - exact) <= REF_TOL_RMSE, (F, K, hog, exact)
+    assert ph.U.shape == (tr.M, F) and ph.V.shape == (tr.N, F)
+    if F in (50, 96, 200):    # padded storage: the extra features stay exactly zero
+        m = ph._dev
+        U = m.U[:tr.M * m.Fp].view(tr.M, m.Fp)[:, F:]
+        assert m.Fp > F and bool((U == 0).all())
+        ph.U[0, :] = 0.5                           # a host edit reaches the padded device copy
+        j = int(tr.row_cols[0])
+        assert P.predict(0, j, ph, tr) == P.predict(0, j, ph.copy(), tr)
 
 
 @pytest.mark.parametrize("work", [False, True])
