@@ -173,6 +173,33 @@ def workload_config(name):
             "rates": "Netflix Table 6 (alpha 0.02/0.001, lambda 0.01/0.05, beta 0.3)"}
 
 
+def lib_sha256():
+    import hashlib
+    from paper_2111_11682_b200 import _native as nat
+    with open(nat.LIB_PATH, "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()
+
+
+def ncu_measured(config, kernel):
+    """The epoch kernel's measured DRAM bytes and unit utilisations from the committed ncu
+    --set full capture (profiles/ncu_roofline_<config>.json, tools/ncu_summary.py), with
+    same_build = whether that capture profiled the library this process loaded."""
+    path = os.path.join(ROOT, "profiles", f"ncu_roofline_{config}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        m = json.load(fh)
+    m["same_build"] = bool(m.get("lib_sha256")) and m["lib_sha256"] == lib_sha256()
+    pk, _ = peak_hbm_gbs()
+    m["dram_frac_of_peak"] = m["dram_gbs"] / pk
+    m["limiter"] = max((("l1tex", m["l1tex_throughput_pct"]), ("l2", m["l2_throughput_pct"]),
+                        ("sm_issue", m["sm_throughput_pct"]), ("dram", 100.0 * m["dram_frac_of_peak"])),
+                       key=lambda x: x[1])[0]
+    m["profiled_kernel_matches"] = kernel.split("<")[0] in m.get("kernel", "")
+    m["file"] = os.path.relpath(path, ROOT)
+    return m
+
+
 def cpu_calibration():
     """profiles/r2_cpu_calibration.json (tools/calibrate_cpu_baseline.py, build container):
     the port's time over the unmodified reference's on the same sample and threads."""
@@ -358,11 +385,9 @@ def run_gpu(args):
         except Exception as ex:  # the CPU leg must not sink the GPU line
             cpu = {"value": None, "error": repr(ex)}
 
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+    measured = ncu_measured(args.config, tr.kernel_name())
+    traffic = measured["dram_bytes_per_launch"] if measured and measured["same_build"] else None
+    lsh_gather = float(nnz) * (lcfg.q * lcfg.p * lsh._ns(lcfg.G))   # one row-hash record per rating
     line = {
         "metric": METRIC, "value": ups, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -374,13 +399,22 @@ def run_gpu(args):
                         "rotate": bool(args.rotate), "atomic_rows": bool(args.atomic),
                         "l2": "inputs larger than L2 (rating stream + u matrix > 126 MB), no flush"},
         "lsh_build_s": lsh_s, "lsh_build_runs_s": lsh_runs, "lsh_candidates": ncand,
-        # the simLSH build's work is nnz*p*q*G signed accumulations
-        "lsh_accumulations_per_s": float(nnz) * lcfg.p * lcfg.q * lcfg.G / lsh_s,
+        # the build's dominant traffic: one row-hash record (q*p*ceil(G/8) bytes) gathered per
+        # rating by hash_count_kernel, over the WHOLE build time (value sets, class partition,
+        # row hashes and top-K included), against L2 / HBM
+        "lsh_table_gather": {"bytes": lsh_gather, "gbs_over_build": lsh_gather / lsh_s / 1e9,
+                             "record_bytes": (lcfg.q * lcfg.p * lsh._ns(lcfg.G)), "peak_hbm_gbs": peak},
+        # the reference's work measure (nnz*p*q*G signed adds) per second of the
+        # build -- the bit-count kernel does not execute these adds one by one
+        "lsh_reference_equivalent_adds_per_s": float(nnz) * lcfg.p * lcfg.q * lcfg.G / lsh_s,
         "prep_s": t_prep, "datagen_s": t_gen, "train_rmse_running": train_rmse,
         "epoch_ms": [p * 1e3 for p in per],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_update": b_upd, "kernel": tr.kernel_name()},
+                     "frac_kind": "algorithmic: SURVEY 8(d) bytes per update x updates / launch time; "
+                                  "above 1 because u_i rows hit in L2 (see measured)",
+                     "bytes_per_update": b_upd, "kernel": tr.kernel_name(),
+                     "measured": measured},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,

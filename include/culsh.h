@@ -363,14 +363,25 @@ int culsh_gsm_densify_rows(const int64_t *col_ptr, const int32_t *col_rows, cons
                            int64_t N, int64_t row_lo, int64_t row_hi, int64_t ld, int8_t *xt,
                            int8_t *rt, int8_t *qt, int *status, void *stream);
 
-/* Count route, step 2: the four statistic products of the (3, ld, w) int8 panel
- * array (X rows 0..ld-1, R rows ld..2ld-1, Q rows 2ld..3ld-1, row stride w bytes):
+/* Count route, tiled panels (the layout culsh_gsm_stats_tc reads): for each (128-row
+ * block rb of the ld >= N columns, 64-byte block kb of the w rating rows) a 24 KB group
+ * [X | R | Q] at ((rb * w/64 + kb) * 3 + p) * 8192, each 8 KB tile in the tcgen05 K-major
+ * 64-byte-swizzle layout (column j row r = j % 128 at r * 64, 16-byte chunk c at
+ * c ^ ((r >> 1) & 3)).  densify writes 1 / r / r*r for every rating (i, j) with
+ * row_lo <= i < row_hi into a zero-filled 3*ld*w byte array; *status |= 1 if a value is
+ * not an integer in [-11, 11] (use the merge route then).  tile_panels converts a plain
+ * (3, ld, w) array. */
+int culsh_gsm_densify_tiled(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                            int64_t N, int64_t row_lo, int64_t row_hi, int64_t ld, int64_t w, int8_t *tiles,
+                            int *status, void *stream);
+int culsh_gsm_tile_panels(const int8_t *plain, int64_t ld, int64_t w, int8_t *tiles, void *stream);
+
+/* Count route, step 2: the four statistic products of the tiled panels:
  * g_xx (+)= X X', g_rx (+)= R X', g_rr (+)= R R', g_qx (+)= Q X' (ld x ld int32,
  * row stride ld; accumulate != 0 adds to the existing values, for row passes).  One
- * sm_100a kernel: TMA-fed tcgen05.mma kind::i8 with TMEM accumulators, exact int32
- * (similarity.py:57-90 statistics of every pair at once).  ld % 128 == 0,
- * w % 64 == 0, panels 16-byte aligned. */
-int culsh_gsm_stats_tc(const int8_t *panels, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
+ * sm_100a kernel: bulk-copy-fed tcgen05.mma kind::i8 with TMEM accumulators, exact int32
+ * (similarity.py:57-90 statistics of every pair at once).  ld % 128 == 0, w % 64 == 0. */
+int culsh_gsm_stats_tc(const int8_t *tiles, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
                        int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, void *stream);
 
 /* Count route, step 3 (after the int32 products g_xx = X'X, g_rx = R'X,

@@ -98,6 +98,8 @@ _SIGS = {
     "culsh_gsm_merge_topk": [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_gsm_densify_rows": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
     "culsh_gsm_stats_tc": [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp],
+    "culsh_gsm_densify_tiled": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
+    "culsh_gsm_tile_panels": [_vp, _i64, _i64, _vp, _vp],
     "culsh_gsm_count_select": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_pair_similarity": [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp],
     "culsh_split_holdout": [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp],
@@ -179,10 +181,64 @@ def stream_ptr():
     return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
 
 
+# NVTX ranges (SURVEY §5 tracing): every C-ABI call is a range named after its entry point,
+# and the public API functions open an enclosing range (``nvtx_range``), so an nsys / ncu
+# --nvtx timeline shows the stages (simlsh_topk > culsh_hash_count > ...).  CULSH_NVTX=0
+# turns them off; they cost ~1 us per call (a call launches whole kernels).
+_NVTX = os.environ.get("CULSH_NVTX", "1") != "0"
+_nvtx_mod = None
+
+
+def _nvtx():
+    global _nvtx_mod, _NVTX
+    if _nvtx_mod is None:
+        try:
+            t = torch()
+            _nvtx_mod = t.cuda.nvtx if t.cuda.is_available() else False
+        except Exception:   # pragma: no cover
+            _nvtx_mod = False
+        if not _nvtx_mod:
+            _NVTX = False
+    return _nvtx_mod
+
+
+class nvtx_range:
+    """Context manager / decorator: an NVTX range around a host-side stage."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        if _NVTX and _nvtx():
+            _nvtx_mod.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if _NVTX and _nvtx_mod:
+            _nvtx_mod.range_pop()
+        return False
+
+    def __call__(self, fn):
+        import functools
+
+        @functools.wraps(fn)
+        def wrapped(*a, **k):
+            with nvtx_range(self.name):
+                return fn(*a, **k)
+        return wrapped
+
+
 def call(name: str, *args) -> int:
     """Call an entry point; raise on CULSH_EINVAL / CULSH_ECUDA, return the status."""
     lib = load_library()
-    st = getattr(lib, name)(*args)
+    if _NVTX and _nvtx():
+        _nvtx_mod.range_push(name)
+        try:
+            st = getattr(lib, name)(*args)
+        finally:
+            _nvtx_mod.range_pop()
+    else:
+        st = getattr(lib, name)(*args)
     if st < 0:
         msg = lib.culsh_last_error().decode()
         if st == CULSH_EINVAL:

@@ -15,16 +15,28 @@
 //           cols 128..383  D_rx|D_rr += Ra . [Xb;Rb]'   (N = 256, one instruction)
 //           cols 384..511  D_qx += Qa . Xb'         (N = 128)
 //
-// 4 products share 5 tile loads (a plain GEMM pays 2 per product).  Warp-specialised,
-// persistent (one CTA per SM): warp 0 = TMA producer (cp.async.bulk.tensor, 64-byte
-// swizzle, 5-stage mbarrier ring), warp 1 = TMEM owner + single-thread MMA issuer
+// 4 products share 5 tile loads (a plain GEMM pays 2 per product).
+//
+// Panel layout in HBM ("tiled"): the panels are stored as tile groups, one per (128-row
+// block rb, 64-byte K block kb), rb-major: group = [X | R | Q], 3 x 8 KB, each 8 KB tile
+// already in the tcgen05 K-major SWIZZLE_64B layout (row r at r*64 bytes, 16-byte chunk c
+// at chunk c ^ ((r >> 1) & 3)).  A stage is then TWO contiguous bulk copies (24 KB of
+// A = [Xa|Ra|Qa], 16 KB of B = [Xb|Rb]) instead of five 2D tensor boxes of 64-byte rows:
+// measured with the boxes, the copy engine delivered only ~24 B/clk per SM (tensor pipe
+// 30 % busy, L2 and DRAM far from saturated).  The densify kernel writes this layout
+// directly (culsh_gsm_densify_tiled); culsh_gsm_tile_panels converts a plain (3, ld, w)
+// array.
+//
+// Warp-specialised, persistent (one CTA per SM): warp 0 = bulk-copy producer (5-stage
+// mbarrier ring), warp 1 = TMEM owner + single-thread MMA issuer
 // (tcgen05.commit frees a stage / publishes the accumulator), warps 2..5 = epilogue
 // (tcgen05.ld 32x32b -> int32 stores, += when accumulating over row passes).  Every
 // product entry is an exact integer (|sum| <= 121 * rows < 2^31), so the statistics --
 // and the fp64 similarities the select kernel derives from them -- are bit-identical to
 // the reference's ordered fp64 sums.
-#include <cuda.h>
-#include <cudaTypedefs.h>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -40,6 +52,9 @@ constexpr int kStageBytes = 5 * kTile;       // Xa Ra Qa Xb Rb = 40 KB
 constexpr int kThreads = 192;                // 6 warps
 constexpr int kTmemCols = 512;
 constexpr int kGroupA = 8;                   // tile raster: 8 a-blocks per band (L2 reuse)
+constexpr int kSyncEvery = 128;              // producer checkpoint every 128 K blocks ...
+constexpr int kSyncLag = 2;                  // ... at most 2 checkpoints ahead of the slowest CTA
+                                             // (CULSH_GSM_SYNC="every,lag" overrides; 0 = off)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -69,13 +84,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int32_t x, int32_t y,
-                                            uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-            "r"(dst),
-        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
+// Byte offset of panel p (0 = X, 1 = R, 2 = Q), column j, K position k in the tiled layout.
+__host__ __device__ __forceinline__ int64_t tiled_off(int p, int64_t j, int64_t k, int64_t nkb) {
+    const int64_t r = j & 127, kk = k & 63;
+    const int64_t grp = (j >> 7) * nkb + (k >> 6);
+    const int64_t chunk = (kk >> 4) ^ ((r >> 1) & 3);
+    return (grp * 3 + p) * (int64_t)kTile + r * 64 + chunk * 16 + (kk & 15);
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // K-major operand in shared memory, 64-byte swizzle: 8-row atoms of 512 bytes, stride
@@ -133,10 +154,36 @@ __device__ __forceinline__ void tile_of(int64_t t, int nA, int nB, int &a, int &
     b = (int)(r / gsz);
 }
 
+// Drift control.  The concurrently running CTAs share operand tiles through L2 only while
+// they stream the same K blocks: the band of 148 tiles reads ~0.5 MB per K block, but L2
+// turns over in ~20 us under the panel stream, so CTAs that drift more than ~20 K blocks
+// apart re-read their tiles from DRAM (measured: 3.6 TB of DRAM reads at C2 for 3.8 TB of
+// tile loads, DRAM-bound).  Every kSyncEvery K blocks the producer publishes its
+// checkpoint in prog[cta] and waits until the slowest CTA is at most kSyncLag checkpoints
+// behind; a CTA out of tiles publishes INT_MAX.  The grid is one CTA per SM, so all CTAs
+// are normally co-resident; if a wait ever exceeds 5 ms (CTAs not co-resident, e.g. SMs
+// taken by another context), the CTA stops synchronising instead of deadlocking -- the
+// products are unaffected either way, only the L2 reuse.
+__device__ __forceinline__ bool drift_wait(int *prog, int ncta, int cp, int lane, int lag) {
+    // relaxed (volatile) accesses: no data is handed over, only progress, and an acquire
+    // load would invalidate the SM's L1 (CCTL.IVALL) on every poll
+    if (lane == 0) *(volatile int *)(prog + blockIdx.x) = cp;
+    const uint64_t t0 = global_ns();
+    for (;;) {
+        int lo = INT_MAX;
+        for (int c = lane; c < ncta; c += 32) lo = min(lo, ld_volatile(prog + c));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        if (lo >= cp - lag) return true;
+        if (global_ns() - t0 > 5000000ull) return false;
+        __nanosleep(200);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-gsm_stats_tc_kernel(const __grid_constant__ CUtensorMap panels, int64_t ld, int nk, int accumulate,
+gsm_stats_tc_kernel(const int8_t *__restrict__ tiles, int64_t ld, int nk, int accumulate,
                     int32_t *__restrict__ g_xx, int32_t *__restrict__ g_rx, int32_t *__restrict__ g_rr,
-                    int32_t *__restrict__ g_qx) {
+                    int32_t *__restrict__ g_qx, int *__restrict__ prog, int sync_every, int sync_lag) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + kStages * kStageBytes);
@@ -158,7 +205,6 @@ gsm_stats_tc_kernel(const __grid_constant__ CUtensorMap panels, int64_t ld, int 
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&panels) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -173,31 +219,38 @@ gsm_stats_tc_kernel(const __grid_constant__ CUtensorMap panels, int64_t ld, int 
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int a, b;
-                tile_of(t, nA, nB, a, b);
-                const int ya = a * kBM, yb = b * kBN;
-                for (int kb = 0; kb < nk; ++kb) {
+        // ---------------- TMA producer (lane 0; the warp joins the drift checkpoints) ----------------
+        int stage = 0;
+        uint32_t phase = 0;
+        int cp = 0;
+        bool sync = sync_every > 0;
+        int64_t step = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int a, b;
+            tile_of(t, nA, nB, a, b);
+            for (int kb = 0; kb < nk; ++kb, ++step) {
+                if (sync && step % sync_every == 0) {
+                    __syncwarp();
+                    sync = drift_wait(prog, gridDim.x, ++cp, lane, sync_lag);
+                    sync = __shfl_sync(0xffffffffu, sync, 0);
+                    if (!sync && lane == 0) *(volatile int *)(prog + blockIdx.x) = INT_MAX;   // stop holding others
+                }
+                if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = smem + stage * kStageBytes;
                     mbar_expect_tx(&full[stage], kStageBytes);
-                    const int x = kb * kBK;
-                    tma_load_2d(smem_u32(st + 0 * kTile), &panels, x, (int32_t)(0 * ld + ya), &full[stage]);
-                    tma_load_2d(smem_u32(st + 1 * kTile), &panels, x, (int32_t)(1 * ld + ya), &full[stage]);
-                    tma_load_2d(smem_u32(st + 2 * kTile), &panels, x, (int32_t)(2 * ld + ya), &full[stage]);
-                    tma_load_2d(smem_u32(st + 3 * kTile), &panels, x, (int32_t)(0 * ld + yb), &full[stage]);
-                    tma_load_2d(smem_u32(st + 4 * kTile), &panels, x, (int32_t)(1 * ld + yb), &full[stage]);
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    bulk_load(smem_u32(st), tiles + ((int64_t)a * nk + kb) * (3 * kTile), 3 * kTile, &full[stage]);
+                    bulk_load(smem_u32(st + 3 * kTile), tiles + ((int64_t)b * nk + kb) * (3 * kTile), 2 * kTile,
+                              &full[stage]);
+                }
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
+        __syncwarp();
+        if (lane == 0) *(volatile int *)(prog + blockIdx.x) = INT_MAX;
     } else if (warp == 1) {
         // ---------------- MMA issuer (one thread) ----------------
         if (lane == 0) {
@@ -280,16 +333,44 @@ gsm_stats_tc_kernel(const __grid_constant__ CUtensorMap panels, int64_t ld, int 
 
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 + 256;
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+// Dense int8 panels for the count route in the tiled layout: 1 / r / r*r at (j, i - row_lo)
+// for every rating (i, j) with row_lo <= i < row_hi (zeros elsewhere, memset by the caller).
+// *status |= 1 when a value is not an integer in [-11, 11].
+__global__ void densify_tiled_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ col_rows,
+                                     const double *__restrict__ col_vals, int64_t N, int64_t row_lo,
+                                     int64_t row_hi, int64_t nkb, int8_t *__restrict__ tiles,
+                                     int *__restrict__ status) {
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned lane = lane_id();
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < N; j += warps) {
+        int bad = 0;
+        for (int64_t e = col_ptr[j] + lane; e < col_ptr[j + 1]; e += 32) {
+            const int32_t i = col_rows[e];
+            if (i < row_lo || i >= row_hi) continue;
+            const double v = col_vals[e];
+            const int iv = (int)v;
+            if ((double)iv != v || iv < -11 || iv > 11) bad = 1;
+            const int64_t k = i - row_lo;
+            tiles[tiled_off(0, j, k, nkb)] = 1;
+            tiles[tiled_off(1, j, k, nkb)] = (int8_t)iv;
+            tiles[tiled_off(2, j, k, nkb)] = (int8_t)(iv * iv);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1);
     }
-    return fn;
+}
+
+// plain (3, ld, w) -> tiled, one thread per 16-byte chunk.
+__global__ void tile_panels_kernel(const int8_t *__restrict__ plain, int64_t ld, int64_t w,
+                                   int8_t *__restrict__ tiles) {
+    const int64_t nchunk = 3 * ld * (w / 16), nkb = w / kBK;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunk;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = c / (w / 16), k = (c % (w / 16)) * 16;
+        const int p = (int)(row / ld);
+        const int64_t j = row % ld;
+        *reinterpret_cast<int4 *>(tiles + tiled_off(p, j, k, nkb)) =
+            *reinterpret_cast<const int4 *>(plain + row * w + k);
+    }
 }
 
 }  // namespace gsm_tc
@@ -297,30 +378,51 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 using namespace culsh;
 
-extern "C" int culsh_gsm_stats_tc(const int8_t *panels, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
+extern "C" int culsh_gsm_densify_tiled(const int64_t *col_ptr, const int32_t *col_rows, const double *col_vals,
+                                       int64_t N, int64_t row_lo, int64_t row_hi, int64_t ld, int64_t w,
+                                       int8_t *tiles, int *status, void *stream) {
+    using namespace culsh::gsm_tc;
+    CULSH_REQUIRE(ld >= N && ld % kBM == 0 && w % kBK == 0 && row_hi - row_lo <= w,
+                  "tiled panels need ld >= N, ld % 128 == 0, w % 64 == 0, row range <= w");
+    if (N <= 0) return CULSH_OK;
+    const int64_t blocks = min64((N + 7) / 8, (int64_t)num_sms() * 16);
+    densify_tiled_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(col_ptr, col_rows, col_vals, N, row_lo,
+                                                                              row_hi, w / kBK, tiles, status);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_gsm_tile_panels(const int8_t *plain, int64_t ld, int64_t w, int8_t *tiles, void *stream) {
+    using namespace culsh::gsm_tc;
+    CULSH_REQUIRE(ld > 0 && ld % kBM == 0 && w > 0 && w % kBK == 0, "ld % 128 == 0 and w % 64 == 0");
+    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(plain) & 15) == 0 && (reinterpret_cast<uintptr_t>(tiles) & 15) == 0,
+                  "16-byte aligned arrays");
+    const int64_t blocks = min64((3 * ld * (w / 16) + 255) / 256, (int64_t)num_sms() * 32);
+    tile_panels_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(plain, ld, w, tiles);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
+extern "C" int culsh_gsm_stats_tc(const int8_t *tiles, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
                                   int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, void *stream) {
     using namespace culsh::gsm_tc;
     CULSH_REQUIRE(ld > 0 && ld % kBM == 0, "ld must be a positive multiple of 128");
     CULSH_REQUIRE(w > 0 && w % kBK == 0, "w must be a positive multiple of 64");
-    CULSH_REQUIRE(3 * ld < (1ll << 31) && w < (1ll << 31), "panel too large for 32-bit TMA coordinates");
-    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(panels) & 15) == 0, "panels must be 16-byte aligned");
-    auto enc = encode_fn();
-    CULSH_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
-    CUtensorMap map;
-    const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)(3 * ld)};
-    const cuuint64_t strides[1] = {(cuuint64_t)w};
-    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)panels, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    CULSH_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed");
+    CULSH_REQUIRE(w / kBK < (1ll << 31), "panel too long");
+    CULSH_REQUIRE((reinterpret_cast<uintptr_t>(tiles) & 15) == 0, "tiles must be 16-byte aligned");
     CULSH_CHECK(cudaFuncSetAttribute(gsm_stats_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kSmemBytes));
     const int64_t ntiles = (ld / kBM) * (ld / kBN);
     const int grid = (int)min64(ntiles, (int64_t)num_sms());
-    gsm_stats_tc_kernel<<<grid, kThreads, kSmemBytes, (cudaStream_t)stream>>>(
-        map, ld, (int)(w / kBK), accumulate, g_xx, g_rx, g_rr, g_qx);
+    cudaStream_t st = (cudaStream_t)stream;
+    int *prog = nullptr;
+    CULSH_CHECK(cudaMallocAsync((void **)&prog, sizeof(int) * (size_t)grid, st));
+    CULSH_CHECK(cudaMemsetAsync(prog, 0, sizeof(int) * (size_t)grid, st));
+    int every = kSyncEvery, lag = kSyncLag;
+    if (const char *e = getenv("CULSH_GSM_SYNC")) sscanf(e, "%d,%d", &every, &lag);
+    gsm_stats_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(tiles, ld, (int)(w / kBK), accumulate, g_xx, g_rx,
+                                                            g_rr, g_qx, prog, every, lag);
     CULSH_LAUNCH_CHECK();
+    CULSH_CHECK(cudaFreeAsync(prog, st));
     return CULSH_OK;
 }

@@ -134,10 +134,9 @@ def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
     for m0 in range(0, M, mc):
         m1 = min(M, m0 + mc)
         w = (m1 - m0 + 63) // 64 * 64
-        pan = t.zeros((3, ld, w), dtype=t.int8, device=nat.device())
-        nat.call("culsh_gsm_densify_rows", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(d.col_vals),
-                 N, m0, m1, w, nat.ptr(pan[0]), nat.ptr(pan[1]), nat.ptr(pan[2]), nat.ptr(st),
-                 nat.stream_ptr())
+        pan = t.zeros((3 * ld * w,), dtype=t.int8, device=nat.device())
+        nat.call("culsh_gsm_densify_tiled", nat.ptr(d.col_ptr), nat.ptr(d.col_rows), nat.ptr(d.col_vals),
+                 N, m0, m1, ld, w, nat.ptr(pan), nat.ptr(st), nat.stream_ptr())
         if int(st.item()):
             return False
         nat.call("culsh_gsm_stats_tc", nat.ptr(pan), ld, w, int(m0 > 0), nat.ptr(g[0]), nat.ptr(g[1]),

@@ -815,7 +815,9 @@ class TestGsm:
             want[2] += r @ r.T
             want[3] += q @ x.T
             dpan = pan.cuda()
-            nat.call("culsh_gsm_stats_tc", nat.ptr(dpan), ld, w, int(ps > 0), nat.ptr(g[0]), nat.ptr(g[1]),
+            tiles = torch.empty_like(dpan)
+            nat.call("culsh_gsm_tile_panels", nat.ptr(dpan), ld, w, nat.ptr(tiles), nat.stream_ptr())
+            nat.call("culsh_gsm_stats_tc", nat.ptr(tiles), ld, w, int(ps > 0), nat.ptr(g[0]), nat.ptr(g[1]),
                      nat.ptr(g[2]), nat.ptr(g[3]), nat.stream_ptr())
         torch.cuda.synchronize()
         got = g.cpu().to(torch.int64)

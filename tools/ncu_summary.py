@@ -2,7 +2,13 @@
 
   python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/r1_launches.md
   python tools/ncu_summary.py full gpurun_out/prof_hogwild.ncu-rep profiles/r1_ncu_hogwild.md \
-         [--traffic-json profiles/ncu_traffic_c3.json]
+         [--roofline-json profiles/ncu_roofline_c3.json --lib paper_2111_11682_b200/_lib/libculsh.so]
+  python tools/ncu_summary.py sass paper_2111_11682_b200/_lib/libculsh.so profiles/r2_sass.md \
+         hogwild_kernel hash_count_kernel ...
+
+--roofline-json writes what bench.py's `roofline.measured` quotes: the kernel's DRAM bytes
+and unit utilisations from this capture, with the sha256 of the library it profiled (bench.py
+marks the numbers `same_build` only when the library it loaded has that hash).
 """
 
 from __future__ import annotations
@@ -67,7 +73,19 @@ def launches(src: str, dst: str) -> None:
     print(out.getvalue())
 
 
-def full(rep: str, dst: str, traffic_json: str | None = None) -> None:
+def _num(d, k):
+    v, unit = d[k]
+    x = float(v.replace(",", ""))
+    return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1.0)
+
+
+def _sha256(path: str) -> str:
+    import hashlib
+    with open(path, "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()
+
+
+def full(rep: str, dst: str, traffic_json: str | None = None, lib: str | None = None) -> None:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -92,8 +110,23 @@ def full(rep: str, dst: str, traffic_json: str | None = None) -> None:
             tot = rd * scale[d["dram__bytes_read.sum"][1]] + wr * scale[d["dram__bytes_write.sum"][1]]
             out.write(f"\nDRAM traffic per launch: {tot / 1e9:.3f} GB\n\n")
             if traffic_json:
-                json.dump({"kernel": name.split("(")[0], "dram_bytes_per_launch": tot, "source": rep},
-                          open(traffic_json, "w"), indent=1)
+                ms = _to_ms(_num(d, "gpu__time_duration.sum") / 1.0, d["gpu__time_duration.sum"][1])
+                rec = {"kernel": name.split("(")[0], "source": rep.split("/")[-1],
+                       "ncu": "--set full --clock-control none (cold-ish, one launch)",
+                       "duration_ms": ms, "dram_bytes_per_launch": tot,
+                       "dram_read_bytes": _num(d, "dram__bytes_read.sum"),
+                       "dram_write_bytes": _num(d, "dram__bytes_write.sum"),
+                       "dram_gbs": tot / (ms * 1e-3) / 1e9,
+                       "l2_hit_pct": _num(d, "lts__t_sector_hit_rate.pct"),
+                       "l2_throughput_pct": _num(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                       "l1tex_throughput_pct": _num(d, "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                       "sm_throughput_pct": _num(d, "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+                       "issue_ipc": (_num(d, "smsp__inst_executed.avg.per_cycle_active")
+                                     if "smsp__inst_executed.avg.per_cycle_active" in d else None),
+                       "warps_active_pct": _num(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                       "registers": _num(d, "launch__registers_per_thread"),
+                       "lib_sha256": _sha256(lib) if lib else None}
+                json.dump(rec, open(traffic_json, "w"), indent=1)
         except (KeyError, ValueError):
             pass
     hdr = f"# ncu --set full summary ({rep})\n\n--clock-control none; one launch per kernel; numbers under the profiler are not bench values.\n\n"
@@ -101,12 +134,45 @@ def full(rep: str, dst: str, traffic_json: str | None = None) -> None:
     print(hdr + out.getvalue())
 
 
+def sass(lib: str, dst: str, kernels) -> None:
+    """Per-kernel SASS opcode histogram (cuobjdump -sass): the instruction mix behind the
+    ncu numbers, and proof of which units a kernel uses (UTCIMMA / UTMALDG = tcgen05 MMA /
+    TMA; FFMA2 / FMUL2 = paired fp32; REDG / REDUX = reductions; LDGSTS = cp.async)."""
+    import re
+    txt = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
+    funcs = re.split(r"\n\s+Function : ", txt)
+    out = io.StringIO()
+    out.write(f"# SASS opcode mix per hot kernel (`cuobjdump -sass {lib.split('/')[-1]}`, sm_100a)\n\n")
+    for k in kernels:
+        out.write(f"## kernels matching `{k}`\n\n")
+        for f in funcs[1:]:
+            fname = f.split("\n", 1)[0].strip()
+            if k not in fname:
+                continue
+            ops = defaultdict(int)
+            for line in f.split("\n"):
+                m = re.match(r"\s+/\*[0-9a-f]{4,}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]+)", line)
+                if m:
+                    ops[m.group(2)] += 1
+            tot = sum(ops.values())
+            top = sorted(ops.items(), key=lambda x: -x[1])
+            out.write(f"`{fname[:160]}` -- {tot} instructions\n\n")
+            out.write(", ".join(f"{o} {n}" for o, n in top[:40]) + "\n\n")
+    open(dst, "w").write(out.getvalue())
+    print(out.getvalue()[:4000])
+
+
 if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif mode == "sass":
+        sass(sys.argv[2], sys.argv[3], sys.argv[4:])
     else:
-        tj = None
-        if "--traffic-json" in sys.argv:
-            tj = sys.argv[sys.argv.index("--traffic-json") + 1]
-        full(sys.argv[2], sys.argv[3], tj)
+        tj = lib = None
+        for flag in ("--traffic-json", "--roofline-json"):
+            if flag in sys.argv:
+                tj = sys.argv[sys.argv.index(flag) + 1]
+        if "--lib" in sys.argv:
+            lib = sys.argv[sys.argv.index("--lib") + 1]
+        full(sys.argv[2], sys.argv[3], tj, lib)
