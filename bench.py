@@ -378,6 +378,8 @@ def run_gpu(args):
     # ---- e2e through the public API with host (pinned) buffers every step
     e2e = e2e_streaming(tr, args)
 
+    fit = fit_leg(dm, nbr, F, K, args) if args.fit else None
+
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -417,11 +419,42 @@ def run_gpu(args):
                      "measured": measured},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "fit": fit,
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def fit_leg(dm, nbr, F, K, args):
+    """The per-fit cost the epoch line excludes: ONE public call
+    train_full(ratings, neighbors, TrainConfig(epochs=20), mode="hogwild") on the resident
+    C3 ratings -- device PCG64 init, explicit-neighbour stream, stream packing, 20 epochs --
+    plus reading every parameter back as the reference's fp64 host numpy arrays (U, V, W, C,
+    b, b_hat), timed with a device sync on both sides (after one untimed 1-epoch call that
+    warms the allocator and the pinned staging buffers)."""
+    import torch
+    import paper_2111_11682_b200 as P
+    from paper_2111_11682_b200.factorization import TrainConfig
+    d = dm.dev
+    cols = torch.repeat_interleave(torch.arange(d.N, device=d.col_ptr.device, dtype=torch.int32),
+                                   d.col_ptr[1:] - d.col_ptr[:-1])
+    ratings = P.SparseRatings._from_device(d, (d.col_rows, cols, d.col_vals))
+    names = ("b", "b_hat", "U", "V", "W", "C")
+    P.train_full(ratings, nbr, TrainConfig(F=F, K=K, epochs=1, seed=0, **NETFLIX_RATES), mode="hogwild")
+    cfg = TrainConfig(F=F, K=K, epochs=20, seed=0, **NETFLIX_RATES)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    p = P.train_full(ratings, nbr, cfg, mode="hogwild")
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    arrays = [getattr(p, n) for n in names]
+    t2 = time.perf_counter()
+    return {"epochs": 20, "s": t2 - t0, "train_full_s": t1 - t0, "to_host_s": t2 - t1,
+            "d2h_bytes": int(sum(a.nbytes for a in arrays)), "finite": bool(all(np.isfinite(a).all() for a in arrays)),
+            "api": "train_full(SparseRatings resident in HBM, NeighborTable, TrainConfig(epochs=20), "
+                   "mode='hogwild') + fp64 host numpy of every parameter"}
 
 
 def e2e_streaming(tr, args):
@@ -452,6 +485,7 @@ def main():
     ap.add_argument("--impl", default="culsh", choices=["culsh", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fit", type=int, default=1, help="time one 20-epoch public train_full fit (host fp64 out)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--p16", type=int, default=1, help="2-byte packed records (row deltas) when they fit")
     ap.add_argument("--rotate", type=int, default=0, help="per-column rotated visiting order")

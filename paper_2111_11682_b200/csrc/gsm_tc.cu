@@ -233,7 +233,10 @@ gsm_stats_tc_kernel(const int8_t *__restrict__ tiles, int64_t ld, int nk, int ac
                     __syncwarp();
                     sync = drift_wait(prog, gridDim.x, ++cp, lane, sync_lag);
                     sync = __shfl_sync(0xffffffffu, sync, 0);
-                    if (!sync && lane == 0) *(volatile int *)(prog + blockIdx.x) = INT_MAX;   // stop holding others
+                    if (!sync && lane == 0) {
+                        *(volatile int *)(prog + blockIdx.x) = INT_MAX;   // stop holding others
+                        atomicAdd(prog + gridDim.x, 1);                   // timeouts (CULSH_GSM_DEBUG)
+                    }
                 }
                 if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -416,13 +419,20 @@ extern "C" int culsh_gsm_stats_tc(const int8_t *tiles, int64_t ld, int64_t w, in
     const int grid = (int)min64(ntiles, (int64_t)num_sms());
     cudaStream_t st = (cudaStream_t)stream;
     int *prog = nullptr;
-    CULSH_CHECK(cudaMallocAsync((void **)&prog, sizeof(int) * (size_t)grid, st));
-    CULSH_CHECK(cudaMemsetAsync(prog, 0, sizeof(int) * (size_t)grid, st));
+    CULSH_CHECK(cudaMallocAsync((void **)&prog, sizeof(int) * (size_t)(grid + 1), st));
+    CULSH_CHECK(cudaMemsetAsync(prog, 0, sizeof(int) * (size_t)(grid + 1), st));
     int every = kSyncEvery, lag = kSyncLag;
     if (const char *e = getenv("CULSH_GSM_SYNC")) sscanf(e, "%d,%d", &every, &lag);
     gsm_stats_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(tiles, ld, (int)(w / kBK), accumulate, g_xx, g_rx,
                                                             g_rr, g_qx, prog, every, lag);
     CULSH_LAUNCH_CHECK();
+    if (getenv("CULSH_GSM_DEBUG")) {
+        int timeouts = 0;
+        CULSH_CHECK(cudaMemcpyAsync(&timeouts, prog + grid, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CULSH_CHECK(cudaStreamSynchronize(st));
+        fprintf(stderr, "culsh_gsm_stats_tc: ld=%lld w=%lld grid=%d sync=%d,%d timeouts=%d\n", (long long)ld,
+                (long long)w, grid, every, lag, timeouts);
+    }
     CULSH_CHECK(cudaFreeAsync(prog, st));
     return CULSH_OK;
 }

@@ -375,17 +375,17 @@ class DeviceModel64:
         d = getattr(self, _DEV_NAME[name])
         shape = self._shape(name, self.M, self.N)
         n = int(np.prod(shape))
-        host = nat.to_host(d)[:n].reshape(shape) if n else np.zeros(shape)
+        host = nat.to_host(d[:n]).reshape(shape) if n else np.zeros(shape)
         if out is not None and out.shape == shape and out.dtype == np.float64 and out.flags.writeable:
             out[...] = host
             return out
-        return np.array(host, dtype=np.float64)
+        return np.asarray(host, dtype=np.float64)   # a fresh array already (no second copy)
 
     def upload(self, name: str, host: np.ndarray) -> None:
         d = getattr(self, _DEV_NAME[name])
         a = np.ascontiguousarray(host, dtype=np.float64).reshape(-1)
         if a.size:
-            d[:a.size].copy_(nat.torch().from_numpy(a))
+            nat.copy_to_device(d[:a.size], a)
 
     def all_finite(self, M: int, N: int) -> bool:
         t = nat.torch()

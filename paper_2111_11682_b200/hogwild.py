@@ -117,7 +117,8 @@ class DeviceModel32:
     def download(self, name: str, out=None) -> np.ndarray:
         shape = self._shape(name)
         n = int(np.prod(shape))
-        host = (nat.to_host(self._logical(name)[:n]).astype(np.float64).reshape(shape)
+        # widen on the device, then one staged copy (no host-side fp32 -> fp64 pass)
+        host = (nat.to_host(self._logical(name)[:n].to(nat.torch().float64)).reshape(shape)
                 if n else np.zeros(shape))
         if out is not None and out.shape == shape and out.dtype == np.float64 and out.flags.writeable:
             out[...] = host
@@ -125,9 +126,9 @@ class DeviceModel32:
         return host
 
     def upload(self, name: str, host: np.ndarray) -> None:
-        a = np.ascontiguousarray(host, dtype=np.float32).reshape(-1)
+        a = np.ascontiguousarray(host, dtype=np.float64).reshape(-1)
         if a.size:
-            src = nat.torch().from_numpy(a)
+            src = nat.to_dev(a).to(nat.torch().float32)   # staged fp64 upload, narrowed on the device
             if name in ("U", "V") and self.Fp != self.F:
                 rows = a.size // self.F
                 getattr(self, name)[:rows * self.Fp].view(rows, self.Fp)[:, :self.F].copy_(src.view(rows, self.F))

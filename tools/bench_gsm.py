@@ -53,7 +53,7 @@ def main():
     cpu_s = time.perf_counter() - t0
     ok = bool(np.array_equal(sub, tbl.entries[pick]))
     line = {"metric": "GSM exact top-K build time", "config": cfgname, "M": M, "N": N, "nnz": int(dm.nnz),
-            "K": K, "route": "count (culsh_gsm_stats_tc: tcgen05 kind::i8, TMEM)", "device_s": dev_s,
+            "K": K, "runs_s": [r[0] for r in runs], "route": "count (culsh_gsm_stats_tc: tcgen05 kind::i8, TMEM)", "device_s": dev_s,
             "wall_s": float(np.median([r[1] for r in runs])), "int8_tops": ops / dev_s / 1e12,
             "cpu_oracle": {"threads": threads, "sample_targets": len(pick), "sample_s": cpu_s,
                            "extrapolated_s": cpu_s * N / len(pick)},
