@@ -173,11 +173,19 @@ def workload_config(name):
             "rates": "Netflix Table 6 (alpha 0.02/0.001, lambda 0.01/0.05, beta 0.3)"}
 
 
-def lib_sha256():
+def build_sha256():
+    """Identity of the native build: sha256 over the CUDA sources, the C header and the
+    Makefile (nvcc output itself is not byte-reproducible, the sources and flags are)."""
     import hashlib
-    from paper_2111_11682_b200 import _native as nat
-    with open(nat.LIB_PATH, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
+    import glob
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2111_11682_b200", "csrc", "*")))
+    for f in files + [os.path.join(ROOT, "include", "culsh.h")]:
+        if os.path.isfile(f):
+            h.update(os.path.basename(f).encode())
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()
 
 
 def ncu_measured(config, kernel):
@@ -189,7 +197,7 @@ def ncu_measured(config, kernel):
         return None
     with open(path) as fh:
         m = json.load(fh)
-    m["same_build"] = bool(m.get("lib_sha256")) and m["lib_sha256"] == lib_sha256()
+    m["same_build"] = bool(m.get("build_sha256")) and m["build_sha256"] == build_sha256()
     pk, _ = peak_hbm_gbs()
     m["dram_frac_of_peak"] = m["dram_gbs"] / pk
     m["limiter"] = max((("l1tex", m["l1tex_throughput_pct"]), ("l2", m["l2_throughput_pct"]),

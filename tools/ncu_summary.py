@@ -7,8 +7,10 @@
          hogwild_kernel hash_count_kernel ...
 
 --roofline-json writes what bench.py's `roofline.measured` quotes: the kernel's DRAM bytes
-and unit utilisations from this capture, with the sha256 of the library it profiled (bench.py
-marks the numbers `same_build` only when the library it loaded has that hash).
+and unit utilisations from this capture, with the build identity of the tree it profiled
+(bench.build_sha256: CUDA sources + header + Makefile; bench.py marks the numbers
+`same_build` only when its own tree has that identity).  Run it on the tree that was
+profiled, before changing any CUDA source.
 """
 
 from __future__ import annotations
@@ -79,10 +81,12 @@ def _num(d, k):
     return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1.0)
 
 
-def _sha256(path: str) -> str:
-    import hashlib
-    with open(path, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
+def _build_sha256() -> str:
+    """bench.py's build identity (sources + header + Makefile of the profiled tree)."""
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    return bench.build_sha256()
 
 
 def full(rep: str, dst: str, traffic_json: str | None = None, lib: str | None = None) -> None:
@@ -125,7 +129,7 @@ def full(rep: str, dst: str, traffic_json: str | None = None, lib: str | None = 
                                      if "smsp__inst_executed.avg.per_cycle_active" in d else None),
                        "warps_active_pct": _num(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
                        "registers": _num(d, "launch__registers_per_thread"),
-                       "lib_sha256": _sha256(lib) if lib else None}
+                       "build_sha256": _build_sha256() if lib else None}
                 json.dump(rec, open(traffic_json, "w"), indent=1)
         except (KeyError, ValueError):
             pass
