@@ -365,7 +365,7 @@ int culsh_gsm_densify_rows(const int64_t *col_ptr, const int32_t *col_rows, cons
 
 /* Count route, tiled panels (the layout culsh_gsm_stats_tc reads): for each (128-row
  * block rb of the ld >= N columns, 64-byte block kb of the w rating rows) a 24 KB group
- * [X | R | Q] at ((rb * w/64 + kb) * 3 + p) * 8192, each 8 KB tile in the tcgen05 K-major
+ * [X | R | Q] at ((kb * ld/128 + rb) * 3 + p) * 8192, each 8 KB tile in the tcgen05 K-major
  * 64-byte-swizzle layout (column j row r = j % 128 at r * 64, 16-byte chunk c at
  * c ^ ((r >> 1) & 3)).  densify writes 1 / r / r*r for every rating (i, j) with
  * row_lo <= i < row_hi into a zero-filled 3*ld*w byte array; *status |= 1 if a value is

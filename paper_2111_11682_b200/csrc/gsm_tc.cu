@@ -18,7 +18,7 @@
 // 4 products share 5 tile loads (a plain GEMM pays 2 per product).
 //
 // Panel layout in HBM ("tiled"): the panels are stored as tile groups, one per (128-row
-// block rb, 64-byte K block kb), rb-major: group = [X | R | Q], 3 x 8 KB, each 8 KB tile
+// block rb, 64-byte K block kb), kb-major: group = [X | R | Q], 3 x 8 KB, each 8 KB tile
 // already in the tcgen05 K-major SWIZZLE_64B layout (row r at r*64 bytes, 16-byte chunk c
 // at chunk c ^ ((r >> 1) & 3)).  A stage is then TWO contiguous bulk copies (24 KB of
 // A = [Xa|Ra|Qa], 16 KB of B = [Xb|Rb]) instead of five 2D tensor boxes of 64-byte rows:
@@ -85,9 +85,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 // Byte offset of panel p (0 = X, 1 = R, 2 = Q), column j, K position k in the tiled layout.
-__host__ __device__ __forceinline__ int64_t tiled_off(int p, int64_t j, int64_t k, int64_t nkb) {
+// Groups are K-block-major (group = kb * nrb + rb): the blocks the co-resident tiles read at
+// one K step are contiguous (rb-major placed them nkb * 24 KB apart -- a 2^17-multiple
+// stride at C3 -- and C3 runs varied 0.37-1.37 s with the panel's base address).
+__host__ __device__ __forceinline__ int64_t tiled_off(int p, int64_t j, int64_t k, int64_t nrb) {
     const int64_t r = j & 127, kk = k & 63;
-    const int64_t grp = (j >> 7) * nkb + (k >> 6);
+    const int64_t grp = (k >> 6) * nrb + (j >> 7);
     const int64_t chunk = (kk >> 4) ^ ((r >> 1) & 3);
     return (grp * 3 + p) * (int64_t)kTile + r * 64 + chunk * 16 + (kk & 15);
 }
@@ -242,9 +245,9 @@ gsm_stats_tc_kernel(const int8_t *__restrict__ tiles, int64_t ld, int nk, int ac
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = smem + stage * kStageBytes;
                     mbar_expect_tx(&full[stage], kStageBytes);
-                    bulk_load(smem_u32(st), tiles + ((int64_t)a * nk + kb) * (3 * kTile), 3 * kTile, &full[stage]);
-                    bulk_load(smem_u32(st + 3 * kTile), tiles + ((int64_t)b * nk + kb) * (3 * kTile), 2 * kTile,
-                              &full[stage]);
+                    const int64_t kbase = (int64_t)kb * nA;   // K-block-major groups
+                    bulk_load(smem_u32(st), tiles + (kbase + a) * (3 * kTile), 3 * kTile, &full[stage]);
+                    bulk_load(smem_u32(st + 3 * kTile), tiles + (kbase + b) * (3 * kTile), 2 * kTile, &full[stage]);
                 }
                 if (++stage == kStages) {
                     stage = 0;
@@ -341,7 +344,7 @@ constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 + 256;
 // *status |= 1 when a value is not an integer in [-11, 11].
 __global__ void densify_tiled_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ col_rows,
                                      const double *__restrict__ col_vals, int64_t N, int64_t row_lo,
-                                     int64_t row_hi, int64_t nkb, int8_t *__restrict__ tiles,
+                                     int64_t row_hi, int64_t nrb, int8_t *__restrict__ tiles,
                                      int *__restrict__ status) {
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const unsigned lane = lane_id();
@@ -354,9 +357,9 @@ __global__ void densify_tiled_kernel(const int64_t *__restrict__ col_ptr, const 
             const int iv = (int)v;
             if ((double)iv != v || iv < -11 || iv > 11) bad = 1;
             const int64_t k = i - row_lo;
-            tiles[tiled_off(0, j, k, nkb)] = 1;
-            tiles[tiled_off(1, j, k, nkb)] = (int8_t)iv;
-            tiles[tiled_off(2, j, k, nkb)] = (int8_t)(iv * iv);
+            tiles[tiled_off(0, j, k, nrb)] = 1;
+            tiles[tiled_off(1, j, k, nrb)] = (int8_t)iv;
+            tiles[tiled_off(2, j, k, nrb)] = (int8_t)(iv * iv);
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1);
     }
@@ -365,13 +368,13 @@ __global__ void densify_tiled_kernel(const int64_t *__restrict__ col_ptr, const 
 // plain (3, ld, w) -> tiled, one thread per 16-byte chunk.
 __global__ void tile_panels_kernel(const int8_t *__restrict__ plain, int64_t ld, int64_t w,
                                    int8_t *__restrict__ tiles) {
-    const int64_t nchunk = 3 * ld * (w / 16), nkb = w / kBK;
+    const int64_t nchunk = 3 * ld * (w / 16), nrb = ld / kBM;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunk;
          c += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = c / (w / 16), k = (c % (w / 16)) * 16;
         const int p = (int)(row / ld);
         const int64_t j = row % ld;
-        *reinterpret_cast<int4 *>(tiles + tiled_off(p, j, k, nkb)) =
+        *reinterpret_cast<int4 *>(tiles + tiled_off(p, j, k, nrb)) =
             *reinterpret_cast<const int4 *>(plain + row * w + k);
     }
 }
@@ -390,7 +393,7 @@ extern "C" int culsh_gsm_densify_tiled(const int64_t *col_ptr, const int32_t *co
     if (N <= 0) return CULSH_OK;
     const int64_t blocks = min64((N + 7) / 8, (int64_t)num_sms() * 16);
     densify_tiled_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(col_ptr, col_rows, col_vals, N, row_lo,
-                                                                              row_hi, w / kBK, tiles, status);
+                                                                              row_hi, ld / kBM, tiles, status);
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }

@@ -457,10 +457,12 @@ def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fractio
 
 
 def _check_model_dims(F: int, K: int) -> None:
+    # the reference accepts any F and K (factorization.py:75-82); the kernels keep up to
+    # 256 factors per row and two 32-bit explicit-neighbour mask words per rating
     if not (1 <= F <= 256):
-        raise ValueError(f"F={F} outside the supported range [1, 256]")
+        raise ValueError(f"F={F} outside the supported range [1, 256] (the reference has no bound)")
     if not (0 <= K <= 64):
-        raise ValueError(f"K={K} outside the supported range [0, 64]")
+        raise ValueError(f"K={K} outside the supported range [0, 64] (the reference has no bound)")
 
 
 # ------------------------------------------------------------- public ops ---

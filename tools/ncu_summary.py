@@ -162,6 +162,10 @@ def sass(lib: str, dst: str, kernels) -> None:
             top = sorted(ops.items(), key=lambda x: -x[1])
             out.write(f"`{fname[:160]}` -- {tot} instructions\n\n")
             out.write(", ".join(f"{o} {n}" for o, n in top[:40]) + "\n\n")
+            keyfam = ("UTCIMMA", "UTCHMMA", "UTCBAR", "UBLKCP", "UTMALDG", "LDTM", "LDGSTS", "REDG", "REDUX",
+                      "FFMA2", "FMUL2", "SHFL", "VOTE", "POPC", "ATOMS", "DADD", "DFMA", "DMUL")
+            fam = {k: sum(n for o, n in ops.items() if o.startswith(k)) for k in keyfam}
+            out.write("key families: " + ", ".join(f"{k} {v}" for k, v in fam.items() if v) + "\n\n")
     open(dst, "w").write(out.getvalue())
     print(out.getvalue()[:4000])
 
