@@ -52,8 +52,8 @@ constexpr int kStageBytes = 5 * kTile;       // Xa Ra Qa Xb Rb = 40 KB
 constexpr int kThreads = 192;                // 6 warps
 constexpr int kTmemCols = 512;
 constexpr int kGroupA = 8;                   // tile raster: 8 a-blocks per band (L2 reuse)
-constexpr int kSyncEvery = 128;              // producer checkpoint every 128 K blocks ...
-constexpr int kSyncLag = 2;                  // ... at most 2 checkpoints ahead of the slowest CTA
+constexpr int kSyncEvery = 512;              // producer checkpoint every 512 K blocks ...
+constexpr int kSyncLag = 4;                  // ... at most 4 checkpoints ahead of the slowest CTA
                                              // (CULSH_GSM_SYNC="every,lag" overrides; 0 = off)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

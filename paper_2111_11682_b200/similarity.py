@@ -17,6 +17,9 @@ _topk_insert's strict comparisons produce.
 
 from __future__ import annotations
 
+import os
+import sys
+
 import ctypes
 from dataclasses import dataclass
 
@@ -131,6 +134,8 @@ def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
     mc = max(64, min((M + 63) // 64 * 64, budget // (3 * ld) // 64 * 64))
     g = t.empty((4, ld, ld), dtype=t.int32, device=nat.device())
     st = nat.zeros((1,), "int32")
+    if os.environ.get("CULSH_GSM_DEBUG"):
+        print(f"_gsm_count: free={free / 2**30:.1f} GiB rows/pass={mc} passes={-(-M // mc)}", file=sys.stderr)
     for m0 in range(0, M, mc):
         m1 = min(M, m0 + mc)
         w = (m1 - m0 + 63) // 64 * 64

@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-CULSH_GSM_DEBUG=1 timeout 600 python tools/gsm_phases.py c3 8 > gpurun_out/gsmp_c3.log 2>&1; echo p=$?
-CULSH_GSM_DEBUG=1 CULSH_GSM_SYNC=0,0 timeout 600 python tools/gsm_phases.py c3 5 > gpurun_out/gsmp_c3_nosync.log 2>&1; echo p=$?
-CULSH_GSM_DEBUG=1 CULSH_GSM_SYNC=256,4 timeout 600 python tools/gsm_phases.py c3 6 > gpurun_out/gsmp_c3_256_4.log 2>&1; echo p=$?
+for s in "128,2" "256,4" "512,4" "256,8" "128,4" "64,8"; do
+  CULSH_GSM_SYNC=$s timeout 600 python tools/gsm_phases.py c3 6 > gpurun_out/gsmq_c3_$s.log 2>&1; echo $s $?
+done
+timeout 900 python tools/occupancy_probe.py > gpurun_out/occupancy.log 2>&1; echo occ=$?
