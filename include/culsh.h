@@ -343,6 +343,19 @@ int culsh_append_csc2csr(const CulshData *d, int64_t n_old_cols, const int64_t *
  * exact, hence order-independent, for integer-valued ratings). */
 int culsh_segment_sums(int64_t n, const int64_t *ptr, const double *val, double *out, void *stream);
 
+/* compute_baselines (data.py:289-309) in the reference's summation order for ANY values.
+ * pairwise_chunks: out[c] = numpy's pairwise sum (np.add.reduce, 8-accumulator leaves of
+ * <= 128, halving splits rounded down to multiples of 8) of x[off[c] .. off[c] + len[c]),
+ * each chunk a node of the whole array's split tree with len <= 65,536 (the caller splits
+ * the top of the tree the same way and combines the chunk sums).
+ * ordered_segment_sums: out[s] = (init ? init[s] : 0.0) + val[order[ptr[s]]] + ... one by one
+ * in order (np.add.at's sequential accumulation with entries grouped stably by row or
+ * column; order NULL = identity). */
+int culsh_pairwise_chunks(const double *x, const int64_t *off, const int64_t *len, int64_t nchunks,
+                          double *out, void *stream);
+int culsh_ordered_segment_sums(int64_t n, const int64_t *ptr, const int64_t *order, const double *val,
+                               const double *init, double *out, void *stream);
+
 /* ------------------------------------------------------- similarity --- */
 
 /* Exact GSM top-K by the merge route (similarity.py:164-185 _gsm_topk_kernel):

@@ -118,6 +118,8 @@ _SIGS = {
     "culsh_append_segments": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "culsh_append_csc2csr": [_P(CulshData), _i64, _vp, _vp, _vp, _i64, _vp, _vp],
     "culsh_segment_sums": [_i64, _vp, _vp, _vp, _vp],
+    "culsh_pairwise_chunks": [_vp, _vp, _vp, _i64, _vp, _vp],
+    "culsh_ordered_segment_sums": [_i64, _vp, _vp, _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {"culsh_last_error": ctypes.c_char_p, "culsh_version": ctypes.c_char_p,
              "culsh_split_holdout": ctypes.c_int64}

@@ -271,8 +271,9 @@ class DeviceSparseRatings:
 
     Same role as SparseRatings for the GPU entry points (``device()``,
     ``baselines()``, ``M``/``N``/``nnz``); both index views are built by device
-    sorts.  Baselines are computed on the device; for integer-valued ratings they
-    are bit-identical to compute_baselines (every summation order is exact).
+    sorts.  Baselines are computed on the device in the reference's summation order
+    (exact_baselines_device), so they are bit-identical to compute_baselines of the same
+    triplets for any values.
     """
 
     def __init__(self, M: int, N: int, rows, cols, vals):
@@ -282,20 +283,17 @@ class DeviceSparseRatings:
         rows = rows.to(t.int32)
         cols = cols.to(t.int32)
         vals = vals.to(t.float64)
-        o = t.argsort(cols.long() * M + rows.long())
-        crow, ccol, cval = rows[o].contiguous(), cols[o], vals[o].contiguous()
-        col_ptr = t.zeros(N + 1, dtype=t.int64, device=d)
-        col_ptr[1:] = t.cumsum(t.bincount(ccol, minlength=N), 0)
-        o2 = t.argsort(rows.long() * N + cols.long())
-        row_ptr = t.zeros(M + 1, dtype=t.int64, device=d)
-        row_ptr[1:] = t.cumsum(t.bincount(rows, minlength=M), 0)
-        mu = float(vals.sum().item()) / max(self.nnz, 1)
-        rs = t.zeros(M, dtype=t.float64, device=d).index_add_(0, rows.long(), vals)
-        cs = t.zeros(N, dtype=t.float64, device=d).index_add_(0, cols.long(), vals)
-        rc = t.bincount(rows, minlength=M).double()
-        cc = t.bincount(cols, minlength=N).double()
-        bb = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
-        bh = t.where(cc > 0, cs / cc.clamp(min=1) - mu, t.zeros_like(cs))
+        ckey = cols.long() * M + rows.long()
+        ckey, o = t.sort(ckey)
+        crow, cval = rows[o].contiguous(), vals[o].contiguous()
+        col_ptr = t.searchsorted(ckey, t.arange(N + 1, device=d, dtype=t.int64) * M)
+        rkey, o2 = t.sort(rows.long() * N + cols.long())
+        row_ptr = t.searchsorted(rkey, t.arange(M + 1, device=d, dtype=t.int64) * N)
+        del ckey, rkey
+        if self.nnz:
+            mu, bb, bh = exact_baselines_device(M, N, rows, cols, vals)
+        else:
+            mu, bb, bh = 0.0, t.zeros(M, dtype=t.float64, device=d), t.zeros(N, dtype=t.float64, device=d)
         self._dev = DeviceRatings.from_device(M, N, col_ptr, crow, cval, row_ptr,
                                               cols[o2].contiguous(), vals[o2].contiguous(), mu, bb, bh)
         self._stats = BaselineStats(mu, nat.to_host(bb), nat.to_host(bh))
@@ -386,6 +384,74 @@ class DeviceRatings:
         self.base_b = nat.to_dev(b, np.float64)
         self.base_bhat = nat.to_dev(b_hat, np.float64)
         self.struct = self._make_struct()
+
+
+_PW_CHUNK = 1 << 16
+
+
+def pairwise_sum_device(x) -> float:
+    """numpy's np.add.reduce of a device float64 vector, bit for bit: the top of numpy's
+    pairwise split tree (halves rounded down to multiples of 8) is walked here down to nodes
+    of <= 65,536 elements, which culsh_pairwise_chunks sums on the device (thread per node,
+    the same tree below); the node sums are combined back up in the same order."""
+    n = int(x.numel())
+    offs, lens = [], []
+
+    def split(o, m):                      # leaves of the top tree, left to right
+        if m <= _PW_CHUNK:
+            offs.append(o)
+            lens.append(m)
+            return
+        m2 = m // 2
+        m2 -= m2 % 8
+        split(o, m2)
+        split(o + m2, m - m2)
+
+    if n == 0:
+        return 0.0
+    split(0, n)
+    part = nat.empty((len(offs),), "float64")
+    nat.call("culsh_pairwise_chunks", nat.ptr(x), nat.ptr(nat.to_dev(np.asarray(offs, np.int64))),
+             nat.ptr(nat.to_dev(np.asarray(lens, np.int64))), len(offs), nat.ptr(part), nat.stream_ptr())
+    vals = iter(nat.to_host(part).tolist())
+
+    def combine(m):
+        if m <= _PW_CHUNK:
+            return next(vals)
+        m2 = m // 2
+        m2 -= m2 % 8
+        left = combine(m2)
+        return left + combine(m - m2)     # Python float: IEEE double add
+
+    return combine(n)
+
+
+def _ordered_sums(n_seg: int, keys, vals, init=None):
+    """Per-segment sums of vals grouped by keys (int32 device, 0 <= key < n_seg), each in
+    entry order (a stable sort), as np.add.at(zeros, keys, vals) + init."""
+    t = nat.torch()
+    sk, order = t.sort(keys.to(t.int64), stable=True)
+    ptr = t.searchsorted(sk, t.arange(n_seg + 1, device=sk.device, dtype=t.int64))
+    out = nat.empty((max(n_seg, 1),), "float64")
+    nat.call("culsh_ordered_segment_sums", n_seg, nat.ptr(ptr), nat.ptr(order), nat.ptr(vals), nat.ptr(init),
+             nat.ptr(out), nat.stream_ptr())
+    cnt = (ptr[1:] - ptr[:-1]).to(t.float64)
+    return out[:n_seg], cnt
+
+
+def exact_baselines_device(M: int, N: int, rows, cols, vals):
+    """compute_baselines (data.py:289-309) on the device for ANY values, bit-identical to
+    the host numpy: mu by numpy's pairwise mean, row / column sums sequential in entry order
+    (np.add.at), then sum / count - mu.  rows / cols / vals: device triplets in ENTRY order.
+    Returns (mu, b, b_hat) with b, b_hat device float64."""
+    t = nat.torch()
+    n = int(vals.numel())
+    mu = pairwise_sum_device(vals) / n
+    rs, rc = _ordered_sums(M, rows, vals)
+    cs, cc = _ordered_sums(N, cols, vals)
+    bb = t.where(rc > 0, rs / rc.clamp(min=1) - mu, t.zeros_like(rs))
+    bh = t.where(cc > 0, cs / cc.clamp(min=1) - mu, t.zeros_like(cs))
+    return mu, bb, bh
 
 
 def device_baselines(M: int, N: int, col_ptr, col_vals, row_ptr, row_vals, nnz: int):

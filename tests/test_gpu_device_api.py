@@ -235,3 +235,40 @@ def test_train_set_rmse_large_tree_sum(P):
     a = P.rmse(p, t, r)
     b = P.rmse(p, P.Triplets(t.rows.copy(), t.cols.copy(), t.values.copy()), r)
     assert a == b and np.isfinite(a)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 127, 128, 129, 1000, 65536, 65537, 300001, 3_000_017])
+def test_pairwise_sum_device_equals_numpy(P, n):
+    """numpy's np.add.reduce (pairwise) restated on the device, bit for bit, across the leaf,
+    split and chunk-combine boundaries (values spread over 12 orders of magnitude)."""
+    from paper_2111_11682_b200 import _native as nat
+    from paper_2111_11682_b200.data import pairwise_sum_device
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n) * 10.0 ** rng.integers(-6, 6, n)
+    assert pairwise_sum_device(nat.to_dev(x)) == float(np.add.reduce(x))
+    assert pairwise_sum_device(nat.to_dev(x)) / n == float(x.mean())
+
+
+def test_device_sparse_ratings_real_values_exact_baselines(P):
+    """DeviceSparseRatings from device triplets in arbitrary entry order, real values:
+    mu, b and b_hat equal compute_baselines of the same triplets byte for byte (numpy
+    pairwise mean, np.add.at in entry order), and the index views equal the host build."""
+    import torch
+    from paper_2111_11682_b200 import _native as nat
+    rng = np.random.default_rng(5)
+    M, N, nnz = 3000, 700, 120000
+    key = rng.choice(M * N, nnz, replace=False)          # random entry order, no duplicates
+    rows, cols = (key // N).astype(np.int32), (key % N).astype(np.int32)
+    vals = rng.random(nnz) * 4.7 + 0.3
+    host = P.SparseRatings(M, N, rows, cols, vals)
+    ref = host.baselines()
+    dsr = P.DeviceSparseRatings(M, N, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(),
+                                torch.from_numpy(vals).cuda())
+    got = dsr.baselines()
+    assert got.mu == ref.mu
+    assert got.b.tobytes() == ref.b.tobytes() and got.b_hat.tobytes() == ref.b_hat.tobytes()
+    d = dsr.device()
+    for name, want in (("col_ptr", host.col_ptr), ("col_rows", host.col_rows), ("col_vals", host.col_vals),
+                       ("row_ptr", host.row_ptr), ("row_cols", host.row_cols), ("row_vals", host.row_vals)):
+        n = len(want)
+        assert nat.to_host(getattr(d, name))[:n].tobytes() == np.ascontiguousarray(want).tobytes(), name
