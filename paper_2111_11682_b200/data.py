@@ -411,8 +411,10 @@ def pairwise_sum_device(x) -> float:
         return 0.0
     split(0, n)
     part = nat.empty((len(offs),), "float64")
-    nat.call("culsh_pairwise_chunks", nat.ptr(x), nat.ptr(nat.to_dev(np.asarray(offs, np.int64))),
-             nat.ptr(nat.to_dev(np.asarray(lens, np.int64))), len(offs), nat.ptr(part), nat.stream_ptr())
+    d_off = nat.to_dev(np.asarray(offs, np.int64))      # keep both alive until the kernel ran
+    d_len = nat.to_dev(np.asarray(lens, np.int64))
+    nat.call("culsh_pairwise_chunks", nat.ptr(x), nat.ptr(d_off), nat.ptr(d_len), len(offs), nat.ptr(part),
+             nat.stream_ptr())
     vals = iter(nat.to_host(part).tolist())
 
     def combine(m):
