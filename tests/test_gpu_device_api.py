@@ -262,8 +262,8 @@ def test_device_sparse_ratings_real_values_exact_baselines(P):
     vals = rng.random(nnz) * 4.7 + 0.3
     host = P.SparseRatings(M, N, rows, cols, vals)
     ref = host.baselines()
-    dsr = P.DeviceSparseRatings(M, N, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(),
-                                torch.from_numpy(vals).cuda())
+    dsr = P.DeviceSparseRatings(M, N, torch.from_numpy(rows.copy()).cuda(), torch.from_numpy(cols.copy()).cuda(),
+                                torch.from_numpy(vals.copy()).cuda())
     got = dsr.baselines()
     assert got.mu == ref.mu
     assert got.b.tobytes() == ref.b.tobytes() and got.b_hat.tobytes() == ref.b_hat.tobytes()
