@@ -265,6 +265,17 @@ int culsh_sgd_hogwild_epoch_packed(int64_t N_list, const int64_t *col_ptr, const
                                    CulshModel32 *m, const CulshRates *r, int flags, int max_warps,
                                    int *ticket, double *loss_out, int *status, void *stream);
 
+/* Stream cursors at the start of every work segment (once per work list): seg4[4t..4t+3] =
+ * {lo, hi | S << 40 (copied from seg2), compact-mask slot at lo (packed stream: mptr[j] +
+ * flagged entries of column j before lo), residual offset at lo | (2-byte records: row of
+ * the entry before lo) << 32}.  words / w16 / first_row / mptr describe the packed stream
+ * (mptr NULL: wide stream, mask = one MW-word mask per entry).  The epoch kernels take seg4
+ * with flags bit 4 (| bit 3) and skip the per-segment scan from the column start. */
+int culsh_segment_cursors(int64_t n_list, const int64_t *col_ptr, const int32_t *col_order,
+                          const int64_t *seg2, const uint32_t *words, const uint16_t *w16,
+                          const int32_t *first_row, const int64_t *mptr, const uint32_t *mask, int MW,
+                          int64_t *seg4, void *stream);
+
 /* 2-byte per-rating stream (rows without rotation): words[idx] = row delta from the
  * previous entry of the column (12 bits; 0 for the first) | value code (3 bits) |
  * has-explicit-neighbour (1 bit); first_row[j] = row of column j's first entry.

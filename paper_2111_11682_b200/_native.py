@@ -107,6 +107,7 @@ _SIGS = {
     "culsh_rmse_train": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f64, _f64, _f64, _vp, _vp, _vp],
     "culsh_synth_columns": [_i64, _i64, _i64, _vp, _u64, _vp, _vp, _vp],
     "culsh_pcg64_uniform": [_u64, _u64, _u64, _u64, _u64, _i64, _f64, _i32, _vp, _vp],
+    "culsh_segment_cursors": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp],
     "culsh_pack16": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     "culsh_sgd_hogwild_epoch_packed16": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                          _P(CulshModel32), _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],

@@ -256,9 +256,12 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         }
         float bh = BHv[j];
         const int64_t c_lo = col_ptr[j], c_hi = col_ptr[j + 1];
-        // entry range: per-ticket work segment (flags bit 3), per-column DSGD block, or the column
-        const int64_t lo = seg ? seg[(flags & 8) ? 2 * (int64_t)t : 2 * j] : c_lo;
-        int64_t hi = seg ? seg[(flags & 8) ? 2 * (int64_t)t + 1 : 2 * j + 1] : c_hi;
+        // entry range: per-ticket work segment (flags bit 3), per-column DSGD block, or the column;
+        // flags bit 4: work segments carry precomputed stream cursors at lo (stride 4:
+        // lo, hi | S << 40, compact-mask slot, residual offset | P16 row carry << 32)
+        const int sstride = (flags & 16) ? 4 : 2;
+        const int64_t lo = seg ? seg[(flags & 8) ? sstride * (int64_t)t : 2 * j] : c_lo;
+        int64_t hi = seg ? seg[(flags & 8) ? sstride * (int64_t)t + 1 : 2 * j + 1] : c_hi;
         // a work segment that is only part of its column runs concurrently with the column's
         // other S segments (S in bits 40-63 of its end): its column parameters are merged
         // back as atomic adds of (change / S) -- the average of the segments' changes
@@ -286,7 +289,15 @@ hogwild_kernel(int64_t N, const int64_t *__restrict__ col_ptr, const int64_t *__
         // Hogwild writes to the same u_i rare.
         const int rot = ((flags & 1) && n > 1) ? (int)(splitmix64((uint64_t)j ^ 0x5bd1e995ULL) % (uint64_t)n) : 0;
         int rrel2 = 0;   // residual offset (relative to the column base) at position lo
-        if (PACK && lo > c_lo) {   // work segment: mask cursor and residual offset at lo
+        if ((flags & 16) && lo > c_lo) {   // cursors from the plan (segment_cursors_kernel)
+            const int64_t c3 = seg[sstride * (int64_t)t + 3];
+            if constexpr (PACK) {
+                mrun2 = seg[sstride * (int64_t)t + 2];
+                mrun1 = mrun2;
+            }
+            rrel2 = (int)(uint32_t)(uint64_t)c3;
+            if constexpr (P16) carry = (int)((uint64_t)c3 >> 32);
+        } else if (PACK && lo > c_lo) {   // work segment: mask cursor and residual offset at lo
             int h = 0, dsum = 0;
 #pragma unroll 8   // independent loads: keep several in flight
             for (int64_t x = c_lo + lane; x < lo; x += 32) {
@@ -819,6 +830,53 @@ __global__ void explicit_mask_kernel(CulshData d, const int32_t *__restrict__ nb
     }
 }
 
+// Stream cursors at the start of every work segment (once per plan; the epoch kernel with
+// flags bit 4 reads them instead of scanning from its column's start every epoch -- that scan
+// made late DSGD stages, whose segments start deep in their columns, the slowest).  The same
+// arithmetic as the kernel's scan: number of flagged entries before lo (compact-mask slot),
+// popcount of their masks (residual offset), and for 2-byte records the row before lo.
+__global__ void segment_cursors_kernel(int64_t n_list, const int64_t *__restrict__ col_ptr,
+                                       const int32_t *__restrict__ col_order, const int64_t *__restrict__ seg2,
+                                       const uint32_t *__restrict__ words, const uint16_t *__restrict__ w16,
+                                       const int32_t *__restrict__ first_row, const int64_t *__restrict__ mptr,
+                                       const uint32_t *__restrict__ mask, int MW, int64_t *__restrict__ seg4) {
+    const unsigned lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < n_list; t += warps) {
+        const int64_t j = col_order[t];
+        const int64_t lo = seg2[2 * t], hi = seg2[2 * t + 1];
+        const int64_t c_lo = col_ptr[j];
+        int h = 0, dsum = 0, skip = 0;
+        int64_t m0 = mptr ? mptr[j] : 0;
+        if (mptr) {   // packed: flagged entries before lo, then their compact mask words
+            for (int64_t x = c_lo + lane; x < lo; x += 32) {
+                if (w16) {
+                    const uint32_t v = w16[x];
+                    h += (int)(v >> 15);
+                    dsum += (int)(v & 0xFFFu);
+                } else {
+                    h += (int)(words[x] >> 31);
+                }
+            }
+            h = warp_sum(h);
+            for (int64_t x = m0 + lane; x < m0 + h; x += 32)
+                for (int q = 0; q < MW; ++q) skip += __popc(mask[x * MW + q]);
+        } else {      // wide stream: a mask word (pair) per entry
+            for (int64_t x = c_lo + lane; x < lo; x += 32)
+                for (int q = 0; q < MW; ++q) skip += __popc(mask[x * MW + q]);
+        }
+        skip = warp_sum(skip);
+        dsum = warp_sum(dsum);
+        if (lane == 0) {
+            seg4[4 * t] = lo;
+            seg4[4 * t + 1] = hi;
+            seg4[4 * t + 2] = m0 + h;
+            const uint32_t carry = w16 ? (uint32_t)(first_row[j] + dsum) : 0u;
+            seg4[4 * t + 3] = (int64_t)(((uint64_t)carry << 32) | (uint32_t)skip);
+        }
+    }
+}
+
 // Row-major explicit-neighbour test (once per fit; replaces the column-pair merge above
 // when N <= 65,536 columns).  Warp per row i: the row's column set becomes an N-bit bitmap in
 // shared memory, and every entry (i, j) of the row tests its K neighbours J[j, k] with one
@@ -1102,6 +1160,22 @@ extern "C" int culsh_sgd_hogwild_epoch_packed16(int64_t N_list, const int64_t *c
     if (F == 128) return HWP(4);
     return HWP(8);
 #undef HWP
+}
+
+extern "C" int culsh_segment_cursors(int64_t n_list, const int64_t *col_ptr, const int32_t *col_order,
+                                     const int64_t *seg2, const uint32_t *words, const uint16_t *w16,
+                                     const int32_t *first_row, const int64_t *mptr, const uint32_t *mask, int MW,
+                                     int64_t *seg4, void *stream) {
+    CULSH_REQUIRE(MW == 1 || MW == 2, "MW must be 1 or 2");
+    CULSH_REQUIRE(!w16 || (mptr && first_row), "2-byte records need mptr and first_row");
+    CULSH_REQUIRE(!mptr || words || w16, "the packed stream needs its words");
+    if (n_list <= 0) return CULSH_OK;
+    const int64_t blocks = min64((n_list + 7) / 8, (int64_t)num_sms() * 16);
+    segment_cursors_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(n_list, col_ptr, col_order, seg2,
+                                                                               words, w16, first_row, mptr, mask,
+                                                                               MW, seg4);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
 }
 
 extern "C" int culsh_pack16(int64_t N, const int64_t *col_ptr, const int32_t *rows, const float *vals,

@@ -338,18 +338,40 @@ class HogwildTrainer:
         return {"n": int(len(order)), "col": nat.to_dev(cols_h[idx][order].astype(np.int32), np.int32),
                 "seg": nat.to_dev(sg.astype(np.int64), np.int64), "split_cols": int((nseg > 1).sum())}
 
+    def _seg_cursors(self, work: dict):
+        """The work list with each segment's stream cursors at its start (culsh_segment_cursors,
+        once per list, resident stream): [lo, hi | S << 40, mask slot, residual offset] per
+        ticket.  The epoch kernel (flags bit 4) then starts every segment without scanning its
+        column from the beginning -- the scan grew with the segment's depth in its column (late
+        DSGD stages, the tails of split columns)."""
+        if "seg4" not in work:
+            d = self.dev
+            seg4 = nat.empty((4 * max(work["n"], 1),), "int64")
+            pk = self.packed
+            if pk is not None:
+                nat.call("culsh_segment_cursors", work["n"], nat.ptr(d.col_ptr), nat.ptr(work["col"]),
+                         nat.ptr(work["seg"]), nat.ptr(pk["words"]), None, None, nat.ptr(pk["mptr"]),
+                         nat.ptr(pk["cmask"]), self.MW, nat.ptr(seg4), nat.stream_ptr())
+            else:
+                nat.call("culsh_segment_cursors", work["n"], nat.ptr(d.col_ptr), nat.ptr(work["col"]),
+                         nat.ptr(work["seg"]), None, None, None, None, nat.ptr(self.mask), self.MW,
+                         nat.ptr(seg4), nat.stream_ptr())
+            work["seg4"] = seg4
+        return work["seg4"]
+
     def launch_work(self, t_epoch: int, work: dict) -> None:
         """Enqueue one block_work list (no host synchronisation)."""
         rates = self._rates(t_epoch)
+        seg4 = self._seg_cursors(work)
         if self.packed is not None:
             self._launch_packed(work["n"], self._stream_buffers(resident=True), work["col"], rates, self.loss,
-                                work["seg"])
+                                seg4, cursors=True)
             return
         d = self.dev
-        nat.call("culsh_sgd_hogwild_epoch", work["n"], nat.ptr(d.col_ptr), nat.ptr(work["seg"]),
+        nat.call("culsh_sgd_hogwild_epoch", work["n"], nat.ptr(d.col_ptr), nat.ptr(seg4),
                  nat.ptr(d.col_rows), nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
                  nat.ptr(self.resid), nat.ptr(work["col"]), ctypes.byref(self.model.struct),
-                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0) | 8,
+                 ctypes.byref(rates), int(self.rotate) | (2 if self.atomic_rows else 0) | 8 | 16,
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(self.loss), nat.ptr(self.status),
                  nat.stream_ptr())
 
@@ -386,9 +408,10 @@ class HogwildTrainer:
         n = d.N if n_cols is None else n_cols
         wflag = 0
         if seg is None and col_order is None and self.work is not None:
-            order, seg, n, wflag = self.work["col"], self.work["seg"], self.work["n"], 8
+            order, seg, n, wflag = self.work["col"], self._seg_cursors(self.work), self.work["n"], 8 | 16
         if self.packed is not None and (seg is None or wflag):
-            self._launch_packed(n, self._stream_buffers(resident=True), order, rates, self.loss, seg)
+            self._launch_packed(n, self._stream_buffers(resident=True), order, rates, self.loss, seg,
+                                cursors=bool(wflag & 16))
             return
         nat.call("culsh_sgd_hogwild_epoch", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(d.col_rows),
                  nat.ptr(self.vals32), nat.ptr(self.mask), nat.ptr(self.resid_ptr),
@@ -399,11 +422,15 @@ class HogwildTrainer:
                  nat.ptr(self.loss),
                  nat.ptr(self.status), nat.stream_ptr())
 
-    def _launch_packed(self, n, bufs, order, rates, loss, seg=None) -> None:
-        """Packed-stream epoch over ``bufs`` (the _stream_buffers() layout)."""
+    def _launch_packed(self, n, bufs, order, rates, loss, seg=None, cursors: bool = False) -> None:
+        """Packed-stream epoch over ``bufs`` (the _stream_buffers() layout); ``cursors``: seg is
+        a _seg_cursors list (4-byte records only)."""
         pk, d = self.packed, self.dev
-        flags = int(self.rotate) | (2 if self.atomic_rows else 0) | (8 if seg is not None else 0)
+        flags = (int(self.rotate) | (2 if self.atomic_rows else 0) | (8 if seg is not None else 0) |
+                 (16 if cursors else 0))
         if len(bufs) == 4:   # 2-byte records
+            if cursors:
+                raise ValueError("segment cursors are built for the resident 4-byte records")
             w16, first_row, cmask, resid = bufs
             nat.call("culsh_sgd_hogwild_epoch_packed16", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(w16),
                      nat.ptr(first_row), nat.ptr(pk["lut"]), nat.ptr(pk["mptr"]), nat.ptr(cmask),
@@ -414,8 +441,7 @@ class HogwildTrainer:
         words, cmask, resid = bufs
         nat.call("culsh_sgd_hogwild_epoch_packed", n, nat.ptr(d.col_ptr), nat.ptr(seg), nat.ptr(words),
                  nat.ptr(pk["lut"]), nat.ptr(pk["mptr"]), nat.ptr(cmask), nat.ptr(self.resid_ptr), nat.ptr(resid),
-                 nat.ptr(order), ctypes.byref(self.model.struct), ctypes.byref(rates),
-                 int(self.rotate) | (2 if self.atomic_rows else 0) | (8 if seg is not None else 0),
+                 nat.ptr(order), ctypes.byref(self.model.struct), ctypes.byref(rates), flags,
                  int(self.max_warps), nat.ptr(self.ticket), nat.ptr(loss), nat.ptr(self.status),
                  nat.stream_ptr())
 

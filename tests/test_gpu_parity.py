@@ -473,29 +473,33 @@ class TestPackedStream:
         from paper_2111_11682_b200.hogwild import HogwildTrainer
         r, tbl, cfg = self._problem(P, 16, M=900, N=40, dens=0.3)
         out = []
-        for packed in (True, False):
-            tr = HogwildTrainer(r, tbl, cfg, packed=packed, split_cap=50)
+        # packed / wide stream x cursor scan in the kernel / precomputed segment cursors
+        for packed, cursors in ((True, False), (True, True), (False, False), (False, True)):
+            tr = HogwildTrainer(r, tbl, cfg, packed=packed, split_cap=50, p16=False)
             wk = tr.work
             assert wk is not None and wk["split_cols"] > 0
+            seg4 = tr._seg_cursors(wk) if cursors else None
             for ep in range(2):
                 rates = _rates_struct(cfg.rates_at(ep), cfg.regs)
                 for s_ in range(wk["n"]):
-                    col, seg = wk["col"][s_:s_ + 1], wk["seg"][2 * s_:2 * s_ + 2]
+                    col = wk["col"][s_:s_ + 1]
+                    seg = seg4[4 * s_:4 * s_ + 4] if cursors else wk["seg"][2 * s_:2 * s_ + 2]
                     if packed:
-                        pk = tr.packed
-                        tr._launch_packed(1, tr._stream_buffers(), col, rates, tr.loss, seg)
+                        tr._launch_packed(1, tr._stream_buffers(resident=True), col, rates, tr.loss, seg,
+                                          cursors=cursors)
                     else:
                         d = tr.dev
                         nat.call("culsh_sgd_hogwild_epoch", 1, nat.ptr(d.col_ptr), nat.ptr(seg),
                                  nat.ptr(d.col_rows), nat.ptr(tr.vals32), nat.ptr(tr.mask),
                                  nat.ptr(tr.resid_ptr), nat.ptr(tr.resid), nat.ptr(col),
-                                 ctypes.byref(tr.model.struct), ctypes.byref(rates), 2 | 8, 0,
+                                 ctypes.byref(tr.model.struct), ctypes.byref(rates),
+                                 2 | 8 | (16 if cursors else 0), 0,
                                  nat.ptr(tr.ticket), nat.ptr(tr.loss), nat.ptr(tr.status), nat.stream_ptr())
             torch.cuda.synchronize()
             out.append(tr.to_params())
-        a, b = out
-        for name in ("b", "b_hat", "U", "V", "W", "C"):
-            assert getattr(a, name).tobytes() == getattr(b, name).tobytes(), name
+        for b in out[1:]:
+            for name in ("b", "b_hat", "U", "V", "W", "C"):
+                assert getattr(out[0], name).tobytes() == getattr(b, name).tobytes(), name
 
     def test_work_segments_train(self, P):
         """Concurrent epochs with split columns still train (same data, same epochs).  A
