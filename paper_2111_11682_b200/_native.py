@@ -250,11 +250,23 @@ def call(name: str, *args) -> int:
     return st
 
 
-def ptr(t) -> ctypes.c_void_p:
-    """Device pointer of a torch tensor (None -> NULL)."""
+def ptr(t, offset: int = 0) -> ctypes.c_void_p:
+    """Device pointer of a torch tensor (None -> NULL), optionally ``offset`` elements in."""
     if t is None:
         return ctypes.c_void_p(0)
-    return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(t.data_ptr() + offset * t.element_size())
+
+
+_side = {}
+
+
+def side_stream(name: str):
+    """A named, reused side stream on the current device (stage overlap inside one call)."""
+    t = torch()
+    key = (name, t.cuda.current_device())
+    if key not in _side:
+        _side[key] = t.cuda.Stream()
+    return _side[key]
 
 
 _NP2T = {np.dtype(np.int32): "int32", np.dtype(np.int64): "int64", np.dtype(np.float64): "float64",

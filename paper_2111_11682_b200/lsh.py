@@ -327,7 +327,12 @@ def _psi_int(v: float, e: int):
     return int(p) if float(p).is_integer() and abs(p) < 2 ** 20 else None
 
 
-def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, keys_ld) -> bool:
+_PIPE_CHUNKS = 4        # class-partition / bit-count pipeline depth (column chunks by nnz)
+_PIPE_MIN_COLS = 1024
+
+
+def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, keys_ld,
+                table_ready=None) -> bool:
     """Harley-Seal bit-count kernel (exact integers) when the data allow it."""
     W8 = c.q * c.p * _ns(c.G)
     if W8 % 4 or W8 > 512 or dev.nnz == 0:
@@ -338,23 +343,68 @@ def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, key
     psi = [_psi_int(float(v), c.psi_exponent) for v in classes]
     if any(x is None for x in psi):
         return False
-    rows_bc, off = _class_partition(dev, classes)
     cpsi = nat.to_dev(np.asarray(psi, np.int32))
-    nat.call("culsh_hash_count", nat.ptr(dev.col_ptr), nat.ptr(rows_bc), nat.ptr(off), len(classes),
-             nat.ptr(cpsi), dev.M, int(_SLICE_MB), int(_COUNT_VARIANT), col_begin, n_cols, nat.ptr(table),
-             c.q, c.p, c.G,
-             nat.ptr(acc),
-             nat.ptr(sig), nat.ptr(keys), dev.N if keys_ld is None else keys_ld, nat.stream_ptr())
+
+    def count(c0, nc):
+        nat.call("culsh_hash_count", nat.ptr(dev.col_ptr), nat.ptr(rows_bc), nat.ptr(off), len(classes),
+                 nat.ptr(cpsi), dev.M, int(_SLICE_MB), int(_COUNT_VARIANT), c0, nc, nat.ptr(table),
+                 c.q, c.p, c.G, nat.ptr(acc), nat.ptr(sig), nat.ptr(keys),
+                 dev.N if keys_ld is None else keys_ld, nat.stream_ptr())
+
+    t = nat.torch()
+    main = t.cuda.current_stream()
+    if getattr(dev, "_class_part", None) is not None or n_cols < 4 * _PIPE_MIN_COLS:
+        rows_bc, off = _class_partition(dev, classes)
+        if table_ready is not None:
+            main.wait_event(table_ready)
+        count(col_begin, n_cols)
+        return True
+    # Pipelined: the class partition of column chunk k+1 (memory-bound, side stream) runs
+    # under the bit-count kernel of chunk k (gather-latency-bound, 41 % warps active), and the
+    # first chunk waits only for its own partition and the row-hash table.
+    NC = len(classes)
+    cv = nat.to_dev(np.asarray(classes, np.float64))
+    rows_bc = nat.empty((max(dev.nnz, 1),), "int32")
+    off = nat.empty(((NC + 1) * max(dev.N, 1),), "int32")
+    cp = dev.col_ptr
+    lo_nnz, hi_nnz = int(cp[col_begin].item()), int(cp[col_begin + n_cols].item())
+    targets = t.tensor([lo_nnz + (hi_nnz - lo_nnz) * k // _PIPE_CHUNKS for k in range(1, _PIPE_CHUNKS)],
+                       device=cp.device, dtype=t.int64)
+    cuts = [col_begin] + sorted(set(min(max(int(x), col_begin), col_begin + n_cols) for x in
+                                    t.searchsorted(cp[col_begin:col_begin + n_cols + 1], targets).add_(col_begin)
+                                    .tolist())) + [col_begin + n_cols]
+    cuts = sorted(set(cuts))
+    side = nat.side_stream("class_partition")
+    side.wait_stream(main)
+    done = []
+    with t.cuda.stream(side):
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            nat.call("culsh_class_partition", nat.ptr(cp, a), nat.ptr(dev.col_rows), nat.ptr(dev.col_vals), b - a,
+                     nat.ptr(cv), NC, nat.ptr(rows_bc), nat.ptr(off, a * (NC + 1)), nat.stream_ptr())
+            ev = t.cuda.Event()
+            ev.record(side)
+            done.append(ev)
+    for x in (rows_bc, off, cv):
+        x.record_stream(main)
+    if table_ready is not None:
+        main.wait_event(table_ready)
+    for (a, b), ev in zip(zip(cuts[:-1], cuts[1:]), done):
+        main.wait_event(ev)
+        count(a, b - a)
+    if col_begin == 0 and n_cols == dev.N:   # cache only a partition of every column
+        dev._class_part = (rows_bc, off)
     return True
 
 
 def _accumulate(dev, table, c: LshConfig, acc, sig, keys, col_begin: int, n_cols: int,
                 col_list=None, into: bool = False, keys_ld: int | None = None,
-                allow_count: bool = True) -> None:
+                allow_count: bool = True, table_ready=None) -> None:
     int_path = (not into) and _int_path_ok(dev, col_begin, n_cols, col_list, c.psi_exponent)
     if int_path and col_list is None and allow_count:
-        if _count_path(dev, table, c, acc, sig, keys, col_begin, n_cols, keys_ld):
+        if _count_path(dev, table, c, acc, sig, keys, col_begin, n_cols, keys_ld, table_ready):
             return
+    if table_ready is not None:
+        nat.torch().cuda.current_stream().wait_event(table_ready)
     nat.call("culsh_hash_accumulate", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
              nat.ptr(dev.col_vals), col_begin, n_cols, nat.ptr(col_list), nat.ptr(table), c.q, c.p,
              c.G, c.psi_exponent, int(into), int(int_path), nat.ptr(acc), nat.ptr(sig),
@@ -379,15 +429,28 @@ def compute_hash_state(ratings: SparseRatings, config: LshConfig,
 def hash_state_device(dev, config: LshConfig, hashes: RowHashes | None = None) -> HashState:
     """compute_hash_state on HBM-resident ratings (a DeviceRatings)."""
     config.validate()
+    t = nat.torch()
+    table_ready = None
     if hashes is None:
-        hashes = assign_row_hashes(dev.M, config)
+        # the row-hash table depends only on (seed, M): generate it on a side stream under the
+        # value-set / class-partition passes; the accumulate waits for it
+        main = t.cuda.current_stream()
+        side = nat.side_stream("row_hashes")
+        side.wait_stream(main)
+        with t.cuda.stream(side):
+            hashes = assign_row_hashes(dev.M, config)
+            table_ready = t.cuda.Event()
+            table_ready.record(side)
+        hashes.table().record_stream(main)
     N, c = dev.N, config
     W = c.q * c.p * c.G
     acc = nat.empty((max(N * W, 1),), "float64")
     sig = nat.empty((max(N * W, 1),), "uint8")
     keys = nat.empty((c.q * max(N, 1),), "uint64")
     if N:
-        _accumulate(dev, hashes.table(), c, acc, sig, keys, 0, N)
+        _accumulate(dev, hashes.table(), c, acc, sig, keys, 0, N, table_ready=table_ready)
+    elif table_ready is not None:
+        t.cuda.current_stream().wait_event(table_ready)
     return HashState(config=config, _dev_acc=acc, _dev_sig=sig, _dev_keys=keys,
                      _shape=(N, c.q, c.p, c.G))
 
