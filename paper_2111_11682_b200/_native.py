@@ -254,7 +254,9 @@ def ptr(t, offset: int = 0) -> ctypes.c_void_p:
     """Device pointer of a torch tensor (None -> NULL), optionally ``offset`` elements in."""
     if t is None:
         return ctypes.c_void_p(0)
-    return ctypes.c_void_p(t.data_ptr() + offset * t.element_size())
+    if offset:
+        return ctypes.c_void_p(t.data_ptr() + offset * t.element_size())
+    return ctypes.c_void_p(t.data_ptr())   # (also accepts pointer-only stand-ins, dsgd._Offset)
 
 
 _side = {}

@@ -327,10 +327,6 @@ def _psi_int(v: float, e: int):
     return int(p) if float(p).is_integer() and abs(p) < 2 ** 20 else None
 
 
-_PIPE_CHUNKS = 4        # class-partition / bit-count pipeline depth (column chunks by nnz)
-_PIPE_MIN_COLS = 1024
-
-
 def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, keys_ld,
                 table_ready=None) -> bool:
     """Harley-Seal bit-count kernel (exact integers) when the data allow it."""
@@ -351,58 +347,23 @@ def _count_path(dev, table, c: LshConfig, acc, sig, keys, col_begin, n_cols, key
                  c.q, c.p, c.G, nat.ptr(acc), nat.ptr(sig), nat.ptr(keys),
                  dev.N if keys_ld is None else keys_ld, nat.stream_ptr())
 
-    t = nat.torch()
-    main = t.cuda.current_stream()
-    if getattr(dev, "_class_part", None) is not None or n_cols < 4 * _PIPE_MIN_COLS:
-        rows_bc, off = _class_partition(dev, classes)
-        if table_ready is not None:
-            main.wait_event(table_ready)
-        count(col_begin, n_cols)
-        return True
-    # Pipelined: the class partition of column chunk k+1 (memory-bound, side stream) runs
-    # under the bit-count kernel of chunk k (gather-latency-bound, 41 % warps active), and the
-    # first chunk waits only for its own partition and the row-hash table.
-    NC = len(classes)
-    cv = nat.to_dev(np.asarray(classes, np.float64))
-    rows_bc = nat.empty((max(dev.nnz, 1),), "int32")
-    off = nat.empty(((NC + 1) * max(dev.N, 1),), "int32")
-    cp = dev.col_ptr
-    lo_nnz, hi_nnz = int(cp[col_begin].item()), int(cp[col_begin + n_cols].item())
-    targets = t.tensor([lo_nnz + (hi_nnz - lo_nnz) * k // _PIPE_CHUNKS for k in range(1, _PIPE_CHUNKS)],
-                       device=cp.device, dtype=t.int64)
-    cuts = [col_begin] + sorted(set(min(max(int(x), col_begin), col_begin + n_cols) for x in
-                                    t.searchsorted(cp[col_begin:col_begin + n_cols + 1], targets).add_(col_begin)
-                                    .tolist())) + [col_begin + n_cols]
-    cuts = sorted(set(cuts))
-    side = nat.side_stream("class_partition")
-    side.wait_stream(main)
-    done = []
-    with t.cuda.stream(side):
-        for a, b in zip(cuts[:-1], cuts[1:]):
-            nat.call("culsh_class_partition", nat.ptr(cp, a), nat.ptr(dev.col_rows), nat.ptr(dev.col_vals), b - a,
-                     nat.ptr(cv), NC, nat.ptr(rows_bc), nat.ptr(off, a * (NC + 1)), nat.stream_ptr())
-            ev = t.cuda.Event()
-            ev.record(side)
-            done.append(ev)
-    for x in (rows_bc, off, cv):
-        x.record_stream(main)
+    # (pipelining the class partition by column chunks on a side stream under the bit-count
+    # kernel was measured slower: 10.7 vs 10.1 ms at C3 -- the concurrent partition slows the
+    # gather-bound count kernel more than it hides)
+    rows_bc, off = _class_partition(dev, classes)
     if table_ready is not None:
-        main.wait_event(table_ready)
-    for (a, b), ev in zip(zip(cuts[:-1], cuts[1:]), done):
-        main.wait_event(ev)
-        count(a, b - a)
-    if col_begin == 0 and n_cols == dev.N:   # cache only a partition of every column
-        dev._class_part = (rows_bc, off)
+        nat.torch().cuda.current_stream().wait_event(table_ready)
+    count(col_begin, n_cols)
     return True
 
 
 def _accumulate(dev, table, c: LshConfig, acc, sig, keys, col_begin: int, n_cols: int,
                 col_list=None, into: bool = False, keys_ld: int | None = None,
                 allow_count: bool = True, table_ready=None) -> None:
+    if not into and col_list is None and allow_count and _count_path(dev, table, c, acc, sig, keys, col_begin,
+                                                                     n_cols, keys_ld, table_ready):
+        return   # (its value classes all have integer psi: no separate integer check needed)
     int_path = (not into) and _int_path_ok(dev, col_begin, n_cols, col_list, c.psi_exponent)
-    if int_path and col_list is None and allow_count:
-        if _count_path(dev, table, c, acc, sig, keys, col_begin, n_cols, keys_ld, table_ready):
-            return
     if table_ready is not None:
         nat.torch().cuda.current_stream().wait_event(table_ready)
     nat.call("culsh_hash_accumulate", nat.ptr(dev.col_ptr), nat.ptr(dev.col_rows),
