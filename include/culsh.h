@@ -367,6 +367,28 @@ int culsh_pairwise_chunks(const double *x, const int64_t *off, const int64_t *le
 int culsh_ordered_segment_sums(int64_t n, const int64_t *ptr, const int64_t *order, const double *val,
                                const double *init, double *out, void *stream);
 
+/* ------------------------------------------------- DSGD peer ring --- */
+
+/* Ring shift of the moving DSGD block over peer memory (parallel.py:166-227's block hand-
+ * over between workers; dsgd.PeerRing).  ring_alloc: this rank's buffer (64 u64 flags +
+ * two data slots of slot_bytes) via cudaMalloc, with its CUDA IPC handle (handle_bytes()
+ * bytes) for the neighbours; ring_open / ring_close map / unmap a neighbour's buffer.
+ * ring_push (after stage s): once the receiver acknowledged slot seq & 1's previous use
+ * (seq - 2), copy the n block pieces (ptrs / bytes, at 16-byte-aligned slot offsets offs)
+ * into the receiver's slot and release receiver.ready[seq & 1] = seq (system scope).
+ * ring_pull: wait on the device for my.ready[seq & 1] >= seq, copy the slot's pieces into
+ * ptrs, release sender.ack[seq & 1] = seq.  Stream-ordered, no host synchronisation; a
+ * flag wait longer than 20 s sets *status |= 4. */
+int culsh_ring_alloc(int64_t slot_bytes, void **buf, void *ipc_handle_out);
+int culsh_ring_open(const void *ipc_handle, void **buf);
+int culsh_ring_close(void *peer_buf);
+int culsh_ring_free(void *buf);
+int culsh_ring_handle_bytes(void);
+int culsh_ring_push(int n, void *const *ptrs, const int64_t *bytes, const int64_t *offs, void *my_buf,
+                    void *peer_buf, int64_t slot_bytes, uint64_t seq, int *status, void *stream);
+int culsh_ring_pull(int n, void *const *ptrs, const int64_t *bytes, const int64_t *offs, void *my_buf,
+                    void *sender_buf, int64_t slot_bytes, uint64_t seq, int *status, void *stream);
+
 /* ------------------------------------------------------- similarity --- */
 
 /* Exact GSM top-K by the merge route (similarity.py:164-185 _gsm_topk_kernel):

@@ -107,6 +107,13 @@ _SIGS = {
     "culsh_rmse_train": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f64, _f64, _f64, _vp, _vp, _vp],
     "culsh_synth_columns": [_i64, _i64, _i64, _vp, _u64, _vp, _vp, _vp],
     "culsh_pcg64_uniform": [_u64, _u64, _u64, _u64, _u64, _i64, _f64, _i32, _vp, _vp],
+    "culsh_ring_alloc": [_i64, _vp, _vp],
+    "culsh_ring_open": [_vp, _vp],
+    "culsh_ring_close": [_vp],
+    "culsh_ring_free": [_vp],
+    "culsh_ring_handle_bytes": [],
+    "culsh_ring_push": [_i32, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_uint64, _vp, _vp],
+    "culsh_ring_pull": [_i32, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_uint64, _vp, _vp],
     "culsh_segment_cursors": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp],
     "culsh_pack16": [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     "culsh_sgd_hogwild_epoch_packed16": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -307,6 +307,75 @@ def simlsh_topk_sharded(dev, config, K: int, rank: int, D: int, group=None):
     return full2.reshape(-1), ncand
 
 
+class PeerRing:
+    """The ring shift as device-side peer-memory traffic (csrc/ring.cu): after stage s each
+    rank's push kernel writes the block it trained straight into the next rank's receive
+    slot (CUDA IPC mapping: NVLink P2P stores between GPUs) and raises a system-scope ready
+    flag there; the next rank's pull kernel waits for the flag on the device, copies the block
+    into its parameter arrays and acknowledges in the sender's memory.  Stage kernel -> push ->
+    pull -> next stage are stream-ordered on every rank; no NCCL call and no host
+    synchronisation between stages.  Same blocks and order as ring_shift, so the result is the
+    same bytes (exact mode == parallel_train(D))."""
+
+    def __init__(self, plan: RingPlan, rank: int, tensors, group=None):
+        import ctypes
+        import torch.distributed as dist
+        from . import _native as nat
+        self.plan, self.rank, self.tensors = plan, rank, [t for t in tensors if t.numel()]
+        span = max(plan.moving_span(b).stop - plan.moving_span(b).start for b in range(plan.D))
+        self.offs, off = [], 0
+        for t in self.tensors:
+            self.offs.append(off)
+            row_bytes = (t[0].numel() if t.dim() > 1 else 1) * t.element_size()
+            off += (span * row_bytes + 15) // 16 * 16
+        self.slot = max(off, 16)
+        hb = nat.load_library().culsh_ring_handle_bytes()
+        handle = ctypes.create_string_buffer(hb)
+        buf = ctypes.c_void_p()
+        nat.call("culsh_ring_alloc", self.slot, ctypes.byref(buf), handle)
+        self.buf = buf
+        handles = [None] * plan.D
+        dist.all_gather_object(handles, bytes(handle.raw), group=group)
+        self.peers = {}
+        for q in {plan.send_peer(rank), plan.recv_peer(rank)}:
+            pb = ctypes.c_void_p()
+            nat.call("culsh_ring_open", ctypes.create_string_buffer(handles[q], hb), ctypes.byref(pb))
+            self.peers[q] = pb
+        self.status = nat.zeros((1,), "int32")
+        self.seq = 0
+
+    def _pieces(self, span):
+        import ctypes
+        n = len(self.tensors)
+        views = [t[span] for t in self.tensors]
+        ptrs = (ctypes.c_void_p * n)(*[v.data_ptr() for v in views])
+        nbytes = (ctypes.c_int64 * n)(*[v.numel() * v.element_size() for v in views])
+        offs = (ctypes.c_int64 * n)(*self.offs)
+        return n, ptrs, nbytes, offs
+
+    def shift(self, stage: int) -> None:
+        """Enqueue the shift after `stage` (push of its block, pull of the next one)."""
+        from . import _native as nat
+        p, r = self.plan, self.rank
+        self.seq += 1
+        send = p.moving_span(p.moving_block(r, stage))
+        recv = p.moving_span(p.moving_block(r, stage + 1))
+        n, ptrs, nb, offs = self._pieces(send)
+        nat.call("culsh_ring_push", n, ptrs, nb, offs, self.buf, self.peers[p.send_peer(r)], self.slot, self.seq,
+                 nat.ptr(self.status), nat.stream_ptr())
+        n, ptrs, nb, offs = self._pieces(recv)
+        nat.call("culsh_ring_pull", n, ptrs, nb, offs, self.buf, self.peers[p.recv_peer(r)], self.slot, self.seq,
+                 nat.ptr(self.status), nat.stream_ptr())
+
+    def close(self) -> None:
+        from . import _native as nat
+        nat.torch().cuda.synchronize()
+        for pb in self.peers.values():
+            nat.call("culsh_ring_close", pb)
+        nat.call("culsh_ring_free", self.buf)
+        self.peers = {}
+
+
 # ------------------------------------------------------------- the trainer ---
 
 class DistTrainer:
@@ -319,15 +388,20 @@ class DistTrainer:
     launches (csrc/sgd_hogwild.cu), the performance mode."""
 
     def __init__(self, shard, plan: RingPlan, rank: int, neighbors, config, baselines, mode: str = "exact",
-                 parts: int = 1, group=None):
+                 parts: int = 1, group=None, exchange: str = "collective"):
         from . import _native as nat
         from .factorization import DeviceModel64, _check_model_dims, pcg64_uniform_device
         from .hogwild import DeviceModel32, HogwildTrainer
         t = nat.torch()
         if mode not in ("exact", "hogwild"):
             raise ValueError(f"unknown mode {mode!r}")
+        if exchange not in ("collective", "peer"):
+            raise ValueError(f"unknown exchange {exchange!r}")
         self.plan, self.rank, self.mode, self.group = plan, rank, mode, group
         self.parts = parts if plan.D > 1 else 1
+        self.exchange = exchange if plan.D > 1 else "collective"
+        if self.exchange == "peer" and self.parts != 1:
+            raise ValueError("the peer-memory ring shifts whole blocks (parts=1)")
         self.config = config
         M, N, F = shard.M, shard.N, config.F
         K = neighbors.K if neighbors is not None else 0
@@ -365,6 +439,7 @@ class DistTrainer:
             self.hw = HogwildTrainer(None, neighbors, config, dev=shard, params=p, split=False)
             self.model = self.hw.model
             self._build_hogwild()
+        self.ring = PeerRing(plan, rank, self.moving_tensors(), group) if self.exchange == "peer" else None
 
     # -- per-(stage, part) block ranges --------------------------------------
     def _block(self, s: int, h: int):
@@ -433,7 +508,15 @@ class DistTrainer:
         else:
             def fn(s, rb, cb, h):
                 self.hw.launch_work(ep, self.works[(s, h)])
-        run_epoch(self.plan, self.rank, fn, self.moving_tensors(), self.group, self.parts)
+        if self.ring is not None:
+            for s_ in range(self.plan.D):
+                rb, cb = self.plan.stage_block(self.rank, s_)
+                fn(s_, rb, cb, 0)
+                self.ring.shift(s_)
+            if int(self.ring.status.item()):
+                raise nat.NativeError("peer-memory ring shift timed out waiting for a neighbour")
+        else:
+            run_epoch(self.plan, self.rank, fn, self.moving_tensors(), self.group, self.parts)
         status = self.sc.status_value() if self.mode == "exact" else int(self.hw.status.item())
         bad = nat.torch().tensor([float(status & 1)], dtype=nat.torch().float64, device=nat.device())
         if self.plan.D > 1:
@@ -458,14 +541,17 @@ class DistTrainer:
 
 
 def parallel_train_distributed(ratings, neighbors, config, epoch_callback=None, mode: str = "exact",
-                               side: str = "auto", parts: int = 1, group=None):
+                               side: str = "auto", parts: int = 1, group=None, exchange: str = "collective"):
     """parallel_train (parallel.py:166-227) across the ranks of a torch.distributed group,
     one GPU per rank, D = world size.  Called on every rank with the same arguments
     (SPMD); each rank uploads only its shard of ``ratings``.  mode="exact" returns the
     same bytes as parallel_train(ratings, neighbors, config, D); mode="hogwild" is the
     fp32 performance mode.  ``epoch_callback(t, params)`` runs on every rank with the
     whole (gathered, device-backed) model; edits it makes are kept.  Returns the whole
-    model (device-backed ModelParams) on every rank."""
+    model (device-backed ModelParams) on every rank.  exchange="collective": torch.distributed
+    send/recv ring shift (NCCL; sub-block pipelining with parts > 1); exchange="peer": the
+    block is pushed by this package's own kernels into the neighbour's memory (PeerRing,
+    CUDA IPC / NVLink P2P, device-side flags, parts = 1)."""
     import torch.distributed as dist
     from . import _native as nat
     from dataclasses import replace
@@ -487,14 +573,19 @@ def parallel_train_distributed(ratings, neighbors, config, epoch_callback=None, 
         shard = DeviceRatings(ratings, with_baselines=False)
     st = ratings.baselines()     # the reference's host statistics (any values)
     base = (st.mu, nat.to_dev(st.b, np.float64), nat.to_dev(st.b_hat, np.float64))
-    tr = DistTrainer(shard, plan, rank, neighbors, config, base, mode=mode, parts=parts, group=group)
-    for ep in range(config.epochs):
-        tr.epoch(ep)
-        if epoch_callback is not None:
-            tr.gather()
-            p = tr.params()
-            epoch_callback(ep, p)
-            p._device(0)      # edits made by the callback (identical on every rank)
+    tr = DistTrainer(shard, plan, rank, neighbors, config, base, mode=mode, parts=parts, group=group,
+                     exchange=exchange)
+    try:
+        for ep in range(config.epochs):
+            tr.epoch(ep)
+            if epoch_callback is not None:
+                tr.gather()
+                p = tr.params()
+                epoch_callback(ep, p)
+                p._device(0)      # edits made by the callback (identical on every rank)
+    finally:
+        if tr.ring is not None:
+            tr.ring.close()
     tr.gather()
     return tr.params()
 
@@ -576,7 +667,10 @@ def bench_main(args, metric, workload, rates):
     nnz = int(local_nnz.item()) if side == "cols" else shard.nnz
     cfg = TrainConfig(F=F, K=K, epochs=args.warmup + args.steps, seed=0, **rates)
     parts = int(os.environ.get("CULSH_DSGD_PARTS", "2")) if D > 1 else 1
-    tr = DistTrainer(shard, plan, rank, nbr, cfg, base, mode="hogwild", parts=parts)
+    exchange = os.environ.get("CULSH_DSGD_EXCHANGE", "collective")
+    if exchange == "peer":
+        parts = 1
+    tr = DistTrainer(shard, plan, rank, nbr, cfg, base, mode="hogwild", parts=parts, exchange=exchange)
     hw = tr.hw
 
     for w in range(args.warmup):
@@ -636,7 +730,10 @@ def bench_main(args, metric, workload, rates):
                 "impl_config": {"nnz_generated": nnz, "parallelism": f"dsgd{D}",
                            "ring_parts": parts, "rotating_side": side,
                            "moving_bytes_per_stage_per_gpu": moving,
-                           "exchange": (f"NCCL send/recv ring shift of the {side} parameter sub-blocks, each "
+                           "exchange": (f"peer-memory push/pull kernels (csrc/ring.cu): the {side} block written "
+                                        "into the neighbour's memory over IPC/NVLink, device-side flags"
+                                        if exchange == "peer" else
+                                        f"NCCL send/recv ring shift of the {side} parameter sub-blocks, each "
                                         "overlapping the next sub-block's kernel" if backend == "nccl" else
                                         f"{backend} ring shift of the {side} parameter sub-blocks (host-staged)"),
                            "l2": "inputs larger than L2, no flush"},

@@ -57,7 +57,8 @@ def _worker(rank, world, port, job, out_q):
             cfg = P.TrainConfig(F=job["F"], K=job["K"], epochs=job["epochs"], seed=1)
             seen = []
             p = parallel_train_distributed(r, tbl, cfg, mode=kind, side=job["side"], parts=job["parts"],
-                                           epoch_callback=lambda t, q: seen.append(P.rmse(q, r.triplets(), r)))
+                                           epoch_callback=lambda t, q: seen.append(P.rmse(q, r.triplets(), r)),
+                                           exchange=job.get("exchange", "collective"))
             out = {n: getattr(p, n).tobytes() for n in ("b", "b_hat", "U", "V", "W", "C")}
             out["curve"] = seen
         if rank == 0:
@@ -105,6 +106,24 @@ def test_distributed_exact_equals_parallel_train(P, world, side, parts, integer)
                            epoch_callback=lambda t, q: seen.append(P.rmse(q, r.triplets(), r)))
     for n in ("b", "b_hat", "U", "V", "W", "C"):
         assert res[n] == getattr(ref, n).tobytes(), (side, parts, n)
+    assert res["curve"] == seen
+
+
+@pytest.mark.parametrize("world,side,integer", [(2, "cols", True), (3, "cols", False), (3, "rows", True)])
+def test_peer_ring_exact_equals_parallel_train(P, world, side, integer):
+    """exchange="peer": the ring shift done by csrc/ring.cu's push / pull kernels over CUDA
+    IPC-mapped neighbour memory with device-side flags (ranks share one GPU here; NVLink P2P
+    between GPUs) -- the same bytes as parallel_train(D)."""
+    job = {"kind": "exact", "side": side, "parts": 1, "F": 12, "K": 5, "epochs": 3, "exchange": "peer",
+           "data": {"seed": world + 7, "integer": integer}}
+    res = _run(world, job)
+    r = _case(P, seed=world + 7, integer=integer)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 5)
+    seen = []
+    ref = P.parallel_train(r, tbl, P.TrainConfig(F=12, K=5, epochs=3, seed=1), world,
+                           epoch_callback=lambda t, q: seen.append(P.rmse(q, r.triplets(), r)))
+    for n in ("b", "b_hat", "U", "V", "W", "C"):
+        assert res[n] == getattr(ref, n).tobytes(), (side, n)
     assert res["curve"] == seen
 
 
