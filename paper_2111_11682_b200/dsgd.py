@@ -395,8 +395,10 @@ class DistTrainer:
         t = nat.torch()
         if mode not in ("exact", "hogwild"):
             raise ValueError(f"unknown mode {mode!r}")
-        if exchange not in ("collective", "peer"):
+        if exchange not in ("collective", "peer", "auto"):
             raise ValueError(f"unknown exchange {exchange!r}")
+        if exchange == "auto" and parts != 1:
+            exchange = "collective"
         self.plan, self.rank, self.mode, self.group = plan, rank, mode, group
         self.parts = parts if plan.D > 1 else 1
         self.exchange = exchange if plan.D > 1 else "collective"
@@ -439,7 +441,32 @@ class DistTrainer:
             self.hw = HogwildTrainer(None, neighbors, config, dev=shard, params=p, split=False)
             self.model = self.hw.model
             self._build_hogwild()
-        self.ring = PeerRing(plan, rank, self.moving_tensors(), group) if self.exchange == "peer" else None
+        self.ring = None
+        if self.exchange in ("peer", "auto"):
+            self.ring = self._peer_ring(strict=self.exchange == "peer")
+            self.exchange = "peer" if self.ring is not None else "collective"
+
+    def _peer_ring(self, strict: bool):
+        """The peer-memory ring, or None when a rank cannot map its neighbours' buffers
+        (strict: raise instead).  All ranks agree (one all-reduce of the failures)."""
+        import torch.distributed as dist
+        from . import _native as nat
+        ring, err = None, None
+        try:
+            ring = PeerRing(self.plan, self.rank, self.moving_tensors(), self.group)
+        except Exception as ex:   # e.g. no P2P between the GPUs: fall back to the collective path
+            err = ex
+        bad = nat.torch().tensor([0.0 if err is None else 1.0], dtype=nat.torch().float64)
+        if dist.get_backend(self.group) == "nccl":
+            bad = bad.cuda()
+        dist.all_reduce(bad, group=self.group)
+        if float(bad.item()):
+            if ring is not None:
+                ring.close()
+            if strict:
+                raise nat.NativeError(f"peer-memory ring unavailable: {err!r}")
+            return None
+        return ring
 
     # -- per-(stage, part) block ranges --------------------------------------
     def _block(self, s: int, h: int):
@@ -667,8 +694,9 @@ def bench_main(args, metric, workload, rates):
     nnz = int(local_nnz.item()) if side == "cols" else shard.nnz
     cfg = TrainConfig(F=F, K=K, epochs=args.warmup + args.steps, seed=0, **rates)
     parts = int(os.environ.get("CULSH_DSGD_PARTS", "2")) if D > 1 else 1
-    exchange = os.environ.get("CULSH_DSGD_EXCHANGE", "collective")
-    if exchange == "peer":
+    # own push/pull kernels over peer memory unless a rank cannot map its neighbours
+    exchange = os.environ.get("CULSH_DSGD_EXCHANGE", "auto")
+    if exchange in ("peer", "auto"):
         parts = 1
     tr = DistTrainer(shard, plan, rank, nbr, cfg, base, mode="hogwild", parts=parts, exchange=exchange)
     hw = tr.hw
@@ -732,7 +760,7 @@ def bench_main(args, metric, workload, rates):
                            "moving_bytes_per_stage_per_gpu": moving,
                            "exchange": (f"peer-memory push/pull kernels (csrc/ring.cu): the {side} block written "
                                         "into the neighbour's memory over IPC/NVLink, device-side flags"
-                                        if exchange == "peer" else
+                                        if tr.exchange == "peer" else
                                         f"NCCL send/recv ring shift of the {side} parameter sub-blocks, each "
                                         "overlapping the next sub-block's kernel" if backend == "nccl" else
                                         f"{backend} ring shift of the {side} parameter sub-blocks (host-staged)"),
