@@ -303,6 +303,19 @@ int culsh_rmse(const CulshData *d, const CulshModel64 *m, const int32_t *t_rows,
                double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
                double *rmse_out, void *stream);
 
+/* culsh_rmse / culsh_rmse_train on an fp32 model (a Hogwild fit) without widening it:
+ * fp32 values loaded, arithmetic in fp64 in the reference's order -- the same bytes as on
+ * the widened fp64 copy.  mu: the model's fp64 mu; F: logical factors (m->F is the row
+ * stride, >= F for zero-padded widths); nbr: J^K. */
+int culsh_rmse_m32(const CulshData *d, const CulshModel32 *m, double mu, int F, const int32_t *nbr,
+                   const int32_t *t_rows, const int32_t *t_cols, const double *t_vals, int64_t n,
+                   int do_clamp, double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
+                   double *rmse_out, void *stream);
+int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, double mu, int F, const int32_t *nbr,
+                         const uint32_t *mask, const int64_t *group_base, const int32_t *pos,
+                         const int64_t *perm, int do_clamp, double clamp_lo, double clamp_hi,
+                         double unscale, double *sqerr_scratch, double *rmse_out, void *stream);
+
 /* RMSE of the fp32 Hogwild model (predictions in fp32, sum in fp64). */
 int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int32_t *nbr,
                  const int32_t *t_rows, const int32_t *t_cols, const double *t_vals, int64_t n,

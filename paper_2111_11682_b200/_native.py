@@ -120,6 +120,10 @@ _SIGS = {
                                          _P(CulshModel32), _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
     "culsh_rmse": [_P(CulshData), _P(CulshModel64), _vp, _vp, _vp, _i64, _i32, _f64, _f64, _f64,
                    _vp, _vp, _vp],
+    "culsh_rmse_m32": [_P(CulshData), _P(CulshModel32), _f64, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _f64, _f64,
+                       _f64, _vp, _vp, _vp],
+    "culsh_rmse_train_m32": [_P(CulshData), _P(CulshModel32), _f64, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _f64,
+                             _f64, _f64, _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "culsh_predict": [_P(CulshData), _P(CulshModel64), _vp, _vp, _i64, _vp, _vp],
     "culsh_csc_to_csr_map": [_P(CulshData), _vp, _vp],
@@ -307,7 +311,7 @@ def copy_to_device(dst, a: np.ndarray) -> None:
     T = _pool._max_workers
     src = a.reshape(-1).view(np.uint8)
     d8 = dst.view(-1).view(t.uint8)
-    cs.wait_stream(t.cuda.current_stream())
+    cur = t.cuda.current_stream()
     for c, lo in enumerate(range(0, nb, _STAGE_BYTES)):
         b = c & 1
         evs[b].synchronize()            # the DMA that last read this chunk is done
@@ -317,12 +321,11 @@ def copy_to_device(dst, a: np.ndarray) -> None:
         for f in [_pool.submit(np.copyto, h[k * sub:min(hi - lo, (k + 1) * sub)],
                                src[lo + k * sub:min(hi, lo + (k + 1) * sub)]) for k in range(T)]:
             f.result()
-        with t.cuda.stream(cs):
-            d8[lo:hi].copy_(bufs[b][:hi - lo], non_blocking=True)
-            evs[b].record(cs)
-    t.cuda.current_stream().wait_stream(cs)
-    for e in evs:
-        e.synchronize()                 # the caller may free or reuse `a` on return
+        # the DMA runs on the caller's stream, in order with its other work; `a` is fully
+        # copied into the pinned chunk already, so nothing waits for the DMA here (a later
+        # reuse of the chunk waits on its event)
+        d8[lo:hi].copy_(bufs[b][:hi - lo], non_blocking=True)
+        evs[b].record(cur)
 
 
 def to_dev(a: np.ndarray, dtype=None):

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(PRE ? 128 : 64) pred_tile_kernel(CulshData d, 
                                                         const P *__restrict__ bhat, const P *__restrict__ U,
                                                         const P *__restrict__ V, const P *__restrict__ W,
                                                         const P *__restrict__ C, const int32_t *__restrict__ nbr,
-                                                        int F, int K, const int32_t *__restrict__ t_rows,
+                                                        int F, int ldF, int K, const int32_t *__restrict__ t_rows,
                                                         const int32_t *__restrict__ t_cols,
                                                         const double *__restrict__ t_vals, int64_t n, PreLookup pre,
                                                         int mode, int do_clamp, double lo, double hi,
@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(PRE ? 128 : 64) pred_tile_kernel(CulshData d, 
                 const int64_t ir = __shfl_sync(0xffffffffu, i, r);
                 const int64_t jr = PRE ? 0 : __shfl_sync(0xffffffffu, j, r);
                 if (f < F) {
-                    cp_async<sizeof(P)>(ut + lane * kTileLd + r, U + ir * F + f);
-                    if (!PRE) cp_async<sizeof(P)>(vt + lane * kTileLd + r, V + jr * F + f);
+                    cp_async<sizeof(P)>(ut + lane * kTileLd + r, U + ir * ldF + f);
+                    if (!PRE) cp_async<sizeof(P)>(vt + lane * kTileLd + r, V + jr * ldF + f);
                 }
             }
             cp_async_wait_all();
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(PRE ? 128 : 64) pred_tile_kernel(CulshData d, 
             const int fe = F - f0 < 32 ? F - f0 : 32;
             if (valid) {
                 for (int q = 0; q < fe; ++q) {
-                    const double v = PRE ? (double)__ldg(V + j * F + f0 + q) : (double)vt[q * kTileLd + lane];
+                    const double v = PRE ? (double)__ldg(V + j * ldF + f0 + q) : (double)vt[q * kTileLd + lane];
                     dot = __dadd_rn(dot, __dmul_rn((double)ut[q * kTileLd + lane], v));
                 }
             }
@@ -309,7 +309,7 @@ extern "C" int culsh_rmse(const CulshData *d, const CulshModel64 *m, const int32
     cudaStream_t st = (cudaStream_t)stream;
     const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
     pred_tile_kernel<double, false><<<blocks, 64, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
-                                                            m->nbr, m->F, m->K, t_rows, t_cols, t_vals, n,
+                                                            m->nbr, m->F, m->F, m->K, t_rows, t_cols, t_vals, n,
                                                             PreLookup{}, 0, do_clamp, clamp_lo, clamp_hi, unscale,
                                                             sqerr_scratch);
     CULSH_LAUNCH_CHECK();
@@ -342,7 +342,7 @@ extern "C" int culsh_rmse_train(const CulshData *d, const CulshModel64 *m, const
     const int blocks = (int)min64((n + 127) / 128, (int64_t)num_sms() * 12);
     PreLookup pre{mask, group_base, pos, perm, m->K <= 32 ? 1 : 2};
     pred_tile_kernel<double, true><<<blocks, 128, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
-                                                           m->nbr, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
+                                                           m->nbr, m->F, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
                                                            do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
     return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
@@ -355,7 +355,7 @@ extern "C" int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int
     cudaStream_t st = (cudaStream_t)stream;
     const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
     pred_tile_kernel<float, false><<<blocks, 64, 0, st>>>(*d, (double)m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
-                                                           nbr, m->F, m->K, t_rows, t_cols, t_vals, n, PreLookup{},
+                                                           nbr, m->F, m->F, m->K, t_rows, t_cols, t_vals, n, PreLookup{},
                                                            0, 0, 0.0, 0.0, 1.0, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
     return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, false, st);
@@ -367,8 +367,47 @@ extern "C" int culsh_predict(const CulshData *d, const CulshModel64 *m, const in
     cudaStream_t st = (cudaStream_t)stream;
     const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
     pred_tile_kernel<double, false><<<blocks, 64, 0, st>>>(*d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
-                                                            m->nbr, m->F, m->K, rows, cols, nullptr, n, PreLookup{},
+                                                            m->nbr, m->F, m->F, m->K, rows, cols, nullptr, n, PreLookup{},
                                                             1, 0, 0.0, 0.0, 1.0, out);
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
+}
+
+// rmse / rmse_train on an fp32 model (a Hogwild fit) without widening it: the kernel loads
+// the fp32 values and computes in fp64 exactly as on the widened copy (every fp32 value is
+// an fp64 value), so the result is the same bytes; F = logical factors, the model's row
+// stride is m->F (zero-padded widths).  nbr: the model's J^K.
+extern "C" int culsh_rmse_m32(const CulshData *d, const CulshModel32 *m, double mu, int F, const int32_t *nbr,
+                              const int32_t *t_rows, const int32_t *t_cols, const double *t_vals, int64_t n,
+                              int do_clamp, double clamp_lo, double clamp_hi, double unscale,
+                              double *sqerr_scratch, double *rmse_out, void *stream) {
+    CULSH_REQUIRE(n > 0, "empty test set");
+    CULSH_REQUIRE(F >= 1 && F <= m->F, "logical F exceeds the model's row stride");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = (int)min64((n + 63) / 64, (int64_t)num_sms() * 24);
+    pred_tile_kernel<float, false><<<blocks, 64, 0, st>>>(*d, mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
+                                                           nbr, F, m->F, m->K, t_rows, t_cols, t_vals, n,
+                                                           PreLookup{}, 0, do_clamp, clamp_lo, clamp_hi, unscale,
+                                                           sqerr_scratch);
+    CULSH_LAUNCH_CHECK();
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+}
+
+extern "C" int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, double mu, int F,
+                                    const int32_t *nbr,
+                                    const uint32_t *mask, const int64_t *group_base, const int32_t *pos,
+                                    const int64_t *perm, int do_clamp, double clamp_lo, double clamp_hi,
+                                    double unscale, double *sqerr_scratch, double *rmse_out, void *stream) {
+    const int64_t n = d->nnz;
+    CULSH_REQUIRE(n > 0, "empty training set");
+    CULSH_REQUIRE(F >= 1 && F <= m->F, "logical F exceeds the model's row stride");
+    CULSH_REQUIRE(m->K == 0 || (mask && group_base && pos), "lookup cache missing");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = (int)min64((n + 127) / 128, (int64_t)num_sms() * 12);
+    PreLookup pre{mask, group_base, pos, perm, m->K <= 32 ? 1 : 2};
+    pred_tile_kernel<float, true><<<blocks, 128, 0, st>>>(*d, mu, m->b, m->bhat, m->U, m->V, m->W, m->C,
+                                                          nbr, F, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
+                                                          do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch);
+    CULSH_LAUNCH_CHECK();
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
 }

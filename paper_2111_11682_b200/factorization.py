@@ -751,24 +751,27 @@ def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
         raise ValueError("empty test set")
     _check_model_dims(max(params.F, 1), params.K)
     dev = ratings.device()
-    dm = params._device(64)
+    dm = params._device(0)
+    m32 = not isinstance(dm, DeviceModel64)   # a Hogwild fit's fp32 backing: read as is, fp64 math
     n = len(testset)
     scratch = nat.empty((n + 256,), "float64")
     out = nat.empty((1,), "float64")
     lo, hi = clamp if clamp is not None else (0.0, 0.0)
     us = 1.0 if unscale is None else float(unscale)
+    head = ((ctypes.byref(dev.struct), ctypes.byref(dm.struct), float(dm.mu), int(dm.F), nat.ptr(dm.nbr))
+            if m32 else (ctypes.byref(dev.struct), ctypes.byref(dm.struct)))
     if getattr(testset, "_source", None) is ratings and n == dev.nnz:
         K = dm.K
         mask = base = pos = None
         if K:
             mask, base, pos = _train_lookup(dev, dm.nbr, K)
         perm = ratings.csc_entry_perm()
-        nat.call("culsh_rmse_train", ctypes.byref(dev.struct), ctypes.byref(dm.struct), nat.ptr(mask),
+        nat.call("culsh_rmse_train_m32" if m32 else "culsh_rmse_train", *head, nat.ptr(mask),
                  nat.ptr(base), nat.ptr(pos), nat.ptr(perm), int(clamp is not None), float(lo), float(hi),
                  us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
         return float(out.item())
     tr, tc, tv = _test_device(testset, ratings)
-    nat.call("culsh_rmse", ctypes.byref(dev.struct), ctypes.byref(dm.struct), nat.ptr(tr),
+    nat.call("culsh_rmse_m32" if m32 else "culsh_rmse", *head, nat.ptr(tr),
              nat.ptr(tc), nat.ptr(tv), n, int(clamp is not None), float(lo), float(hi), us,
              nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
     return float(out.item())

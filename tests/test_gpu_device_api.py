@@ -272,3 +272,20 @@ def test_device_sparse_ratings_real_values_exact_baselines(P):
                        ("row_ptr", host.row_ptr), ("row_cols", host.row_cols), ("row_vals", host.row_vals)):
         n = len(want)
         assert nat.to_host(getattr(d, name))[:n].tobytes() == np.ascontiguousarray(want).tobytes(), name
+
+
+@pytest.mark.parametrize("F", [32, 50])
+def test_rmse_on_fp32_model_equals_widened(P, F):
+    """rmse() on a Hogwild fit reads its fp32 arrays directly (culsh_rmse[_train]_m32; F = 50
+    runs on zero-padded 64-wide rows) and returns the same float as on a widened fp64 copy
+    of the same parameters, for a held-out set and for the training set."""
+    r, rows, cols, vals = _case(P, seed=21, M=400, N=90, dens=0.2)
+    tbl, _ = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=8, seed=3), 6)
+    ph = P.train_full(r, tbl, P.TrainConfig(F=F, K=6, epochs=3, seed=0), mode="hogwild")
+    host = ph.copy()                                   # fp64 host arrays -> DeviceModel64 path
+    rng = np.random.default_rng(2)
+    sel = rng.choice(len(rows), 300, replace=False)
+    te = P.Triplets(rows[sel].astype(np.int32), cols[sel].astype(np.int32), vals[sel])
+    assert P.rmse(ph, te, r) == P.rmse(host, te, r)
+    assert P.rmse(ph, r.triplets(), r) == P.rmse(host, r.triplets(), r)
+    assert P.rmse(ph, te, r, clamp=(1.0, 5.0), unscale=2.0) == P.rmse(host, te, r, clamp=(1.0, 5.0), unscale=2.0)

@@ -19,4 +19,6 @@ timeout 900 python tools/bench_gsm.py c3 --sample 8 > gpurun_out/gsm_c3.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gsm_stats_tc_kernel -c 1 -o gpurun_out/r2f_gsm_tc_c3 python tools/bench_gsm.py c3 --sample 1 > /dev/null 2>&1; echo ncu_gsm=$?
 timeout 1200 python tools/api_costs.py fit online > gpurun_out/api_costs.log 2>&1; echo api=$?
 timeout 900 python tools/dsgd_stage_time.py > gpurun_out/dsgd_stage.log 2>&1; echo dsgd_stage=$?
-CULSH_DIST_BACKEND=gloo CULSH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --steps 3 --warmup 3 > gpurun_out/bench_2rank_gloo.log 2>&1; echo b2=$?
+CULSH_DIST_BACKEND=gloo CULSH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/bench_2rank_peer.log 2>&1; echo b2=$?
+timeout 900 python tools/absorb_breakdown.py > gpurun_out/absorb_breakdown.log 2>&1; echo ab=$?
+timeout 600 python tools/lsh_breakdown.py > gpurun_out/lsh_breakdown.log 2>&1; echo lb=$?
