@@ -389,15 +389,12 @@ class DeviceRatings:
 _PW_CHUNK = 1 << 16
 
 
-def pairwise_sum_device(x) -> float:
-    """numpy's np.add.reduce of a device float64 vector, bit for bit: the top of numpy's
-    pairwise split tree (halves rounded down to multiples of 8) is walked here down to nodes
-    of <= 65,536 elements, which culsh_pairwise_chunks sums on the device (thread per node,
-    the same tree below); the node sums are combined back up in the same order."""
-    n = int(x.numel())
+def _pairwise_plan(n: int):
+    """Nodes of numpy's pairwise split tree over n elements (halves rounded down to multiples
+    of 8) of at most _PW_CHUNK elements, left to right: (offsets, lengths)."""
     offs, lens = [], []
 
-    def split(o, m):                      # leaves of the top tree, left to right
+    def split(o, m):
         if m <= _PW_CHUNK:
             offs.append(o)
             lens.append(m)
@@ -407,15 +404,15 @@ def pairwise_sum_device(x) -> float:
         split(o, m2)
         split(o + m2, m - m2)
 
-    if n == 0:
-        return 0.0
-    split(0, n)
-    part = nat.empty((len(offs),), "float64")
-    d_off = nat.to_dev(np.asarray(offs, np.int64))      # keep both alive until the kernel ran
-    d_len = nat.to_dev(np.asarray(lens, np.int64))
-    nat.call("culsh_pairwise_chunks", nat.ptr(x), nat.ptr(d_off), nat.ptr(d_len), len(offs), nat.ptr(part),
-             nat.stream_ptr())
-    vals = iter(nat.to_host(part).tolist())
+    if n:
+        split(0, n)
+    return offs, lens
+
+
+def _pairwise_combine(n: int, node_sums) -> float:
+    """numpy's sum of the whole array from the sums of _pairwise_plan(n)'s nodes, combined
+    up the same tree (left + right, IEEE double)."""
+    vals = iter(node_sums)
 
     def combine(m):
         if m <= _PW_CHUNK:
@@ -423,9 +420,26 @@ def pairwise_sum_device(x) -> float:
         m2 = m // 2
         m2 -= m2 % 8
         left = combine(m2)
-        return left + combine(m - m2)     # Python float: IEEE double add
+        return left + combine(m - m2)
 
-    return combine(n)
+    return combine(n) if n else 0.0
+
+
+def pairwise_sum_device(x) -> float:
+    """numpy's np.add.reduce of a device float64 vector, bit for bit: the top of numpy's
+    pairwise split tree is walked on the host down to nodes of <= 65,536 elements
+    (_pairwise_plan), culsh_pairwise_chunks sums each node on the device (thread per node,
+    the same tree below), and the node sums are combined back up in the same order."""
+    n = int(x.numel())
+    if n == 0:
+        return 0.0
+    offs, lens = _pairwise_plan(n)
+    part = nat.empty((len(offs),), "float64")
+    d_off = nat.to_dev(np.asarray(offs, np.int64))      # keep both alive until the kernel ran
+    d_len = nat.to_dev(np.asarray(lens, np.int64))
+    nat.call("culsh_pairwise_chunks", nat.ptr(x), nat.ptr(d_off), nat.ptr(d_len), len(offs), nat.ptr(part),
+             nat.stream_ptr())
+    return _pairwise_combine(n, nat.to_host(part).tolist())
 
 
 def _ordered_sums(n_seg: int, keys, vals, init=None):

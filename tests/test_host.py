@@ -189,3 +189,17 @@ def test_split_holdout_and_transform_match_reference():
     assert tt.values.tobytes() == z["transform_vals"].tobytes()
     with pytest.raises(ValueError):
         P.transform_ratings(tt, scale=0.0)
+
+
+def test_pairwise_plan_combines_to_numpy():
+    """The host half of pairwise_sum_device: numpy's pairwise tree cut into nodes of <= 65,536
+    elements, each node summed by numpy itself (what the device kernel restates) and combined
+    back up the same tree, equals np.add.reduce of the whole array bit for bit."""
+    from paper_2111_11682_b200.data import _pairwise_combine, _pairwise_plan
+    rng = np.random.default_rng(3)
+    for n in (1, 9, 65536, 65537, 131075, 1_000_003):
+        x = rng.standard_normal(n) * 10.0 ** rng.integers(-5, 5, n)
+        offs, lens = _pairwise_plan(n)
+        assert sum(lens) == n and max(lens) <= 65536
+        sums = [float(np.add.reduce(x[o:o + m])) for o, m in zip(offs, lens)]
+        assert _pairwise_combine(n, sums) == float(np.add.reduce(x))
