@@ -307,6 +307,12 @@ def copy_to_device(dst, a: np.ndarray) -> None:
     if nb < (16 << 20):
         dst.view(-1).view(t.uint8)[:nb].copy_(t.from_numpy(a.reshape(-1).view(np.uint8)))
         return
+    with _stage_lock:
+        _copy_to_device_locked(dst, a, nb)
+
+
+def _copy_to_device_locked(dst, a: np.ndarray, nb: int) -> None:
+    t = torch()
     bufs, cs, evs = _stage_init()
     T = _pool._max_workers
     src = a.reshape(-1).view(np.uint8)
@@ -349,6 +355,8 @@ def to_dev(a: np.ndarray, dtype=None):
 _STAGE_BYTES = 64 << 20          # two reusable pinned staging chunks per process
 _stage = None
 _pool = None
+import threading as _threading
+_stage_lock = _threading.Lock()  # the chunks are shared: one staged copy at a time
 
 
 def _staged_to_host(x) -> np.ndarray:
@@ -356,6 +364,11 @@ def _staged_to_host(x) -> np.ndarray:
     chunk c+1 (copy stream) overlaps host threads copying chunk c into a fresh numpy array
     (which also spreads its page faults over the threads).  C3's fp64 U (492 MB): 20 ms,
     against 105 ms for a copy into pageable memory (tools/d2h_bench.py)."""
+    with _stage_lock:
+        return _staged_to_host_locked(x)
+
+
+def _staged_to_host_locked(x) -> np.ndarray:
     t = torch()
     bufs, cs, evs = _stage_init()
     T = _pool._max_workers
