@@ -35,10 +35,11 @@ def main():
     tr = HogwildTrainer(None, nbr, cfg, dev=d)
     out = {"nnz": d.nnz, "max_col": int((d.col_ptr[1:] - d.col_ptr[:-1]).max().item()),
            "segments": tr.work["n"] if tr.work else 0, "split_cols": tr.work["split_cols"] if tr.work else 0}
-    for mode in ("cursors", "scan"):
+    cfg.epochs = 20
+    for rep, mode in enumerate(("cursors", "scan", "cursors", "scan")):   # alternating: same model age
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        for t in range(cfg.epochs):
-            if t == 3:
+        for t in range(5 * rep, 5 * rep + 5):
+            if t == 5 * rep + 1:
                 ev[0].record()
             if mode == "cursors":
                 tr.launch_epoch(t)
@@ -47,7 +48,7 @@ def main():
                                   tr.loss, tr.work["seg"])
         ev[1].record()
         torch.cuda.synchronize()
-        out[f"{mode}_ms_per_epoch"] = ev[0].elapsed_time(ev[1]) / 5
+        out.setdefault(f"{mode}_ms_per_epoch", []).append(ev[0].elapsed_time(ev[1]) / 4)
     print(json.dumps(out), flush=True)
 
 
