@@ -85,50 +85,6 @@ __device__ __forceinline__ Scalars exact_error(const double *buf, int F, int K, 
     return s;
 }
 
-// The neighbour part of _update_one's prediction depends only on the column's own w_j / c_j
-// and the data, not on the row parameters a predecessor may still be writing, so the column
-// kernel evaluates it BEFORE waiting for row i: same expressions, same order of the final
-// additions (pred + sw/sqrt(nr) + sc/sqrt(nn)), hence the same bytes.
-struct KPart {
-    double tw, tc, inv_r, inv_n;
-    int nr, nn;
-};
-
-__device__ __forceinline__ KPart exact_kpart(const double *buf, int F, int K, const uint32_t *emask) {
-    KPart p;
-    p.nr = 0;
-    p.nn = 0;
-    double sw = 0.0, sc = 0.0;
-    for (int k = 0; k < K; ++k) {
-        if ((emask[k >> 5] >> (k & 31)) & 1u) { ++p.nr; sw = sw + buf[F + k]; }
-        else { ++p.nn; sc = sc + buf[F + k]; }
-    }
-    p.tw = p.nr > 0 ? sw / sqrt((double)p.nr) : 0.0;
-    p.tc = p.nn > 0 ? sc / sqrt((double)p.nn) : 0.0;
-    p.inv_r = p.nr > 0 ? 1.0 / sqrt((double)p.nr) : 0.0;
-    p.inv_n = p.nn > 0 ? 1.0 / sqrt((double)p.nn) : 0.0;
-    return p;
-}
-
-__device__ __forceinline__ Scalars exact_error_kp(const double *buf, int F, const KPart &kp, double mu, double bi,
-                                                  double bhj, double r, int variant) {
-    double pred = (variant & 2) ? mu + bhj + bi : mu + bi + bhj;
-    if (variant & 1) {
-        for (int f = 0; f < F; ++f) pred = pred + buf[f];
-    } else {
-        double dot = 0.0;
-        for (int f = 0; f < F; ++f) dot = dot + buf[f];
-        pred = pred + dot;
-    }
-    if (kp.nr > 0) pred = pred + kp.tw;
-    if (kp.nn > 0) pred = pred + kp.tc;
-    Scalars s;
-    s.e = r - pred;
-    s.inv_r = kp.inv_r;
-    s.inv_n = kp.inv_n;
-    return s;
-}
-
 // Precomputed neighbour lookups of a column range (culsh_exact_lookup): per CSC entry
 // idx, KPL mask words at mask[(idx - base) * KPL] (bit k: row i rated J[j,k]) and the
 // looked-up ratings rv[(idx - base) * K + k].  With them the column kernel's per-update
@@ -204,14 +160,6 @@ exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                 resid[q] = expl[q] ? rv - (mu + bbi + bbn[q]) : 0.0;
                 emask[q] = __ballot_sync(0xffffffffu, expl[q]);
             }
-            // neighbour part of the prediction: column-owned values only, before the wait
-#pragma unroll
-            for (int q = 0; q < KPL; ++q) {
-                const int k = lane + 32 * q;
-                if (k < K) buf[F + k] = expl[q] ? resid[q] * w[q] : c[q];
-            }
-            __syncwarp();
-            const KPart kp = exact_kpart(buf, F, K, emask);
 
             if (upd_row) {
                 const int64_t pos = P.csc2csr[idx];
@@ -237,8 +185,13 @@ exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                 if (f < F) buf[f] = u[q] * v[q];
             }
             const double bi = __ldcg(&P.b[i]);
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) {
+                const int k = lane + 32 * q;
+                if (k < K) buf[F + k] = expl[q] ? resid[q] * w[q] : c[q];
+            }
             __syncwarp();
-            const Scalars s = exact_error_kp(buf, F, kp, mu, bi, bhj, r, variant);
+            const Scalars s = exact_error(buf, F, K, emask, mu, bi, bhj, r, variant);
             const double e = s.e;
             if (!isfinite(e)) {
                 if (lane == 0) atomicOr(status, 1);
