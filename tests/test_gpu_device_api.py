@@ -289,3 +289,20 @@ def test_rmse_on_fp32_model_equals_widened(P, F):
     assert P.rmse(ph, te, r) == P.rmse(host, te, r)
     assert P.rmse(ph, r.triplets(), r) == P.rmse(host, r.triplets(), r)
     assert P.rmse(ph, te, r, clamp=(1.0, 5.0), unscale=2.0) == P.rmse(host, te, r, clamp=(1.0, 5.0), unscale=2.0)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.int32])
+def test_staged_copies_round_trip(P, dtype):
+    """Large host <-> device copies go through the reused pinned chunks (to_dev /
+    copy_to_device / to_host): a multi-chunk array (> 2 x 64 MB, ragged tail) survives both
+    directions byte for byte, twice in a row (chunk reuse), and a small one takes the plain path."""
+    from paper_2111_11682_b200 import _native as nat
+    rng = np.random.default_rng(0)
+    n = (200 << 20) // np.dtype(dtype).itemsize + 12345
+    for _ in range(2):
+        a = (rng.standard_normal(n) if dtype == np.float64 else rng.integers(-2**31, 2**31 - 1, n)).astype(dtype)
+        d = nat.to_dev(a)
+        b = nat.to_host(d)
+        assert b.dtype == a.dtype and b.tobytes() == a.tobytes()
+    small = np.arange(1000, dtype=dtype)
+    assert nat.to_host(nat.to_dev(small)).tobytes() == small.tobytes()
