@@ -437,19 +437,26 @@ int culsh_gsm_tile_panels(const int8_t *plain, int64_t ld, int64_t w, int8_t *ti
 
 /* Count route, step 2: the four statistic products of the tiled panels:
  * g_xx (+)= X X', g_rx (+)= R X', g_rr (+)= R R', g_qx (+)= Q X' (ld x ld int32,
- * row stride ld; accumulate != 0 adds to the existing values, for row passes).  One
+ * row stride ld; accumulate != 0 adds to the existing values, for row passes), and when
+ * non-NULL the transposes g_xr (+)= X R', g_xq (+)= X Q' (the s2 / q2 statistics, so the
+ * select kernel reads every statistic row-wise).  One
  * sm_100a kernel: bulk-copy-fed tcgen05.mma kind::i8 with TMEM accumulators, exact int32
  * (similarity.py:57-90 statistics of every pair at once).  ld % 128 == 0, w % 64 == 0. */
 int culsh_gsm_stats_tc(const int8_t *tiles, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
-                       int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, void *stream);
+                       int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, int32_t *g_xr, int32_t *g_xq,
+                       void *stream);
 
 /* Count route, step 3 (after the int32 products g_xx = X'X, g_rx = R'X,
  * g_rr = R'R, g_qx = Q'X, each N x N with row stride ld): shrunk Pearson of every
  * pair from the exact integer statistics and the per-column top-K, rows
- * j_lo..j_lo+n_rows-1 -> entries (n_rows, K).  Bit-identical to the merge route. */
+ * j_lo..j_lo+n_rows-1 -> entries (n_rows, K).  With the transposes g_xr / g_xq (from
+ * culsh_gsm_stats_tc) every statistic is read row-wise and the selection runs as warp
+ * register top-K lists; NULL: strided reads of g_rx / g_qx, per-thread lists.
+ * Bit-identical to the merge route either way. */
 int culsh_gsm_count_select(const int32_t *g_xx, const int32_t *g_rx, const int32_t *g_rr,
-                           const int32_t *g_qx, int64_t ld, int64_t N, int64_t j_lo, int64_t n_rows,
-                           int K, double lambda_rho, int32_t *entries, void *stream);
+                           const int32_t *g_qx, const int32_t *g_xr, const int32_t *g_xq, int64_t ld,
+                           int64_t N, int64_t j_lo, int64_t n_rows, int K, double lambda_rho,
+                           int32_t *entries, void *stream);
 
 /* similarity.py:110-135 pearson / shrunk_similarity of one pair:
  * out (device, 3 doubles) = {pearson, shrunk, co-support n}. */

@@ -97,10 +97,10 @@ _SIGS = {
                                        _P(CulshRates), _i32, _i32, _vp, _vp, _vp, _vp],
     "culsh_gsm_merge_topk": [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_gsm_densify_rows": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
-    "culsh_gsm_stats_tc": [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp],
+    "culsh_gsm_stats_tc": [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "culsh_gsm_densify_tiled": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
     "culsh_gsm_tile_panels": [_vp, _i64, _i64, _vp, _vp],
-    "culsh_gsm_count_select": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
+    "culsh_gsm_count_select": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _f64, _vp, _vp],
     "culsh_pair_similarity": [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp],
     "culsh_split_holdout": [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp],
     "culsh_train_lookup": [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp],

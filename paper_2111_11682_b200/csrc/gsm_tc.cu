@@ -186,7 +186,8 @@ __device__ __forceinline__ bool drift_wait(int *prog, int ncta, int cp, int lane
 __global__ void __launch_bounds__(kThreads, 1)
 gsm_stats_tc_kernel(const int8_t *__restrict__ tiles, int64_t ld, int nk, int accumulate,
                     int32_t *__restrict__ g_xx, int32_t *__restrict__ g_rx, int32_t *__restrict__ g_rr,
-                    int32_t *__restrict__ g_qx, int *__restrict__ prog, int sync_every, int sync_lag) {
+                    int32_t *__restrict__ g_qx, int32_t *__restrict__ g_xr, int32_t *__restrict__ g_xq,
+                    int *__restrict__ prog, int sync_every, int sync_lag) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + kStages * kStageBytes);
@@ -322,6 +323,17 @@ gsm_stats_tc_kernel(const int8_t *__restrict__ tiles, int64_t ld, int nk, int ac
                     }
                     dst[q] = o;
                 }
+                // transposed copies of R X' and Q X' (g_xr = X R', g_xq = X Q': the s2 / q2
+                // statistics read row-wise by the select kernel): for a fixed column the
+                // warp's 32 rows are consecutive, so each of these stores is one 128-byte line
+                int32_t *gt = (c >= 128 && c < 256) ? g_xr : (c >= 384 ? g_xq : nullptr);
+                if (gt) {
+#pragma unroll 8
+                    for (int q = 0; q < 32; ++q) {
+                        int32_t *p = gt + (col0 + (c & 127) + q) * ld + row;
+                        *p = accumulate ? *p + (int)v[q] : (int)v[q];
+                    }
+                }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -410,7 +422,8 @@ extern "C" int culsh_gsm_tile_panels(const int8_t *plain, int64_t ld, int64_t w,
 }
 
 extern "C" int culsh_gsm_stats_tc(const int8_t *tiles, int64_t ld, int64_t w, int accumulate, int32_t *g_xx,
-                                  int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, void *stream) {
+                                  int32_t *g_rx, int32_t *g_rr, int32_t *g_qx, int32_t *g_xr, int32_t *g_xq,
+                                  void *stream) {
     using namespace culsh::gsm_tc;
     CULSH_REQUIRE(ld > 0 && ld % kBM == 0, "ld must be a positive multiple of 128");
     CULSH_REQUIRE(w > 0 && w % kBK == 0, "w must be a positive multiple of 64");
@@ -427,7 +440,7 @@ extern "C" int culsh_gsm_stats_tc(const int8_t *tiles, int64_t ld, int64_t w, in
     int every = kSyncEvery, lag = kSyncLag;
     if (const char *e = getenv("CULSH_GSM_SYNC")) sscanf(e, "%d,%d", &every, &lag);
     gsm_stats_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(tiles, ld, (int)(w / kBK), accumulate, g_xx, g_rx,
-                                                            g_rr, g_qx, prog, every, lag);
+                                                            g_rr, g_qx, g_xr, g_xq, prog, every, lag);
     CULSH_LAUNCH_CHECK();
     if (getenv("CULSH_GSM_DEBUG")) {
         int timeouts = 0;

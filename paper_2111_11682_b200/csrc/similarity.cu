@@ -186,6 +186,137 @@ gsm_merge_kernel(const int64_t *__restrict__ col_ptr, const int32_t *__restrict_
     block_merge_topk<KMAX>(L, K, entries + blockIdx.x * (int64_t)K);
 }
 
+// Warp top-K list in registers: entry k = q * 32 + lane lives in lane `lane`, slot q (KE
+// slots per lane, K <= 32 * KE), kept sorted best-first under `better` (similarity desc,
+// index asc -- the order _topk_insert's strict comparisons produce).  Only static indexing,
+// so the list never touches local memory (the per-thread insertion lists it replaces
+// spilled: 32 GB of local-memory DRAM writes per C3 select).
+template <int KE>
+struct WarpTopK {
+    double s[KE];
+    int32_t j[KE];
+    int count = 0;
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int q = 0; q < KE; ++q) { s[q] = -DBL_MAX; j[q] = INT32_MAX; }
+    }
+    // the K-th (worst kept) entry, warp-uniform
+    __device__ __forceinline__ void kth(int K, double &ts, int32_t &tj) const {
+        const int q = (K - 1) >> 5, l = (K - 1) & 31;
+        double v = s[0];
+        int32_t x = j[0];
+#pragma unroll
+        for (int p = 1; p < KE; ++p) if (p == q) { v = s[p]; x = j[p]; }
+        ts = __shfl_sync(0xffffffffu, v, l);
+        tj = __shfl_sync(0xffffffffu, x, l);
+    }
+    // insert a warp-uniform candidate (caller guarantees it belongs in the top K)
+    __device__ __forceinline__ void insert(double cs, int32_t cj, int K) {
+        const unsigned lane = lane_id();
+        int pos = 0;
+#pragma unroll
+        for (int q = 0; q < KE; ++q) {
+            const int k = q * 32 + (int)lane;
+            pos += __popc(__ballot_sync(0xffffffffu, k < count && better(s[q], j[q], cs, cj)));
+        }
+        double ps[KE];
+        int32_t pj[KE];
+#pragma unroll
+        for (int q = 0; q < KE; ++q) {   // entry k - 1 of every k: lane - 1 of slot q, or lane 31 of slot q - 1
+            double up = __shfl_up_sync(0xffffffffu, s[q], 1);
+            int32_t upj = __shfl_up_sync(0xffffffffu, j[q], 1);
+            const double wrap = __shfl_sync(0xffffffffu, q > 0 ? s[q > 0 ? q - 1 : 0] : 0.0, 31);
+            const int32_t wrapj = __shfl_sync(0xffffffffu, q > 0 ? j[q > 0 ? q - 1 : 0] : 0, 31);
+            ps[q] = lane == 0 ? wrap : up;
+            pj[q] = lane == 0 ? wrapj : upj;
+        }
+#pragma unroll
+        for (int q = 0; q < KE; ++q) {
+            const int k = q * 32 + (int)lane;
+            if (k == pos) { s[q] = cs; j[q] = cj; }
+            else if (k > pos && k < K) { s[q] = ps[q]; j[q] = pj[q]; }
+        }
+        if (count < K) ++count;
+    }
+    // offer one candidate per lane (valid lanes only): accepted ones are inserted in lane order
+    __device__ __forceinline__ void offer(bool valid, double cs, int32_t cj, int K) {
+        double ts = -DBL_MAX;
+        int32_t tj = INT32_MAX;
+        if (count >= K) kth(K, ts, tj);
+        unsigned acc = __ballot_sync(0xffffffffu, valid && (count < K || better(cs, cj, ts, tj)));
+        while (acc) {
+            const int l = __ffs(acc) - 1;
+            acc &= acc - 1u;
+            const double vs = __shfl_sync(0xffffffffu, cs, l);
+            const int32_t vj = __shfl_sync(0xffffffffu, cj, l);
+            if (count >= K) {                       // the threshold moved: re-check
+                kth(K, ts, tj);
+                if (!better(vs, vj, ts, tj)) continue;
+            }
+            insert(vs, vj, K);
+        }
+    }
+};
+
+// Count route selection, warp-parallel: block per target column j1, each warp offers 32
+// candidates j2 at a time to its register top-K list, then warp 0 merges the others' lists.
+// All six statistics are read row-wise (s2 / q2 from the transposed copies g_xr / g_xq
+// written by the tensor-core kernel's epilogue; the strided reads of the transposes cost
+// ~20 GB of sector traffic at C3).
+template <int KE>
+__global__ void __launch_bounds__(kSelThreads)
+gsm_count_select_warp_kernel(const int32_t *__restrict__ g_xx, const int32_t *__restrict__ g_rx,
+                             const int32_t *__restrict__ g_rr, const int32_t *__restrict__ g_qx,
+                             const int32_t *__restrict__ g_xr, const int32_t *__restrict__ g_xq, int64_t ld,
+                             int64_t N, int64_t j_lo, int K, double lambda_rho, int32_t *__restrict__ entries) {
+    constexpr int NW = kSelThreads / 32;
+    __shared__ double m_s[NW][32 * KE];
+    __shared__ int32_t m_j[NW][32 * KE];
+    __shared__ int m_n[NW];
+    const int64_t j1 = j_lo + blockIdx.x;
+    const int64_t row = j1 * ld;
+    const unsigned lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    WarpTopK<KE> L;
+    L.init();
+    for (int64_t base = (int64_t)warp * 32; base < N; base += kSelThreads) {
+        const int64_t j2 = base + lane;
+        const bool valid = j2 < N && j2 != j1;
+        double sim = 0.0;
+        if (valid) {
+            PairStats st;
+            st.n = (double)g_xx[row + j2];
+            st.s1 = (double)g_rx[row + j2];
+            st.s2 = (double)g_xr[row + j2];
+            st.s12 = (double)g_rr[row + j2];
+            st.q1 = (double)g_qx[row + j2];
+            st.q2 = (double)g_xq[row + j2];
+            sim = shrunk_of(st, lambda_rho);
+        }
+        L.offer(valid, sim, (int32_t)j2, K);
+    }
+#pragma unroll
+    for (int q = 0; q < KE; ++q) {
+        m_s[warp][q * 32 + lane] = L.s[q];
+        m_j[warp][q * 32 + lane] = L.j[q];
+    }
+    if (lane == 0) m_n[warp] = L.count;
+    __syncthreads();
+    if (warp == 0) {
+        for (int w = 1; w < NW; ++w)
+            for (int k0 = 0; k0 < m_n[w]; k0 += 32) {
+                const int k = k0 + (int)lane;
+                const bool v = k < m_n[w];
+                L.offer(v, v ? m_s[w][k] : -DBL_MAX, v ? m_j[w][k] : INT32_MAX, K);
+            }
+#pragma unroll
+        for (int q = 0; q < KE; ++q) {
+            const int k = q * 32 + (int)lane;
+            if (k < K) entries[blockIdx.x * (int64_t)K + k] = L.j[q];
+        }
+    }
+}
+
 // Count route, selection over the int32 products (rows [j_lo, j_lo + n_rows) of
 // the N x N statistics; g_* row r holds target column j_lo + r, ld = row stride).
 // s2 / q2 are read from the transposed entry of the full products g_rx / g_qx.
@@ -295,14 +426,25 @@ extern "C" int culsh_gsm_densify_rows(const int64_t *col_ptr, const int32_t *col
 }
 
 extern "C" int culsh_gsm_count_select(const int32_t *g_xx, const int32_t *g_rx, const int32_t *g_rr,
-                                      const int32_t *g_qx, int64_t ld, int64_t N, int64_t j_lo, int64_t n_rows,
-                                      int K, double lambda_rho, int32_t *entries, void *stream) {
+                                      const int32_t *g_qx, const int32_t *g_xr, const int32_t *g_xq, int64_t ld,
+                                      int64_t N, int64_t j_lo, int64_t n_rows, int K, double lambda_rho,
+                                      int32_t *entries, void *stream) {
     CULSH_REQUIRE(K >= 1 && K <= 128 && K <= N - 1, "GSM needs 1 <= K <= min(128, N-1)");
     CULSH_REQUIRE(j_lo >= 0 && n_rows >= 0 && j_lo + n_rows <= N && ld >= N, "row range out of bounds");
     if (n_rows == 0) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned grid = (unsigned)n_rows;
     const size_t smem = 0;
+    if (g_xr && g_xq) {
+        if (K <= 32) gsm_count_select_warp_kernel<1><<<grid, kSelThreads, 0, st>>>(
+            g_xx, g_rx, g_rr, g_qx, g_xr, g_xq, ld, N, j_lo, K, lambda_rho, entries);
+        else if (K <= 64) gsm_count_select_warp_kernel<2><<<grid, kSelThreads, 0, st>>>(
+            g_xx, g_rx, g_rr, g_qx, g_xr, g_xq, ld, N, j_lo, K, lambda_rho, entries);
+        else gsm_count_select_warp_kernel<4><<<grid, kSelThreads, 0, st>>>(
+            g_xx, g_rx, g_rr, g_qx, g_xr, g_xq, ld, N, j_lo, K, lambda_rho, entries);
+        CULSH_LAUNCH_CHECK();
+        return CULSH_OK;
+    }
     CULSH_GSM_KDISPATCH(gsm_count_select_kernel, g_xx, g_rx, g_rr, g_qx, ld, N, j_lo, K, lambda_rho, entries);
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;

@@ -128,11 +128,11 @@ def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
     N, M = d.N, d.M
     ld = max(128, (N + 127) // 128 * 128)
     free = t.cuda.mem_get_info()[0]
-    prod_bytes = 4 * ld * ld * 4
+    prod_bytes = 6 * ld * ld * 4
     # rows of the dense panels per pass (int32 products accumulate exactly across passes)
     budget = max(int(0.5 * free) - prod_bytes, 3 * ld * 64)
     mc = max(64, min((M + 63) // 64 * 64, budget // (3 * ld) // 64 * 64))
-    g = t.empty((4, ld, ld), dtype=t.int32, device=nat.device())
+    g = t.empty((6, ld, ld), dtype=t.int32, device=nat.device())   # + transposes of R X', Q X' 
     st = nat.zeros((1,), "int32")
     if os.environ.get("CULSH_GSM_DEBUG"):
         print(f"_gsm_count: free={free / 2**30:.1f} GiB rows/pass={mc} passes={-(-M // mc)}", file=sys.stderr)
@@ -145,10 +145,10 @@ def _gsm_count(d, K: int, lambda_rho: float, entries) -> bool:
         if int(st.item()):
             return False
         nat.call("culsh_gsm_stats_tc", nat.ptr(pan), ld, w, int(m0 > 0), nat.ptr(g[0]), nat.ptr(g[1]),
-                 nat.ptr(g[2]), nat.ptr(g[3]), nat.stream_ptr())
+                 nat.ptr(g[2]), nat.ptr(g[3]), nat.ptr(g[4]), nat.ptr(g[5]), nat.stream_ptr())
         del pan
-    nat.call("culsh_gsm_count_select", nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]), nat.ptr(g[3]), ld, N,
-             0, N, K, float(lambda_rho), nat.ptr(entries), nat.stream_ptr())
+    nat.call("culsh_gsm_count_select", nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]), nat.ptr(g[3]),
+             nat.ptr(g[4]), nat.ptr(g[5]), ld, N, 0, N, K, float(lambda_rho), nat.ptr(entries), nat.stream_ptr())
     return True
 
 

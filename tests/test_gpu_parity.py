@@ -807,8 +807,8 @@ class TestGsm:
         import torch
         from paper_2111_11682_b200 import _native as nat
         gen = torch.Generator().manual_seed(ld + w)
-        g = torch.zeros((4, ld, ld), dtype=torch.int32, device="cuda")
-        want = torch.zeros((4, ld, ld), dtype=torch.int64)
+        g = torch.zeros((6, ld, ld), dtype=torch.int32, device="cuda")
+        want = torch.zeros((6, ld, ld), dtype=torch.int64)
         for ps in range(passes):
             pan = torch.randint(-11, 12, (3, ld, w), generator=gen, dtype=torch.int8)
             pan[0] = (pan[0] > 0).to(torch.int8)           # indicator
@@ -818,14 +818,16 @@ class TestGsm:
             want[1] += r @ x.T
             want[2] += r @ r.T
             want[3] += q @ x.T
+            want[4] += x @ r.T          # transposed copies for the select kernel
+            want[5] += x @ q.T
             dpan = pan.cuda()
             tiles = torch.empty_like(dpan)
             nat.call("culsh_gsm_tile_panels", nat.ptr(dpan), ld, w, nat.ptr(tiles), nat.stream_ptr())
             nat.call("culsh_gsm_stats_tc", nat.ptr(tiles), ld, w, int(ps > 0), nat.ptr(g[0]), nat.ptr(g[1]),
-                     nat.ptr(g[2]), nat.ptr(g[3]), nat.stream_ptr())
+                     nat.ptr(g[2]), nat.ptr(g[3]), nat.ptr(g[4]), nat.ptr(g[5]), nat.stream_ptr())
         torch.cuda.synchronize()
         got = g.cpu().to(torch.int64)
-        for i, name in enumerate(("xx", "rx", "rr", "qx")):
+        for i, name in enumerate(("xx", "rx", "rr", "qx", "xr", "xq")):
             assert torch.equal(got[i], want[i]), name
 
     def test_gsm_mid_scale_vs_oracle(self, P, orc):

@@ -21,7 +21,7 @@ def main():
     ld = (N + 127) // 128 * 128
     w = (M + 63) // 64 * 64
     pan = torch.zeros((3 * ld * w,), dtype=torch.int8, device="cuda")
-    g = torch.empty((4, ld, ld), dtype=torch.int32, device="cuda")
+    g = torch.empty((6, ld, ld), dtype=torch.int32, device="cuda")
     st = nat.zeros((1,), "int32")
     entries = nat.empty((N * K,), "int32")
     for r in range(runs):
@@ -32,9 +32,10 @@ def main():
                  ld, w, nat.ptr(pan), nat.ptr(st), nat.stream_ptr())
         ev[1].record()
         nat.call("culsh_gsm_stats_tc", nat.ptr(pan), ld, w, 0, nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]),
-                 nat.ptr(g[3]), nat.stream_ptr())
+                 nat.ptr(g[3]), nat.ptr(g[4]), nat.ptr(g[5]), nat.stream_ptr())
         ev[2].record()
-        nat.call("culsh_gsm_count_select", nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]), nat.ptr(g[3]), ld, N, 0, N,
+        nat.call("culsh_gsm_count_select", nat.ptr(g[0]), nat.ptr(g[1]), nat.ptr(g[2]), nat.ptr(g[3]),
+                 nat.ptr(g[4]), nat.ptr(g[5]), ld, N, 0, N,
                  K, 100.0, nat.ptr(entries), nat.stream_ptr())
         ev[3].record()
         torch.cuda.synchronize()
