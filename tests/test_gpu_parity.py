@@ -830,6 +830,20 @@ class TestGsm:
         for i, name in enumerate(("xx", "rx", "rr", "qx", "xr", "xq")):
             assert torch.equal(got[i], want[i]), name
 
+    @pytest.mark.parametrize("K", [50, 100])
+    def test_gsm_large_k_vs_oracle(self, P, orc, K):
+        """K > 32 (two / four top-K entries per lane in the warp select): count route ==
+        merge route == oracle."""
+        rng = np.random.default_rng(K)
+        M, N = 3000, 160
+        mask = rng.random((M, N)) < 0.05
+        rows, cols = np.nonzero(mask)
+        r = P.SparseRatings(M, N, rows, cols, rng.integers(1, 6, len(rows)).astype(np.float64))
+        cfg = P.SimilarityConfig(K=K, lambda_rho=10.0)
+        a = P.gsm_topk(r, cfg, method="count").entries
+        assert np.array_equal(a, P.gsm_topk(r, cfg, method="merge").entries)
+        assert np.array_equal(a, orc.gsm_topk(r.col_ptr, r.col_rows, r.col_vals, N, K, 10.0))
+
     def test_gsm_mid_scale_vs_oracle(self, P, orc):
         """20,000 x 3,000, ~600k integer ratings: count route == merge route == oracle."""
         rng = np.random.default_rng(7)
