@@ -95,11 +95,7 @@ struct ExactPre {
     int64_t base;
 };
 
-// PF (online column pass, row_mode 2): old rows (i < M_old) are read-only in the pass, so
-// the next entry's u_i / b_i are loaded one update ahead when its row is old -- the HBM/L2
-// latency of the row gather leaves the column's dependency chain (a new column's ~5,600
-// updates are one sequential chain); new rows keep the in-order wait-then-load.
-template <int FPL, int KPL, bool PF = false>
+template <int FPL, int KPL>
 __global__ void __launch_bounds__(256)
 exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                  const int32_t *__restrict__ chain_lo, int64_t col_lo, int64_t col_hi, int row_mode,
@@ -139,10 +135,6 @@ exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
         const int32_t cl = chain_lo ? chain_lo[j] : (int32_t)col_lo;
         const int64_t lo = seg[2 * j], hi = seg[2 * j + 1];
         bool stop = false;
-        double u_pf[FPL], bi_pf = 0.0;
-        bool have_pf = false;
-#pragma unroll
-        for (int q = 0; q < FPL; ++q) u_pf[q] = 0.0;
 
         for (int64_t idx = lo; idx < hi && !stop; ++idx) {
             const int32_t i = P.col_rows[idx];
@@ -186,39 +178,13 @@ exact_col_kernel(ExactModel P, CulshRates R, const int64_t *__restrict__ seg,
                 __syncwarp();
             }
             double u[FPL];
-            double bi;
-            if (PF && have_pf) {   // prefetched one update ago (old row: constant in this pass)
-#pragma unroll
-                for (int q = 0; q < FPL; ++q) u[q] = u_pf[q];
-                bi = bi_pf;
-            } else {
-#pragma unroll
-                for (int q = 0; q < FPL; ++q) {
-                    const int f = lane + 32 * q;
-                    u[q] = f < F ? __ldcg(&P.U[(int64_t)i * F + f]) : 0.0;
-                }
-                bi = __ldcg(&P.b[i]);
-            }
-            if (PF) {   // the next entry's row, if old: its loads overlap this update
-                have_pf = false;
-                if (idx + 1 < hi) {
-                    const int32_t i2 = P.col_rows[idx + 1];
-                    if (i2 < M_old) {
-#pragma unroll
-                        for (int q = 0; q < FPL; ++q) {
-                            const int f = lane + 32 * q;
-                            u_pf[q] = f < F ? __ldcg(&P.U[(int64_t)i2 * F + f]) : 0.0;
-                        }
-                        bi_pf = __ldcg(&P.b[i2]);
-                        have_pf = true;
-                    }
-                }
-            }
 #pragma unroll
             for (int q = 0; q < FPL; ++q) {
                 const int f = lane + 32 * q;
+                u[q] = f < F ? __ldcg(&P.U[(int64_t)i * F + f]) : 0.0;
                 if (f < F) buf[f] = u[q] * v[q];
             }
+            const double bi = __ldcg(&P.b[i]);
 #pragma unroll
             for (int q = 0; q < KPL; ++q) {
                 const int k = lane + 32 * q;
@@ -445,18 +411,16 @@ int launch_col(const ExactModel &P, const CulshRates &R, const int64_t *seg, con
                int *ticket, int *status, cudaStream_t st, ExactPre pre) {
     const int threads = 128;
     const size_t smem = (size_t)(threads / 32) * (P.F + P.K) * sizeof(double);
-    const bool pf = row_mode == 2;
-    auto kern = pf ? exact_col_kernel<FPL, KPL, true> : exact_col_kernel<FPL, KPL, false>;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, exact_col_kernel<FPL, KPL>, threads, smem);
     if (occ < 1) occ = 1;
     const int64_t ncols = col_hi - col_lo;
     int64_t blocks = (int64_t)num_sms() * occ;
     const int64_t need = (ncols + (threads / 32) - 1) / (threads / 32);
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, threads, smem, st>>>(P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant,
-                                                   row_last, ticket, status, pre);
+    exact_col_kernel<FPL, KPL><<<(unsigned)blocks, threads, smem, st>>>(
+        P, R, seg, chain_lo, col_lo, col_hi, row_mode, M_old, variant, row_last, ticket, status, pre);
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
 }
 
