@@ -306,3 +306,27 @@ def test_staged_copies_round_trip(P, dtype):
         assert b.dtype == a.dtype and b.tobytes() == a.tobytes()
     small = np.arange(1000, dtype=dtype)
     assert nat.to_host(nat.to_dev(small)).tobytes() == small.tobytes()
+
+
+@pytest.mark.parametrize("integer", [True, False])
+def test_sparse_ratings_device_build_equals_host_build(P, integer, monkeypatch):
+    """SparseRatings from host triplets >= 1M entries builds CSR / CSC / baselines on the
+    device: every host view (materialised on first read) and the baselines equal the host
+    lexsort build byte for byte, including duplicate (row, col) entries (ties in entry order)."""
+    import paper_2111_11682_b200.data as D
+    rng = np.random.default_rng(11)
+    M, N, n = 5000, 900, 1_300_000
+    rows = rng.integers(0, M, n).astype(np.int32)       # duplicates included on purpose
+    cols = rng.integers(0, N, n).astype(np.int32)
+    vals = (rng.integers(1, 6, n).astype(np.float64) if integer else rng.random(n) * 5)
+    dev = P.SparseRatings(M, N, rows.copy(), cols.copy(), vals.copy())
+    assert dev._dev is not None and "row_ptr" not in dev.__dict__
+    monkeypatch.setattr(D, "_DEVICE_BUILD_MIN", 1 << 62)
+    host = P.SparseRatings(M, N, rows.copy(), cols.copy(), vals.copy())
+    assert host._dev is None
+    for name in ("entry_rows", "entry_cols", "entry_values", "row_ptr", "row_cols", "row_vals",
+                 "col_ptr", "col_rows", "col_vals"):
+        assert getattr(dev, name).tobytes() == getattr(host, name).tobytes(), name
+        assert not getattr(dev, name).flags.writeable
+    a, b = dev.baselines(), host.baselines()
+    assert a.mu == b.mu and a.b.tobytes() == b.b.tobytes() and a.b_hat.tobytes() == b.b_hat.tobytes()
