@@ -277,7 +277,16 @@ def build_indices(triplets: Triplets, M: int | None = None, N: int | None = None
         raise ValueError("column index out of range")
     if len(vals) and not np.all(np.isfinite(vals)):
         raise ValueError("non-finite rating value")
-    if len(rows):
+    if len(rows) >= _DEVICE_BUILD_MIN and _gpu_present():
+        # the same first duplicate as the host lexsort below: stable device sort of row*N+col
+        t = nat.torch()
+        key = nat.to_dev(np.asarray(rows, np.int64)) * int(N) + nat.to_dev(np.asarray(cols, np.int64))
+        sk, order = t.sort(key, stable=True)
+        same = t.nonzero(sk[1:] == sk[:-1])
+        if same.numel():
+            k = int(order[int(same[0, 0].item())].item())
+            raise ValueError(f"duplicate entry at (row={rows[k]}, col={cols[k]})")
+    elif len(rows):
         order = np.lexsort((cols, rows))
         same = (np.diff(rows[order]) == 0) & (np.diff(cols[order]) == 0)
         if same.any():

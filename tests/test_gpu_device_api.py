@@ -330,3 +330,24 @@ def test_sparse_ratings_device_build_equals_host_build(P, integer, monkeypatch):
         assert not getattr(dev, name).flags.writeable
     a, b = dev.baselines(), host.baselines()
     assert a.mu == b.mu and a.b.tobytes() == b.b.tobytes() and a.b_hat.tobytes() == b.b_hat.tobytes()
+
+
+def test_build_indices_duplicate_check_on_device(P):
+    """build_indices on >= 1M triplets checks duplicates on the device and reports the same
+    first duplicate as the reference's lexsort (data.py:269-286)."""
+    rng = np.random.default_rng(4)
+    M, N = 4000, 3000
+    key = rng.choice(M * N, 1_200_000, replace=False)
+    rows, cols = (key // N).astype(np.int32), (key % N).astype(np.int32)
+    vals = rng.integers(1, 6, len(key)).astype(np.float64)
+    r = P.build_indices(P.Triplets(rows, cols, vals), M=M, N=N)
+    assert r.nnz == len(key)
+    rows2, cols2 = rows.copy(), cols.copy()
+    rows2[1_000_000], cols2[1_000_000] = rows2[17], cols2[17]        # entry 17 duplicated later
+    rows2[500_000], cols2[500_000] = rows2[900_000], cols2[900_000]  # and another pair
+    order = np.lexsort((cols2, rows2))
+    same = (np.diff(rows2[order]) == 0) & (np.diff(cols2[order]) == 0)
+    k = order[int(np.flatnonzero(same)[0])]
+    import re
+    with pytest.raises(ValueError, match=re.escape(f"duplicate entry at (row={rows2[k]}, col={cols2[k]})")):
+        P.build_indices(P.Triplets(rows2, cols2, vals), M=M, N=N)
