@@ -338,6 +338,20 @@ int culsh_rmse_train(const CulshData *d, const CulshModel64 *m, const uint32_t *
                      double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
                      double *rmse_out, void *stream);
 
+/* factorization.py:559-579 rmse over the TRAINING set in CSR order, for N <= 65536: one
+ * warp per row (U[i] broadcast, the lanes' V rows staged; a per-warp shared bitmap of the
+ * row's columns answers "rated J[j, k]?", rated ones binary-search the row for the value).
+ * No lookup cache.  csr_entry[p] = entry index of CSR position p (NULL: identity); the
+ * squared errors are the same bytes as culsh_rmse_train's and are summed in entry order.
+ * The _m32 form reads a Hogwild fit's fp32 arrays (arguments as culsh_rmse_train_m32). */
+int culsh_rmse_train_rows(const CulshData *d, const CulshModel64 *m, const int32_t *csr_entry,
+                          int do_clamp, double clamp_lo, double clamp_hi, double unscale,
+                          double *sqerr_scratch, double *rmse_out, void *stream);
+int culsh_rmse_train_rows_m32(const CulshData *d, const CulshModel32 *m, double mu, int F,
+                              const int32_t *nbr, const int32_t *csr_entry, int do_clamp,
+                              double clamp_lo, double clamp_hi, double unscale,
+                              double *sqerr_scratch, double *rmse_out, void *stream);
+
 /* factorization.py:235-263 _predict_one for n (i, j) pairs -> out (n) f64. */
 int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows,
                   const int32_t *cols, int64_t n, double *out, void *stream);

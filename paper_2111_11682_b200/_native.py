@@ -124,6 +124,9 @@ _SIGS = {
                        _f64, _vp, _vp, _vp],
     "culsh_rmse_train_m32": [_P(CulshData), _P(CulshModel32), _f64, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _f64,
                              _f64, _f64, _vp, _vp, _vp],
+    "culsh_rmse_train_rows": [_P(CulshData), _P(CulshModel64), _vp, _i32, _f64, _f64, _f64, _vp, _vp, _vp],
+    "culsh_rmse_train_rows_m32": [_P(CulshData), _P(CulshModel32), _f64, _i32, _vp, _vp, _i32, _f64, _f64, _f64,
+                                  _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "culsh_predict": [_P(CulshData), _P(CulshModel64), _vp, _vp, _i64, _vp, _vp],
     "culsh_csc_to_csr_map": [_P(CulshData), _vp, _vp],
@@ -304,7 +307,7 @@ def copy_to_device(dst, a: np.ndarray) -> None:
     t = torch()
     a = np.ascontiguousarray(a)
     nb = a.nbytes
-    if nb < (16 << 20):
+    if nb < _STAGE_MIN:
         dst.view(-1).view(t.uint8)[:nb].copy_(t.from_numpy(a.reshape(-1).view(np.uint8)))
         return
     with _stage_lock:
@@ -343,7 +346,7 @@ def to_dev(a: np.ndarray, dtype=None):
         a = a.view(np.int64)
     elif a.dtype == np.uint32:
         a = a.view(np.int32)
-    if a.nbytes >= (16 << 20) and a.dtype in _NP2T:
+    if a.nbytes >= _STAGE_MIN and a.dtype in _NP2T:
         out = t.empty(a.shape, dtype=getattr(t, _NP2T[a.dtype]), device=dev)
         copy_to_device(out, a)
         return out
@@ -353,6 +356,8 @@ def to_dev(a: np.ndarray, dtype=None):
 
 
 _STAGE_BYTES = 64 << 20          # two reusable pinned staging chunks per process
+_STAGE_MIN = 1 << 20             # H2D copies from this size on go through them (pageable
+                                 # torch copies of a 1 % C3 test set: ~20 ms for 16 MB)
 _stage = None
 _pool = None
 import threading as _threading

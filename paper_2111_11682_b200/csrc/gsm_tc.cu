@@ -56,34 +56,6 @@ constexpr int kSyncEvery = 512;              // producer checkpoint every 512 K 
 constexpr int kSyncLag = 4;                  // ... at most 4 checkpoints ahead of the slowest CTA
                                              // (CULSH_GSM_SYNC="every,lag" overrides; 0 = off)
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-
 // Byte offset of panel p (0 = X, 1 = R, 2 = Q), column j, K position k in the tiled layout.
 // Groups are K-block-major (group = kb * nrb + rb): the blocks the co-resident tiles read at
 // one K step are contiguous (rb-major placed them nkb * 24 KB apart -- a 2^17-multiple

@@ -3,6 +3,8 @@
 // order (explicit _rn intrinsics; the TU is also compiled with -fmad=false); the RMSE sum
 // is sequential (bit-identical to factorization.py:394-409) when `sequential` is set,
 // otherwise a fixed pairwise tree (deterministic, within a few ulp of the sequential sum).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace culsh {
@@ -227,6 +229,229 @@ __global__ void __launch_bounds__(PRE ? 128 : 64) pred_tile_kernel(CulshData d, 
     }
 }
 
+// Training-set RMSE in CSR order (N <= 65,536): one warp per row i at a time, U[i] kept
+// in shared memory and the 32 ratings' V rows, J^K rows and C rows staged per 32-rating
+// chunk (V, J^K, W and C are the small, L2-resident side; the CSC-order kernel above
+// gathers a 1 KB U row per rating from HBM instead).  Staging is 16-byte cp.async into
+// 32 x 32-element tiles whose 16-byte granules are XOR-swizzled by row, so lane r reads
+// its own row with conflict-free 16-byte shared loads.  The row's columns go into a
+// per-warp shared bitmap with per-word prefix counts: "did row i rate J[j, k]" is one bit
+// probe and the value's CSR position is rlo + prefix + popc (no search); the rare rated
+// neighbour reads its W entry directly.  Lane x owns rating x and runs its f and k loops in
+// the reference's order, so the squared errors are the bytes of the CSC kernel's (stored
+// at entry index csr_entry[p], NULL: identity).  (Measured alternatives, C3 fp64: one bulk
+// copy per lane instead of the cp.async granules 28.8 ms vs 26.2 ms; double-buffered bulk
+// stages 79 ms -- 32 KB per warp leaves one 4-warp CTA per SM.)
+constexpr int kRowWarpsRmse = 4;
+constexpr int kRowTile = 32 * 32;   // elements of one staged tile
+
+template <typename T>
+__device__ __forceinline__ int swz(int r, int f) {
+    constexpr int GE = 16 / (int)sizeof(T);
+    return r * 32 + (((f / GE) ^ (r & 7)) * GE) + f % GE;
+}
+
+template <typename P>
+struct RowSmem {   // per-warp carve-up (bytes, 16-aligned): V/C tile, J^K tile, bitmap + prefix, U[i]
+    static __host__ __device__ int bytes(int words, int F) {
+        return kRowTile * (int)sizeof(P) + kRowTile * 4 + 8 * ((words + 1) & ~1) + ((F + 31) & ~31) * (int)sizeof(P);
+    }
+};
+
+// Rows [0, cnt) of the chunk's ne ratings (lane r's row starts at myrow) -> swizzled tile.
+// vec: 16-byte granules (the caller guarantees 16-byte aligned rows and that the last
+// granule stays inside the array), else element copies.
+template <typename T>
+__device__ __forceinline__ void stage_rows(T *tile, const T *myrow, int ne, int cnt, bool vec, int lane) {
+    constexpr int GE = 16 / (int)sizeof(T);
+    constexpr int G = 32 / GE;     // granules per 32-element row
+    constexpr int RPI = 32 / G;    // rows per instruction
+    const uintptr_t mine = reinterpret_cast<uintptr_t>(myrow);
+    if (vec) {
+        const int g = lane % G, rs = lane / G;
+        const int ng = (cnt + GE - 1) / GE;
+        for (int r0 = 0; r0 < ne; r0 += RPI) {
+            const int r = r0 + rs;
+            const T *src = reinterpret_cast<const T *>(__shfl_sync(0xffffffffu, mine, r & 31));
+            if (r < ne && g < ng) cp_async<16>(tile + r * 32 + ((g ^ (r & 7)) * GE), src + g * GE);
+        }
+    } else {
+#pragma unroll 4
+        for (int r = 0; r < ne; ++r) {
+            const T *src = reinterpret_cast<const T *>(__shfl_sync(0xffffffffu, mine, r));
+            if (lane < cnt) cp_async<sizeof(T)>(tile + swz<T>(r, lane), src + lane);
+        }
+    }
+}
+
+template <typename P>
+__global__ void __launch_bounds__(kRowWarpsRmse * 32, 3)
+    pred_row_kernel(CulshData d, double mu, const P *__restrict__ b, const P *__restrict__ bhat,
+                    const P *__restrict__ U, const P *__restrict__ V, const P *__restrict__ W,
+                    const P *__restrict__ C, const int32_t *__restrict__ nbr, int F, int ldF, int K,
+                    int words, int vec, const int32_t *__restrict__ csr_entry, int do_clamp, double lo,
+                    double hi, double unscale, double *__restrict__ out) {
+    using V2 = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
+    constexpr int GE = 16 / (int)sizeof(P);
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const int wid = threadIdx.x >> 5;
+    unsigned char *base = s_raw + (size_t)wid * RowSmem<P>::bytes(words, F);
+    P *vt = reinterpret_cast<P *>(base);                                              // V tile, then C tile
+    int32_t *jt = reinterpret_cast<int32_t *>(base + kRowTile * sizeof(P));           // J^K tile
+    uint32_t *bm = reinterpret_cast<uint32_t *>(base + kRowTile * (sizeof(P) + 4));
+    uint32_t *pre = bm + words;                                                       // set bits before w
+    P *us = reinterpret_cast<P *>(base + kRowTile * (sizeof(P) + 4) + 8 * ((words + 1) & ~1));   // U[i]
+    const int Fs = (F + 31) & ~31;
+    const int lane = (int)lane_id();
+    const bool vecV = vec & 1, vecJ = vec & 2, vecC = vec & 4;
+    const int per = (words + 31) >> 5;
+    const int w0 = min(words, lane * per), w1 = min(words, w0 + per);
+    for (int w = lane; w < words; w += 32) bm[w] = 0u;
+    __syncwarp();
+    const int64_t nw = (int64_t)gridDim.x * kRowWarpsRmse;
+    for (int64_t i = (int64_t)blockIdx.x * kRowWarpsRmse + wid; i < d.M; i += nw) {
+        const int64_t rlo = d.row_ptr[i], rhi = d.row_ptr[i + 1];
+        if (rlo == rhi) continue;
+        if (K > 0) {
+            for (int64_t p = rlo + lane; p < rhi; p += 32) {
+                const int32_t c = d.row_cols[p];
+                atomicOr(bm + (c >> 5), 1u << (c & 31));
+            }
+            __syncwarp();
+            int cnt = 0;
+            for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int run = incl - cnt;
+            for (int w = w0; w < w1; ++w) {
+                pre[w] = (uint32_t)run;
+                run += __popc(bm[w]);
+            }
+        }
+        const double mb = __dadd_rn(mu, (double)b[i]);
+        const double mbb = __dadd_rn(mu, d.base_b[i]);
+        for (int f = lane; f < Fs; f += 32) us[f] = f < F ? U[i * ldF + f] : P(0);
+        __syncwarp();
+        for (int64_t c0 = rlo; c0 < rhi; c0 += 32) {
+            const int ne = (int)min64(32, rhi - c0);
+            const bool valid = lane < ne;
+            const int64_t p = c0 + lane;
+            const int32_t j = valid ? d.row_cols[p] : 0;
+            double pred = valid ? __dadd_rn(mb, (double)bhat[j]) : 0.0;
+            double dot = 0.0;
+            for (int f0 = 0; f0 < F; f0 += 32) {
+                const int fe = F - f0 < 32 ? F - f0 : 32;
+                stage_rows<P>(vt, V + (int64_t)j * ldF + f0, ne, fe, vecV, lane);
+                cp_async_wait_all();
+                __syncwarp();
+                if (valid) {
+                    const P *uf = us + f0;
+                    if (fe == 32) {   // full chunk: no bounds, loads hoisted
+#pragma unroll 4
+                        for (int g = 0; g < 32 / GE; ++g) {
+                            const V2 v = *reinterpret_cast<const V2 *>(vt + lane * 32 + ((g ^ (lane & 7)) * GE));
+                            const V2 u = *reinterpret_cast<const V2 *>(uf + g * GE);
+                            const P *vv = reinterpret_cast<const P *>(&v);
+                            const P *uu = reinterpret_cast<const P *>(&u);
+#pragma unroll
+                            for (int e = 0; e < GE; ++e) dot = __dadd_rn(dot, __dmul_rn((double)uu[e], (double)vv[e]));
+                        }
+                    } else {
+                        for (int q = 0; q < fe; ++q)
+                            dot = __dadd_rn(dot, __dmul_rn((double)uf[q], (double)vt[swz<P>(lane, q)]));
+                    }
+                }
+                __syncwarp();
+            }
+            pred = __dadd_rn(pred, dot);
+            int nr = 0, nn = 0;
+            double sw = 0.0, sc = 0.0;
+            for (int k0 = 0; k0 < K; k0 += 32) {
+                const int kn = K - k0 < 32 ? K - k0 : 32;
+                const int64_t jrow = (int64_t)j * K + k0;
+                stage_rows<int32_t>(jt, nbr + jrow, ne, kn, vecJ, lane);
+                stage_rows<P>(vt, C + jrow, ne, kn, vecC, lane);
+                cp_async_wait_all();
+                __syncwarp();
+                if (valid) {
+                    for (int g = 0; g * 4 < kn; ++g) {
+                        const int4 j4 = *reinterpret_cast<const int4 *>(jt + lane * 32 + ((g ^ (lane & 7)) * 4));
+                        const int32_t *jj = reinterpret_cast<const int32_t *>(&j4);
+                        P cv[4];
+                        *reinterpret_cast<V2 *>(cv) =
+                            *reinterpret_cast<const V2 *>(vt + lane * 32 + (((4 * g / GE) ^ (lane & 7)) * GE));
+                        if (GE == 2)
+                            *reinterpret_cast<V2 *>(cv + 2) =
+                                *reinterpret_cast<const V2 *>(vt + lane * 32 + (((4 * g / GE + 1) ^ (lane & 7)) * GE));
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int k = g * 4 + e;
+                            if (k >= kn) break;
+                            const int32_t j1 = jj[e];
+                            const uint32_t word = bm[j1 >> 5];
+                            if ((word >> (j1 & 31)) & 1u) {
+                                const int64_t pos = rlo + pre[j1 >> 5] + __popc(word & ((1u << (j1 & 31)) - 1u));
+                                ++nr;
+                                sw = __dadd_rn(sw, __dmul_rn(__dsub_rn(d.row_vals[pos],
+                                                                       __dadd_rn(mbb, d.base_bhat[j1])),
+                                                             (double)__ldg(W + jrow + k)));
+                            } else {
+                                ++nn;
+                                sc = __dadd_rn(sc, (double)cv[e]);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (nr > 0) pred = __dadd_rn(pred, __ddiv_rn(sw, __dsqrt_rn((double)nr)));
+            if (nn > 0) pred = __dadd_rn(pred, __ddiv_rn(sc, __dsqrt_rn((double)nn)));
+            if (valid) {
+                if (do_clamp) {
+                    if (pred < lo) pred = lo;
+                    else if (pred > hi) pred = hi;
+                }
+                const double dd = __dmul_rn(__dsub_rn(pred, d.row_vals[p]), unscale);
+                out[csr_entry ? (int64_t)csr_entry[p] : p] = __dmul_rn(dd, dd);
+            }
+        }
+        if (K > 0) {
+            __syncwarp();
+            for (int64_t p = rlo + lane; p < rhi; p += 32) bm[d.row_cols[p] >> 5] = 0u;
+            __syncwarp();
+        }
+    }
+}
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <typename P>
+int launch_pred_rows(const CulshData *d, double mu, const P *b, const P *bhat, const P *U, const P *V, const P *W,
+                     const P *C, const int32_t *nbr, int F, int ldF, int K, const int32_t *csr_entry, int do_clamp,
+                     double lo, double hi, double unscale, double *sq, cudaStream_t st) {
+    CULSH_REQUIRE(d->N <= 65536, "the CSR-order rmse needs N <= 65536 (per-warp row bitmap)");
+    CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
+    const int words = (int)((d->N + 31) / 32);
+    // 16-byte granule copies: row starts and pitches must be 16-aligned
+    // (then the last granule of a row stays inside the array)
+    const int vec = ((aligned16(V) && (ldF * sizeof(P)) % 16 == 0) ? 1 : 0) |
+                    ((aligned16(nbr) && (K * 4) % 16 == 0) ? 2 : 0) |
+                    ((aligned16(C) && (K * sizeof(P)) % 16 == 0) ? 4 : 0);
+    const size_t smem = (size_t)kRowWarpsRmse * RowSmem<P>::bytes(words, F);
+    CULSH_CHECK(cudaFuncSetAttribute(pred_row_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CULSH_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pred_row_kernel<P>, kRowWarpsRmse * 32, smem));
+    const int64_t blocks = min64((d->M + kRowWarpsRmse - 1) / kRowWarpsRmse, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
+    pred_row_kernel<P><<<(unsigned)blocks, kRowWarpsRmse * 32, smem, st>>>(
+        *d, mu, b, bhat, U, V, W, C, nbr, F, ldF, K, words, vec, csr_entry, do_clamp, lo, hi, unscale, sq);
+    CULSH_LAUNCH_CHECK();
+    return CULSH_OK;
+}
+
 // Lookup cache of the training set: per 32-entry group of CSC entries, the number of
 // explicit (i, J[j, k]) pairs, then their CSC positions (warp scan per group).
 __global__ void lookup_count_kernel(int64_t nnz, const uint32_t *__restrict__ mask, int MW,
@@ -409,5 +634,35 @@ extern "C" int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, d
                                                           nbr, F, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
                                                           do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+}
+
+// factorization.py:559-579 rmse over the training set in CSR order (pred_row_kernel;
+// N <= 65,536, no lookup cache).  csr_entry: entry index of each CSR position (NULL:
+// identity); the sum runs in entry order like culsh_rmse_train.
+extern "C" int culsh_rmse_train_rows(const CulshData *d, const CulshModel64 *m, const int32_t *csr_entry,
+                                     int do_clamp, double clamp_lo, double clamp_hi, double unscale,
+                                     double *sqerr_scratch, double *rmse_out, void *stream) {
+    const int64_t n = d->nnz;
+    CULSH_REQUIRE(n > 0, "empty training set");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rc = launch_pred_rows<double>(d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->nbr, m->F, m->F,
+                                            m->K, csr_entry, do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch,
+                                            st);
+    if (rc != CULSH_OK) return rc;
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+}
+
+extern "C" int culsh_rmse_train_rows_m32(const CulshData *d, const CulshModel32 *m, double mu, int F,
+                                         const int32_t *nbr, const int32_t *csr_entry, int do_clamp,
+                                         double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
+                                         double *rmse_out, void *stream) {
+    const int64_t n = d->nnz;
+    CULSH_REQUIRE(n > 0, "empty training set");
+    CULSH_REQUIRE(F >= 1 && F <= m->F, "logical F exceeds the model's row stride");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rc = launch_pred_rows<float>(d, mu, m->b, m->bhat, m->U, m->V, m->W, m->C, nbr, F, m->F, m->K,
+                                           csr_entry, do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch, st);
+    if (rc != CULSH_OK) return rc;
     return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
 }

@@ -205,6 +205,24 @@ class SparseRatings:
         self._csc_perm_done = True
         return self._csc_perm
 
+    def csr_entry_index(self):
+        """Entry index of every CSR position (int32, device), or None when the entries
+        are in CSR order: the CSC entry permutation carried through csc2csr (cached)."""
+        if self.__dict__.get("_csr_entry_done"):
+            return self._csr_entry
+        t = nat.torch()
+        n = self._nnz
+        dev = self.device()
+        perm = self.csc_entry_perm()
+        src = perm.to(t.int32) if perm is not None else t.arange(n, dtype=t.int32, device=dev.csc2csr.device)
+        ce = t.empty(max(n, 1), dtype=t.int32, device=src.device)
+        if n:
+            ce.scatter_(0, dev.csc2csr[:n].to(t.int64), src)
+        ident = bool(t.equal(ce[:n], t.arange(n, dtype=t.int32, device=ce.device))) if n else True
+        self._csr_entry = None if ident else ce
+        self._csr_entry_done = True
+        return self._csr_entry
+
     def row_slice(self, i: int):
         lo, hi = self.row_ptr[i], self.row_ptr[i + 1]
         return self.row_cols[lo:hi], self.row_vals[lo:hi]

@@ -739,6 +739,9 @@ def _train_lookup(dev, nbr, K: int):
     return mask, base, pos
 
 
+_ROWS_RMSE_MAX_N = 65536   # per-warp row bitmap of the CSR-order training-set kernel
+
+
 def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
          unscale: float | None = None, clamp: tuple[float, float] | None = None) -> float:
     """Root-mean-square error over held-out triplets (factorization.py:559-579).
@@ -760,6 +763,16 @@ def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
     us = 1.0 if unscale is None else float(unscale)
     head = ((ctypes.byref(dev.struct), ctypes.byref(dm.struct), float(dm.mu), int(dm.F), nat.ptr(dm.nbr))
             if m32 else (ctypes.byref(dev.struct), ctypes.byref(dm.struct)))
+    if getattr(testset, "_source", None) is ratings and n == dev.nnz and dev.N <= _ROWS_RMSE_MAX_N:
+        # CSR order, one warp per row (U read once per row; no lookup cache)
+        ce = ratings.csr_entry_index()
+        if m32:
+            nat.call("culsh_rmse_train_rows_m32", *head, nat.ptr(ce), int(clamp is not None), float(lo),
+                     float(hi), us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
+        else:
+            nat.call("culsh_rmse_train_rows", *head, nat.ptr(ce), int(clamp is not None), float(lo), float(hi),
+                     us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
+        return float(out.item())
     if getattr(testset, "_source", None) is ratings and n == dev.nnz:
         K = dm.K
         mask = base = pos = None

@@ -221,6 +221,44 @@ def test_train_set_rmse_path_equals_generic(P, orc, K):
     assert a == b == ref
 
 
+@pytest.mark.parametrize("K,F,mode,order", [(0, 8, "exact", "csr"), (7, 40, "exact", "random"),
+                                          (40, 33, "exact", "csc"), (64, 64, "exact", "random"),
+                                          (16, 64, "hogwild", "random"), (33, 32, "hogwild", "csr")])
+def test_train_set_rmse_row_kernel_equals_lookup_kernel(P, orc, monkeypatch, K, F, mode, order):
+    """The CSR-order training-set kernel (one warp per row, row bitmap) returns the same
+    float as the CSC-order lookup-cache kernel and the oracle: empty rows and columns, rows
+    longer than 32, K spanning two 32-wide halves, entry orders CSR / CSC / random, fp64 and
+    fp32 (Hogwild) models, clamp + unscale."""
+    from paper_2111_11682_b200 import factorization as fz
+    rng = np.random.default_rng(5)
+    M, N = 300, 120
+    dense = rng.random((M, N)) < 0.25
+    dense[7] = False                      # empty row
+    dense[:, 11] = False                  # empty column
+    dense[3, :100] = True                 # long row (4 chunks of 32)
+    rows, cols = np.nonzero(dense)
+    if order == "csc":
+        o = np.lexsort((rows, cols))
+    elif order == "random":
+        o = rng.permutation(len(rows))
+    else:
+        o = np.arange(len(rows))
+    rows, cols = rows[o], cols[o]
+    vals = rng.integers(1, 6, len(rows)).astype(np.float64)
+    r = P.SparseRatings(M, N, rows, cols, vals)
+    tbl = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=6, seed=1), K)[0] if K else None
+    p = P.train_full(r, tbl, P.TrainConfig(F=F, K=K, epochs=2, seed=2), mode=mode)
+    kw = dict(clamp=(1.0, 5.0), unscale=2.0)
+    a = P.rmse(p, r.triplets(), r, **kw)
+    monkeypatch.setattr(fz, "_ROWS_RMSE_MAX_N", 0)
+    b = P.rmse(p, r.triplets(), r, **kw)
+    assert a == b
+    if mode == "exact":
+        d, _ = orc.build_csr(r.M, r.N, rows, cols, vals)
+        m = orc.Model(p.mu, p.b, p.b_hat, p.U, p.V, p.W, p.C, tbl.entries if K else np.zeros((N, 0), np.int32))
+        assert a == orc.rmse(d, m, r.entry_rows, r.entry_cols, r.entry_values, **kw)
+
+
 def test_train_set_rmse_large_tree_sum(P):
     """Above 2^22 ratings both paths use the same fixed tree over entry order."""
     rng = np.random.default_rng(3)
@@ -235,6 +273,13 @@ def test_train_set_rmse_large_tree_sum(P):
     a = P.rmse(p, t, r)
     b = P.rmse(p, P.Triplets(t.rows.copy(), t.cols.copy(), t.values.copy()), r)
     assert a == b and np.isfinite(a)
+    from paper_2111_11682_b200 import factorization as fz
+    old = fz._ROWS_RMSE_MAX_N
+    fz._ROWS_RMSE_MAX_N = 0                    # the CSC lookup-cache kernel
+    try:
+        assert P.rmse(p, t, r) == a
+    finally:
+        fz._ROWS_RMSE_MAX_N = old
 
 
 @pytest.mark.parametrize("n", [1, 7, 8, 9, 127, 128, 129, 1000, 65536, 65537, 300001, 3_000_017])
