@@ -72,6 +72,21 @@ def main():
             "train_kernels_s": kernels(lambda: P.rmse(p, train_t, r)),
             "test_kernels_s": kernels(lambda: P.rmse(p, test, r)),
         }
+    # the same two calls from inside a fit's per-epoch callback (cli.py:204-210), timed per call
+    for mode in ("exact", "hogwild"):
+        seen = []
+
+        def cb(t, q):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.rmse(q, train_t, r)
+            t1 = time.perf_counter()
+            P.rmse(q, test_w, r)
+            t2 = time.perf_counter()
+            seen.append((t1 - t0, t2 - t1))
+
+        P.train_full(r, tbl, P.TrainConfig(F=F, K=K, epochs=4, seed=0, **RATES), mode=mode, epoch_callback=cb)
+        out[mode]["in_callback_s"] = seen
     print(json.dumps(out), flush=True)
 
 
