@@ -352,6 +352,19 @@ int culsh_rmse_train_rows_m32(const CulshData *d, const CulshModel32 *m, double 
                               double clamp_lo, double clamp_hi, double unscale,
                               double *sqerr_scratch, double *rmse_out, void *stream);
 
+/* culsh_rmse over any test set grouped by row (same kernel as culsh_rmse_train_rows,
+ * N <= 65536): row i's targets are [t_ptr[i], t_ptr[i+1]) (t_ptr: M+1 int64) with columns
+ * t_cols, values t_vals and t_index = each target's position in the test set (the sum runs
+ * in test-set order; NULL: identity).  n = number of targets.  Same squared errors as
+ * culsh_rmse on the ungrouped triplets. */
+int culsh_rmse_rows(const CulshData *d, const CulshModel64 *m, const int64_t *t_ptr, const int32_t *t_cols,
+                    const double *t_vals, const int32_t *t_index, int64_t n, int do_clamp, double clamp_lo,
+                    double clamp_hi, double unscale, double *sqerr_scratch, double *rmse_out, void *stream);
+int culsh_rmse_rows_m32(const CulshData *d, const CulshModel32 *m, double mu, int F, const int32_t *nbr,
+                        const int64_t *t_ptr, const int32_t *t_cols, const double *t_vals,
+                        const int32_t *t_index, int64_t n, int do_clamp, double clamp_lo, double clamp_hi,
+                        double unscale, double *sqerr_scratch, double *rmse_out, void *stream);
+
 /* factorization.py:235-263 _predict_one for n (i, j) pairs -> out (n) f64. */
 int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows,
                   const int32_t *cols, int64_t n, double *out, void *stream);

@@ -301,13 +301,23 @@ __device__ __forceinline__ void stage_rows(T *tile, const T *myrow, int ne, int 
     }
 }
 
+// The ratings to predict, grouped by row: row i's targets are [ptr[i], ptr[i+1]) with
+// their columns, values and entry index (the position of their squared error; NULL:
+// identity).  The training set is the ratings' own CSR.
+struct RowTargets {
+    const int64_t *ptr;
+    const int32_t *cols;
+    const double *vals;
+    const int32_t *index;
+};
+
 template <typename P>
 __global__ void __launch_bounds__(kRowWarpsRmse * 32, 3)
     pred_row_kernel(CulshData d, double mu, const P *__restrict__ b, const P *__restrict__ bhat,
                     const P *__restrict__ U, const P *__restrict__ V, const P *__restrict__ W,
                     const P *__restrict__ C, const int32_t *__restrict__ nbr, int F, int ldF, int K,
-                    int words, int vec, const int32_t *__restrict__ csr_entry, int do_clamp, double lo,
-                    double hi, double unscale, double *__restrict__ out) {
+                    int words, int vec, RowTargets tg, int do_clamp, double lo, double hi, double unscale,
+                    double *__restrict__ out) {
     using V2 = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
     constexpr int GE = 16 / (int)sizeof(P);
     extern __shared__ __align__(16) unsigned char s_raw[];
@@ -327,8 +337,9 @@ __global__ void __launch_bounds__(kRowWarpsRmse * 32, 3)
     __syncwarp();
     const int64_t nw = (int64_t)gridDim.x * kRowWarpsRmse;
     for (int64_t i = (int64_t)blockIdx.x * kRowWarpsRmse + wid; i < d.M; i += nw) {
+        const int64_t tlo = tg.ptr[i], thi = tg.ptr[i + 1];
+        if (tlo == thi) continue;
         const int64_t rlo = d.row_ptr[i], rhi = d.row_ptr[i + 1];
-        if (rlo == rhi) continue;
         if (K > 0) {
             for (int64_t p = rlo + lane; p < rhi; p += 32) {
                 const int32_t c = d.row_cols[p];
@@ -353,11 +364,11 @@ __global__ void __launch_bounds__(kRowWarpsRmse * 32, 3)
         const double mbb = __dadd_rn(mu, d.base_b[i]);
         for (int f = lane; f < Fs; f += 32) us[f] = f < F ? U[i * ldF + f] : P(0);
         __syncwarp();
-        for (int64_t c0 = rlo; c0 < rhi; c0 += 32) {
-            const int ne = (int)min64(32, rhi - c0);
+        for (int64_t c0 = tlo; c0 < thi; c0 += 32) {
+            const int ne = (int)min64(32, thi - c0);
             const bool valid = lane < ne;
             const int64_t p = c0 + lane;
-            const int32_t j = valid ? d.row_cols[p] : 0;
+            const int32_t j = valid ? tg.cols[p] : 0;
             double pred = valid ? __dadd_rn(mb, (double)bhat[j]) : 0.0;
             double dot = 0.0;
             for (int f0 = 0; f0 < F; f0 += 32) {
@@ -432,8 +443,8 @@ __global__ void __launch_bounds__(kRowWarpsRmse * 32, 3)
                     if (pred < lo) pred = lo;
                     else if (pred > hi) pred = hi;
                 }
-                const double dd = __dmul_rn(__dsub_rn(pred, d.row_vals[p]), unscale);
-                out[csr_entry ? (int64_t)csr_entry[p] : p] = __dmul_rn(dd, dd);
+                const double dd = __dmul_rn(__dsub_rn(pred, tg.vals[p]), unscale);
+                out[tg.index ? (int64_t)tg.index[p] : p] = __dmul_rn(dd, dd);
             }
         }
         if (K > 0) {
@@ -448,7 +459,7 @@ static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 template <typename P>
 int launch_pred_rows(const CulshData *d, double mu, const P *b, const P *bhat, const P *U, const P *V, const P *W,
-                     const P *C, const int32_t *nbr, int F, int ldF, int K, const int32_t *csr_entry, int do_clamp,
+                     const P *C, const int32_t *nbr, int F, int ldF, int K, RowTargets tg, int do_clamp,
                      double lo, double hi, double unscale, double *sq, cudaStream_t st) {
     CULSH_REQUIRE(d->N <= 65536, "the CSR-order rmse needs N <= 65536 (per-warp row bitmap)");
     CULSH_REQUIRE(K >= 0 && K <= 64, "K must be in [0, 64]");
@@ -464,7 +475,7 @@ int launch_pred_rows(const CulshData *d, double mu, const P *b, const P *bhat, c
     CULSH_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pred_row_kernel<P>, kRowWarpsRmse * 32, smem));
     const int64_t blocks = min64((d->M + kRowWarpsRmse - 1) / kRowWarpsRmse, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     pred_row_kernel<P><<<(unsigned)blocks, kRowWarpsRmse * 32, smem, st>>>(
-        *d, mu, b, bhat, U, V, W, C, nbr, F, ldF, K, words, vec, csr_entry, do_clamp, lo, hi, unscale, sq);
+        *d, mu, b, bhat, U, V, W, C, nbr, F, ldF, K, words, vec, tg, do_clamp, lo, hi, unscale, sq);
     CULSH_LAUNCH_CHECK();
     return CULSH_OK;
 }
@@ -654,20 +665,27 @@ extern "C" int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, d
     return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
 }
 
-// factorization.py:559-579 rmse over the training set in CSR order (pred_row_kernel;
-// N <= 65,536, no lookup cache).  csr_entry: entry index of each CSR position (NULL:
-// identity); the sum runs in entry order like culsh_rmse_train.
+// factorization.py:559-579 rmse in row order (pred_row_kernel; N <= 65,536, no lookup
+// cache).  Targets: the training set itself (culsh_rmse_train_rows: the ratings' CSR,
+// csr_entry = entry index of each CSR position, NULL: identity) or any test set grouped by
+// row (culsh_rmse_rows: t_ptr (M+1), t_cols, t_vals, t_index = each target's position in
+// the test set).  The sum runs in entry order like culsh_rmse / culsh_rmse_train.
+static int rows_finish(int rc, const double *sq, int64_t n, double *out, double *scratch, cudaStream_t st) {
+    if (rc != CULSH_OK) return rc;
+    return reduce_rmse(sq, n, out, scratch, n <= (1LL << 22), st);
+}
+
 extern "C" int culsh_rmse_train_rows(const CulshData *d, const CulshModel64 *m, const int32_t *csr_entry,
                                      int do_clamp, double clamp_lo, double clamp_hi, double unscale,
                                      double *sqerr_scratch, double *rmse_out, void *stream) {
     const int64_t n = d->nnz;
     CULSH_REQUIRE(n > 0, "empty training set");
     cudaStream_t st = (cudaStream_t)stream;
-    const int rc = launch_pred_rows<double>(d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->nbr, m->F, m->F,
-                                            m->K, csr_entry, do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch,
-                                            st);
-    if (rc != CULSH_OK) return rc;
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+    const RowTargets tg{d->row_ptr, d->row_cols, d->row_vals, csr_entry};
+    return rows_finish(launch_pred_rows<double>(d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->nbr, m->F,
+                                                m->F, m->K, tg, do_clamp, clamp_lo, clamp_hi, unscale,
+                                                sqerr_scratch, st),
+                       sqerr_scratch, n, rmse_out, sqerr_scratch + n, st);
 }
 
 extern "C" int culsh_rmse_train_rows_m32(const CulshData *d, const CulshModel32 *m, double mu, int F,
@@ -678,8 +696,35 @@ extern "C" int culsh_rmse_train_rows_m32(const CulshData *d, const CulshModel32 
     CULSH_REQUIRE(n > 0, "empty training set");
     CULSH_REQUIRE(F >= 1 && F <= m->F, "logical F exceeds the model's row stride");
     cudaStream_t st = (cudaStream_t)stream;
-    const int rc = launch_pred_rows<float>(d, mu, m->b, m->bhat, m->U, m->V, m->W, m->C, nbr, F, m->F, m->K,
-                                           csr_entry, do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch, st);
-    if (rc != CULSH_OK) return rc;
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+    const RowTargets tg{d->row_ptr, d->row_cols, d->row_vals, csr_entry};
+    return rows_finish(launch_pred_rows<float>(d, mu, m->b, m->bhat, m->U, m->V, m->W, m->C, nbr, F, m->F, m->K,
+                                               tg, do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch, st),
+                       sqerr_scratch, n, rmse_out, sqerr_scratch + n, st);
+}
+
+extern "C" int culsh_rmse_rows(const CulshData *d, const CulshModel64 *m, const int64_t *t_ptr,
+                               const int32_t *t_cols, const double *t_vals, const int32_t *t_index, int64_t n,
+                               int do_clamp, double clamp_lo, double clamp_hi, double unscale,
+                               double *sqerr_scratch, double *rmse_out, void *stream) {
+    CULSH_REQUIRE(n > 0, "empty test set");
+    cudaStream_t st = (cudaStream_t)stream;
+    const RowTargets tg{t_ptr, t_cols, t_vals, t_index};
+    return rows_finish(launch_pred_rows<double>(d, m->mu, m->b, m->bhat, m->U, m->V, m->W, m->C, m->nbr, m->F,
+                                                m->F, m->K, tg, do_clamp, clamp_lo, clamp_hi, unscale,
+                                                sqerr_scratch, st),
+                       sqerr_scratch, n, rmse_out, sqerr_scratch + n, st);
+}
+
+extern "C" int culsh_rmse_rows_m32(const CulshData *d, const CulshModel32 *m, double mu, int F, const int32_t *nbr,
+                                   const int64_t *t_ptr, const int32_t *t_cols, const double *t_vals,
+                                   const int32_t *t_index, int64_t n, int do_clamp, double clamp_lo,
+                                   double clamp_hi, double unscale, double *sqerr_scratch, double *rmse_out,
+                                   void *stream) {
+    CULSH_REQUIRE(n > 0, "empty test set");
+    CULSH_REQUIRE(F >= 1 && F <= m->F, "logical F exceeds the model's row stride");
+    cudaStream_t st = (cudaStream_t)stream;
+    const RowTargets tg{t_ptr, t_cols, t_vals, t_index};
+    return rows_finish(launch_pred_rows<float>(d, mu, m->b, m->bhat, m->U, m->V, m->W, m->C, nbr, F, m->F, m->K,
+                                               tg, do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch, st),
+                       sqerr_scratch, n, rmse_out, sqerr_scratch + n, st);
 }

@@ -708,6 +708,30 @@ def _test_device(testset: Triplets, ratings: SparseRatings):
     return dev
 
 
+def _test_rows(testset: Triplets, ratings: SparseRatings):
+    """The test set grouped by row on the device: (ptr (M+1) int64, cols int32, values f64,
+    position in the test set int32).  A stable sort keeps each row's targets in test-set
+    order; cached next to the device copy when the test set is immutable."""
+    cache = getattr(testset, "_dev_rows", None)
+    if cache is not None and cache[0] is ratings:
+        return cache[1]
+    t = nat.torch()
+    tr, tc, tv = _test_device(testset, ratings)
+    n = len(testset)
+    M, N = ratings.M, ratings.N
+    rmin, rmax = t.aminmax(tr[:n])
+    cmin, cmax = t.aminmax(tc[:n])
+    if int(rmin) < 0 or int(rmax) >= M or int(cmin) < 0 or int(cmax) >= N:
+        raise IndexError(f"test triplet outside the ratings' {M} x {N} index space")
+    order = t.sort(tr[:n], stable=True)[1]
+    ptr = t.zeros(M + 1, dtype=t.int64, device=tr.device)
+    t.cumsum(t.bincount(tr[:n].to(t.int64), minlength=M), 0, out=ptr[1:])
+    rows = (ptr, tc[:n][order].contiguous(), tv[:n][order].contiguous(), order.to(t.int32))
+    if getattr(testset, "_dev", None) is not None:
+        testset._dev_rows = (ratings, rows)
+    return rows
+
+
 def _train_lookup(dev, nbr, K: int):
     """Per-(ratings, J^K) lookup cache for rmse over the training set: the explicit-
     neighbour mask of every CSC entry and the CSC position of each explicit pair (built
@@ -739,7 +763,8 @@ def _train_lookup(dev, nbr, K: int):
     return mask, base, pos
 
 
-_ROWS_RMSE_MAX_N = 65536   # per-warp row bitmap of the CSR-order training-set kernel
+_ROWS_RMSE_MAX_N = 65536   # per-warp row bitmap of the row-order rmse kernel
+_ROWS_RMSE_MIN_TEST = 4096  # smaller test sets: the ungrouped kernel (no sort)
 
 
 def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
@@ -782,6 +807,19 @@ def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
         nat.call("culsh_rmse_train_m32" if m32 else "culsh_rmse_train", *head, nat.ptr(mask),
                  nat.ptr(base), nat.ptr(pos), nat.ptr(perm), int(clamp is not None), float(lo), float(hi),
                  us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
+        return float(out.item())
+    if dev.N <= _ROWS_RMSE_MAX_N and n >= _ROWS_RMSE_MIN_TEST:
+        # grouped by row: one warp per row against the row's bitmap (the ungrouped kernel
+        # binary-searches every neighbour and gathers U and V per target)
+        tp, tcol, tval, tix = _test_rows(testset, ratings)
+        if m32:
+            nat.call("culsh_rmse_rows_m32", *head, nat.ptr(tp), nat.ptr(tcol), nat.ptr(tval), nat.ptr(tix), n,
+                     int(clamp is not None), float(lo), float(hi), us, nat.ptr(scratch), nat.ptr(out),
+                     nat.stream_ptr())
+        else:
+            nat.call("culsh_rmse_rows", *head, nat.ptr(tp), nat.ptr(tcol), nat.ptr(tval), nat.ptr(tix), n,
+                     int(clamp is not None), float(lo), float(hi), us, nat.ptr(scratch), nat.ptr(out),
+                     nat.stream_ptr())
         return float(out.item())
     tr, tc, tv = _test_device(testset, ratings)
     nat.call("culsh_rmse_m32" if m32 else "culsh_rmse", *head, nat.ptr(tr),

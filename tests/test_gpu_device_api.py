@@ -225,10 +225,11 @@ def test_train_set_rmse_path_equals_generic(P, orc, K):
                                           (40, 33, "exact", "csc"), (64, 64, "exact", "random"),
                                           (16, 64, "hogwild", "random"), (33, 32, "hogwild", "csr")])
 def test_train_set_rmse_row_kernel_equals_lookup_kernel(P, orc, monkeypatch, K, F, mode, order):
-    """The CSR-order training-set kernel (one warp per row, row bitmap) returns the same
-    float as the CSC-order lookup-cache kernel and the oracle: empty rows and columns, rows
-    longer than 32, K spanning two 32-wide halves, entry orders CSR / CSC / random, fp64 and
-    fp32 (Hogwild) models, clamp + unscale."""
+    """The row-order kernel (one warp per row, row bitmap) returns the same float as the
+    CSC-order lookup-cache kernel (training set) / the ungrouped kernel (a test set) and the
+    oracle: empty rows and columns, rows longer than 32, K spanning two 32-wide halves, entry
+    orders CSR / CSC / random, duplicate and unrated test pairs, fp64 and fp32 (Hogwild)
+    models, clamp + unscale."""
     from paper_2111_11682_b200 import factorization as fz
     rng = np.random.default_rng(5)
     M, N = 300, 120
@@ -249,14 +250,21 @@ def test_train_set_rmse_row_kernel_equals_lookup_kernel(P, orc, monkeypatch, K, 
     tbl = P.simlsh_topk(r, P.LshConfig(G=4, p=2, q=6, seed=1), K)[0] if K else None
     p = P.train_full(r, tbl, P.TrainConfig(F=F, K=K, epochs=2, seed=2), mode=mode)
     kw = dict(clamp=(1.0, 5.0), unscale=2.0)
+    # a held-out-style test set: random rows / cols (rated or not, duplicates, unsorted)
+    nt = 6000
+    te = P.Triplets(rng.integers(0, M, nt).astype(np.int32), rng.integers(0, N, nt).astype(np.int32),
+                    rng.integers(1, 6, nt).astype(np.float64))
     a = P.rmse(p, r.triplets(), r, **kw)
+    at = P.rmse(p, te, r, **kw)
     monkeypatch.setattr(fz, "_ROWS_RMSE_MAX_N", 0)
     b = P.rmse(p, r.triplets(), r, **kw)
-    assert a == b
+    bt = P.rmse(p, te, r, **kw)
+    assert a == b and at == bt
     if mode == "exact":
         d, _ = orc.build_csr(r.M, r.N, rows, cols, vals)
         m = orc.Model(p.mu, p.b, p.b_hat, p.U, p.V, p.W, p.C, tbl.entries if K else np.zeros((N, 0), np.int32))
         assert a == orc.rmse(d, m, r.entry_rows, r.entry_cols, r.entry_values, **kw)
+        assert at == orc.rmse(d, m, te.rows, te.cols, te.values, **kw)
 
 
 def test_train_set_rmse_large_tree_sum(P):
