@@ -488,8 +488,11 @@ def split_neighbors(i: int, j: int, neighbors: NeighborTable,
 def _predict_pairs(params: ModelParams, ratings: SparseRatings, rows, cols) -> np.ndarray:
     dev = ratings.device()
     dm = params._device(64)
-    rows = nat.to_dev(np.asarray(rows, np.int32).reshape(-1))
-    cols = nat.to_dev(np.asarray(cols, np.int32).reshape(-1))
+    rows = np.asarray(rows, np.int32).reshape(-1)
+    cols = np.asarray(cols, np.int32).reshape(-1)
+    if len(rows) and (rows.min() < 0 or rows.max() >= ratings.M or cols.min() < 0 or cols.max() >= ratings.N):
+        raise IndexError(f"pair outside the ratings' {ratings.M} x {ratings.N} index space")
+    rows, cols = nat.to_dev(rows), nat.to_dev(cols)
     n = rows.numel()
     out = nat.empty((max(n, 1),), "float64")
     nat.call("culsh_predict", ctypes.byref(dev.struct), ctypes.byref(dm.struct), nat.ptr(rows),
@@ -698,13 +701,27 @@ def _test_device(testset: Triplets, ratings: SparseRatings):
     src = getattr(testset, "_source", None)
     if src is not None and src is ratings:
         return ratings.device_entries()
-    cache = getattr(testset, "_dev", None)
-    if cache is not None:
-        return cache
-    dev = (nat.to_dev(np.asarray(testset.rows, np.int32)), nat.to_dev(np.asarray(testset.cols, np.int32)),
-           nat.to_dev(np.asarray(testset.values, np.float64)))
-    if all(not np.asarray(a).flags.writeable for a in (testset.rows, testset.cols, testset.values)):
-        testset._dev = dev
+    dev = getattr(testset, "_dev", None)
+    cached = dev is not None
+    if not cached:
+        dev = (nat.to_dev(np.asarray(testset.rows, np.int32)), nat.to_dev(np.asarray(testset.cols, np.int32)),
+               nat.to_dev(np.asarray(testset.values, np.float64)))
+        if all(not np.asarray(a).flags.writeable for a in (testset.rows, testset.cols, testset.values)):
+            testset._dev = dev
+            cached = True
+    # the kernels index b / U / V / the CSR with these: out-of-range pairs raise here
+    # (the reference's numba loop would read out of bounds); once per immutable test set
+    key = (ratings.M, ratings.N)
+    n = len(testset)
+    if n and getattr(testset, "_dev_checked", None) != key:
+        t = nat.torch()
+        lo_r, hi_r = t.aminmax(dev[0][:n])
+        lo_c, hi_c = t.aminmax(dev[1][:n])
+        r0, r1, c0, c1 = t.stack([lo_r, hi_r, lo_c, hi_c]).tolist()
+        if r0 < 0 or r1 >= ratings.M or c0 < 0 or c1 >= ratings.N:
+            raise IndexError(f"test triplet outside the ratings' {ratings.M} x {ratings.N} index space")
+        if cached:
+            testset._dev_checked = key
     return dev
 
 
@@ -718,11 +735,7 @@ def _test_rows(testset: Triplets, ratings: SparseRatings):
     t = nat.torch()
     tr, tc, tv = _test_device(testset, ratings)
     n = len(testset)
-    M, N = ratings.M, ratings.N
-    rmin, rmax = t.aminmax(tr[:n])
-    cmin, cmax = t.aminmax(tc[:n])
-    if int(rmin) < 0 or int(rmax) >= M or int(cmin) < 0 or int(cmax) >= N:
-        raise IndexError(f"test triplet outside the ratings' {M} x {N} index space")
+    M = ratings.M
     order = t.sort(tr[:n], stable=True)[1]
     ptr = t.zeros(M + 1, dtype=t.int64, device=tr.device)
     t.cumsum(t.bincount(tr[:n].to(t.int64), minlength=M), 0, out=ptr[1:])

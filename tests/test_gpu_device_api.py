@@ -267,6 +267,26 @@ def test_train_set_rmse_row_kernel_equals_lookup_kernel(P, orc, monkeypatch, K, 
         assert at == orc.rmse(d, m, te.rows, te.cols, te.values, **kw)
 
 
+@pytest.mark.parametrize("n", [10, 5000])
+def test_rmse_rejects_out_of_range_test_pairs(P, n):
+    """Both test-set routes (ungrouped below 4,096 targets, row-grouped above) raise
+    IndexError for a pair outside the ratings' index space instead of reading out of bounds."""
+    r, rows, cols, vals = _case(P, seed=4, M=200, N=50, dens=0.2)
+    p = P.train_full(r, None, P.TrainConfig(F=8, K=0, epochs=1, seed=0))
+    rng = np.random.default_rng(0)
+    tr = rng.integers(0, r.M, n).astype(np.int32)
+    tc = rng.integers(0, r.N, n).astype(np.int32)
+    tv = np.ones(n)
+    assert np.isfinite(P.rmse(p, P.Triplets(tr, tc, tv), r))
+    bad_r, bad_c = tr.copy(), tc.copy()
+    bad_r[n // 2] = r.M
+    bad_c[n // 3] = -1
+    with pytest.raises(IndexError):
+        P.rmse(p, P.Triplets(bad_r, tc, tv), r)
+    with pytest.raises(IndexError):
+        P.rmse(p, P.Triplets(tr, bad_c, tv), r)
+
+
 def test_train_set_rmse_large_tree_sum(P):
     """Above 2^22 ratings both paths use the same fixed tree over entry order."""
     rng = np.random.default_rng(3)
