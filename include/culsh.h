@@ -181,7 +181,7 @@ int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, const CulshRate
                             int *row_last, int *ticket, int *status, void *stream);
 
 /* Neighbour lookups (factorization.py:218-232) of every CSC entry of columns
- * [col_lo, col_hi), ahead of a column pass: mask (entries x (K<=32 ? 1 : 2) u32, bit k
+ * [col_lo, col_hi), ahead of a column pass: mask (entries x (K<=32 ? 1 : K<=64 ? 2 : 4) u32, bit k
  * set iff row i rated J[j,k]) and rv (entries x K f64, the ratings found), entry
  * index relative to col_ptr[col_lo]. */
 int culsh_exact_lookup(const CulshData *d, const CulshModel64 *m, int64_t col_lo, int64_t col_hi,

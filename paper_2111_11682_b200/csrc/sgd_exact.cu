@@ -437,18 +437,26 @@ int launch_row(const ExactModel &P, const CulshRates &R, int64_t row_lo, int64_t
     return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
 }
 
+// explicit-neighbour mask words per rating: 1 (K <= 32), 2 (K <= 64), 4 (K <= 128, the
+// top-K kernels' bound; the reference's K is unbounded)
+__host__ __device__ constexpr int exact_kpl(int K) { return K <= 32 ? 1 : K <= 64 ? 2 : 4; }
+
 #define CULSH_DISPATCH_FK(F, K, CALL)                                  \
     do {                                                               \
         const int _fpl = (F) <= 32 ? 1 : (F) <= 64 ? 2 : (F) <= 128 ? 4 : 8; \
-        const int _kpl = (K) <= 32 ? 1 : 2;                            \
+        const int _kpl = exact_kpl(K);                                 \
         if (_fpl == 1 && _kpl == 1) return CALL(1, 1);                 \
         if (_fpl == 1 && _kpl == 2) return CALL(1, 2);                 \
+        if (_fpl == 1 && _kpl == 4) return CALL(1, 4);                 \
         if (_fpl == 2 && _kpl == 1) return CALL(2, 1);                 \
         if (_fpl == 2 && _kpl == 2) return CALL(2, 2);                 \
+        if (_fpl == 2 && _kpl == 4) return CALL(2, 4);                 \
         if (_fpl == 4 && _kpl == 1) return CALL(4, 1);                 \
         if (_fpl == 4 && _kpl == 2) return CALL(4, 2);                 \
+        if (_fpl == 4 && _kpl == 4) return CALL(4, 4);                 \
         if (_fpl == 8 && _kpl == 1) return CALL(8, 1);                 \
-        return CALL(8, 2);                                             \
+        if (_fpl == 8 && _kpl == 2) return CALL(8, 2);                 \
+        return CALL(8, 4);                                             \
     } while (0)
 
 }  // namespace culsh
@@ -508,7 +516,7 @@ static int exact_colpass_impl(const CulshData *d, CulshModel64 *m, const CulshRa
                               int64_t M_old, int variant, int *row_last, int *ticket, int *status, void *stream,
                               ExactPre pre) {
     CULSH_REQUIRE(m->F >= 1 && m->F <= 256, "F must be in [1, 256]");
-    CULSH_REQUIRE(m->K >= 0 && m->K <= 64, "K must be in [0, 64]");
+    CULSH_REQUIRE(m->K >= 0 && m->K <= 128, "K must be in [0, 128]");
     if (col_hi <= col_lo) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     CULSH_CHECK(cudaMemsetAsync(row_last, 0xFF, sizeof(int) * d->M, st));
@@ -530,10 +538,10 @@ extern "C" int culsh_sgd_exact_colpass(const CulshData *d, CulshModel64 *m, cons
 
 extern "C" int culsh_exact_lookup(const CulshData *d, const CulshModel64 *m, int64_t col_lo, int64_t col_hi,
                                   uint32_t *mask, double *rv, void *stream) {
-    CULSH_REQUIRE(m->K >= 1 && m->K <= 64, "K must be in [1, 64]");
+    CULSH_REQUIRE(m->K >= 1 && m->K <= 128, "K must be in [1, 128]");
     if (col_hi <= col_lo) return CULSH_OK;
     const ExactModel P = make_model(d, m);
-    const int KPL = m->K <= 32 ? 1 : 2;
+    const int KPL = exact_kpl(m->K);
     exact_lookup_kernel<<<(unsigned)(num_sms() * 16), 256, 0, (cudaStream_t)stream>>>(P, col_lo, col_hi, KPL,
                                                                                      mask, rv);
     CULSH_LAUNCH_CHECK();
@@ -554,7 +562,7 @@ extern "C" int culsh_sgd_exact_rowpass(const CulshData *d, CulshModel64 *m, cons
                                        int64_t row_lo, int64_t row_hi, int64_t N_old, int *status,
                                        void *stream) {
     CULSH_REQUIRE(m->F >= 1 && m->F <= 256, "F must be in [1, 256]");
-    CULSH_REQUIRE(m->K >= 0 && m->K <= 64, "K must be in [0, 64]");
+    CULSH_REQUIRE(m->K >= 0 && m->K <= 128, "K must be in [0, 128]");
     if (row_hi <= row_lo) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const ExactModel P = make_model(d, m);

@@ -446,7 +446,7 @@ def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fractio
     base = int(cp[col_lo].item())
     n = int(cp[col_hi].item()) - base
     t = nat.torch()
-    kpl = 1 if K <= 32 else 2
+    kpl = _mask_words(K)
     if n * (8 * K + 4 * kpl) > mem_fraction * t.cuda.mem_get_info()[0]:   # rv f64 + mask words
         return None
     mask = nat.empty((max(n * kpl, 1),), "int32")
@@ -456,13 +456,24 @@ def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fractio
     return mask, rv, base
 
 
+# the largest K of the exact (reference-order) kernels, the online path and rmse / predict:
+# four 32-bit explicit-neighbour mask words per rating, the top-K kernels' bound (topk.cu).
+# The fp32 Hogwild mode keeps two (K <= 64, hogwild.hogwild_supported).
+MAX_K = 128
+
+
+def _mask_words(K: int) -> int:
+    """Mask words per rating of the exact kernels (sgd_exact.cu exact_kpl)."""
+    return 1 if K <= 32 else 2 if K <= 64 else 4
+
+
 def _check_model_dims(F: int, K: int) -> None:
     # the reference accepts any F and K (factorization.py:75-82); the kernels keep up to
-    # 256 factors per row and two 32-bit explicit-neighbour mask words per rating
+    # 256 factors per row and MAX_K neighbours per column
     if not (1 <= F <= 256):
         raise ValueError(f"F={F} outside the supported range [1, 256] (the reference has no bound)")
-    if not (0 <= K <= 64):
-        raise ValueError(f"K={K} outside the supported range [0, 64] (the reference has no bound)")
+    if not (0 <= K <= MAX_K):
+        raise ValueError(f"K={K} outside the supported range [0, {MAX_K}] (the reference has no bound)")
 
 
 # ------------------------------------------------------------- public ops ---
@@ -801,7 +812,8 @@ def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
     us = 1.0 if unscale is None else float(unscale)
     head = ((ctypes.byref(dev.struct), ctypes.byref(dm.struct), float(dm.mu), int(dm.F), nat.ptr(dm.nbr))
             if m32 else (ctypes.byref(dev.struct), ctypes.byref(dm.struct)))
-    if getattr(testset, "_source", None) is ratings and n == dev.nnz and dev.N <= _ROWS_RMSE_MAX_N:
+    wide_k = dm.K > 64   # beyond the two mask words of the row / lookup-cache kernels
+    if getattr(testset, "_source", None) is ratings and n == dev.nnz and dev.N <= _ROWS_RMSE_MAX_N and not wide_k:
         # CSR order, one warp per row (U read once per row; no lookup cache)
         ce = ratings.csr_entry_index()
         if m32:
@@ -811,7 +823,7 @@ def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
             nat.call("culsh_rmse_train_rows", *head, nat.ptr(ce), int(clamp is not None), float(lo), float(hi),
                      us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
         return float(out.item())
-    if getattr(testset, "_source", None) is ratings and n == dev.nnz:
+    if getattr(testset, "_source", None) is ratings and n == dev.nnz and not wide_k:
         K = dm.K
         mask = base = pos = None
         if K:
@@ -821,7 +833,7 @@ def rmse(params: ModelParams, testset: Triplets, ratings: SparseRatings,
                  nat.ptr(base), nat.ptr(pos), nat.ptr(perm), int(clamp is not None), float(lo), float(hi),
                  us, nat.ptr(scratch), nat.ptr(out), nat.stream_ptr())
         return float(out.item())
-    if dev.N <= _ROWS_RMSE_MAX_N and n >= _ROWS_RMSE_MIN_TEST:
+    if dev.N <= _ROWS_RMSE_MAX_N and n >= _ROWS_RMSE_MIN_TEST and not wide_k:
         # grouped by row: one warp per row against the row's bitmap (the ungrouped kernel
         # binary-searches every neighbour and gathers U and V per target)
         tp, tcol, tval, tix = _test_rows(testset, ratings)

@@ -203,3 +203,19 @@ def test_pairwise_plan_combines_to_numpy():
         assert sum(lens) == n and max(lens) <= 65536
         sums = [float(np.add.reduce(x[o:o + m])) for o, m in zip(offs, lens)]
         assert _pairwise_combine(n, sums) == float(np.add.reduce(x))
+
+
+def test_model_dims_bounds():
+    """Exact kernels take K <= 128 (four mask words, the top-K kernels' bound); the fp32
+    Hogwild mode K <= 64; the reference has no bound (factorization.py:75-82)."""
+    import pytest
+    from paper_2111_11682_b200.factorization import MAX_K, _check_model_dims, _mask_words
+    from paper_2111_11682_b200.hogwild import hogwild_supported
+    assert MAX_K == 128
+    _check_model_dims(256, 128)
+    with pytest.raises(ValueError, match="K=129"):
+        _check_model_dims(8, 129)
+    with pytest.raises(ValueError, match="F=257"):
+        _check_model_dims(257, 8)
+    assert [_mask_words(k) for k in (0, 32, 33, 64, 65, 128)] == [1, 1, 2, 2, 4, 4]
+    assert hogwild_supported(128, 64) and not hogwild_supported(128, 65)
