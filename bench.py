@@ -200,9 +200,12 @@ def ncu_measured(config, kernel):
     m["same_build"] = bool(m.get("build_sha256")) and m["build_sha256"] == build_sha256()
     pk, _ = peak_hbm_gbs()
     m["dram_frac_of_peak"] = m["dram_gbs"] / pk
-    m["limiter"] = max((("l1tex", m["l1tex_throughput_pct"]), ("l2", m["l2_throughput_pct"]),
-                        ("sm_issue", m["sm_throughput_pct"]), ("dram", 100.0 * m["dram_frac_of_peak"])),
-                       key=lambda x: x[1])[0]
+    units = [("l1tex", m["l1tex_throughput_pct"]), ("l2", m["l2_throughput_pct"]),
+             ("sm_issue", m.get("issue_active_pct") or m["sm_throughput_pct"]),
+             ("dram", 100.0 * m["dram_frac_of_peak"])]
+    if m.get("l1_to_l2_req_pct") is not None:   # the L1 -> L2 request interface (RED data)
+        units.append(("l1_to_l2_requests", m["l1_to_l2_req_pct"]))
+    m["limiter"] = max(units, key=lambda x: x[1])[0]
     m["profiled_kernel_matches"] = kernel.split("<")[0] in m.get("kernel", "")
     m["file"] = os.path.relpath(path, ROOT)
     return m

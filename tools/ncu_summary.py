@@ -43,6 +43,10 @@ KEYS = [
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
     "smsp__average_warp_latency_per_inst_issued.ratio",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__m_l1tex2xbar_write_bytes.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -89,6 +93,11 @@ def _build_sha256() -> str:
     return bench.build_sha256()
 
 
+def _opt(d, key):
+    """A metric that older captures may lack (None then)."""
+    return _num(d, key) if key in d else None
+
+
 def full(rep: str, dst: str, traffic_json: str | None = None, lib: str | None = None) -> None:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
@@ -128,6 +137,11 @@ def full(rep: str, dst: str, traffic_json: str | None = None, lib: str | None = 
                        "issue_ipc": (_num(d, "smsp__inst_executed.avg.per_cycle_active")
                                      if "smsp__inst_executed.avg.per_cycle_active" in d else None),
                        "warps_active_pct": _num(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                       "issue_active_pct": _opt(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                       # L1 -> L2 request interface (RED data + read requests) and its write bytes
+                       "l1_to_l2_req_pct": _opt(d, "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                       "l1_to_l2_write_bytes_pct": _opt(d, "l1tex__m_l1tex2xbar_write_bytes.sum.pct_of_peak_sustained_elapsed"),
+                       "shared_wavefronts_pct": _opt(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
                        "registers": _num(d, "launch__registers_per_thread"),
                        "build_sha256": _build_sha256() if lib else None}
                 json.dump(rec, open(traffic_json, "w"), indent=1)
