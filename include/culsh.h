@@ -365,6 +365,13 @@ int culsh_rmse_rows_m32(const CulshData *d, const CulshModel32 *m, double mu, in
                         const int32_t *t_index, int64_t n, int do_clamp, double clamp_lo, double clamp_hi,
                         double unscale, double *sqerr_scratch, double *rmse_out, void *stream);
 
+/* The reference's serial fp64 sum (factorization.py:394-409 `total += d * d`) of n >= 1
+ * terms: out = fl(...fl(fl(0 + x[0]) + x[1]) ... + x[n-1]), bit for bit, in parallel for
+ * non-negative terms (a run of additions inside one binade is an integer sum on that
+ * binade's ulp grid plus a ties-to-even parity bit; chunks that change binade or hold any
+ * other term are added one by one).  Every culsh_rmse* entry point sums this way. */
+int culsh_sequential_sum(const double *x, int64_t n, double *out, void *stream);
+
 /* factorization.py:235-263 _predict_one for n (i, j) pairs -> out (n) f64. */
 int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows,
                   const int32_t *cols, int64_t n, double *out, void *stream);

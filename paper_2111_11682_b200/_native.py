@@ -132,6 +132,7 @@ _SIGS = {
     "culsh_rmse_rows_m32": [_P(CulshData), _P(CulshModel32), _f64, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32,
                             _f64, _f64, _f64, _vp, _vp, _vp],
     "culsh_rmse32": [_P(CulshData), _P(CulshModel32), _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "culsh_sequential_sum": [_vp, _i64, _vp, _vp],
     "culsh_predict": [_P(CulshData), _P(CulshModel64), _vp, _vp, _i64, _vp, _vp],
     "culsh_csc_to_csr_map": [_P(CulshData), _vp, _vp],
     "culsh_append_segments": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -1,8 +1,8 @@
 // Evaluation: exact fp64 prediction and RMSE.
 // pred_tile_kernel restates factorization.py:235-263 _predict_one in its exact operation
 // order (explicit _rn intrinsics; the TU is also compiled with -fmad=false); the RMSE sum
-// is sequential (bit-identical to factorization.py:394-409) when `sequential` is set,
-// otherwise a fixed pairwise tree (deterministic, within a few ulp of the sequential sum).
+// is the reference's sequential one (bit-identical to factorization.py:394-409, at any n:
+// seq_sum_exact) when `sequential` is set, otherwise a fixed pairwise tree.
 #include <type_traits>
 
 #include "common.cuh"
@@ -537,10 +537,282 @@ __global__ void lookup_fill_kernel(CulshData d, const int32_t *__restrict__ nbr,
     }
 }
 
+// ---- the reference's sequential sum of non-negative terms, in parallel -----------------
+// S_{k+1} = fl(S_k + x_k), x_k >= 0 (squared errors).  While S stays inside one binade
+// [2^e, 2^(e+1)) every S is a multiple of u = ulp(S) = 2^(e-52) (2^-1074 for the subnormal
+// range and the first normal binade, which share that grid), and fl(S + x) is S + d*u with
+// d = round(x / u) to nearest -- x / u is exact (power-of-two scaling) -- except that an
+// exact tie (x / u = k + 1/2) rounds to the even sum, which depends on the parity of S / u.
+// So a run of additions inside one binade is an integer sum plus a 1-bit parity state, and
+// its effect is the function b -> (D_b, b'_b) of the starting parity b -- associative under
+// composition.  The sum then runs as: (1) approximate chunk sums, (2) their exclusive
+// prefix (the approximate S at each chunk start, hence its binade), (3) every chunk's
+// function on that binade's grid, in parallel, (4) one CTA walks the chunks with the exact S:
+// a chunk whose grid matches S's and whose integer sum stays below 2^53 (no binade change
+// inside) is applied in O(1); any other chunk (S == 0, a binade change, a huge, negative or
+// non-finite term) is added term by term, exactly like the sequential loop.  The result is
+// the sequential loop's bits (tests/test_gpu_device_api.py::test_exact_sequential_sum).
+constexpr int kSeqChunk = 8192;
+constexpr int kSeqItems = kSeqChunk / 1024;
+
+struct SeqFn {
+    uint64_t d0, d1;   // integer increments (units of u) for starting parity 0 / 1
+    int o0, o1;        // resulting parity
+    int uexp;          // log2(u) of the grid the function was built on
+    int ok;            // no huge / negative / non-finite term, grid known
+};
+
+__device__ __forceinline__ int grid_exp(double S) {   // log2(ulp) of S > 0
+    int E;
+    frexp(S, &E);                                       // S = m * 2^E, m in [0.5, 1)
+    return max(E - 53, -1074);
+}
+
+__device__ __forceinline__ SeqFn seq_compose(const SeqFn &a, const SeqFn &b) {
+    SeqFn r;
+    const uint64_t cap = 1ull << 62;   // saturate: a chunk that large is rejected anyway
+    r.d0 = min(cap, a.d0 + (a.o0 ? b.d1 : b.d0));
+    r.o0 = a.o0 ? b.o1 : b.o0;
+    r.d1 = min(cap, a.d1 + (a.o1 ? b.d1 : b.d0));
+    r.o1 = a.o1 ? b.o1 : b.o0;
+    r.uexp = a.uexp;
+    r.ok = a.ok & b.ok;
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) seq_chunk_sum_kernel(const double *__restrict__ x, int64_t n,
+                                                             double *__restrict__ csum) {
+    __shared__ double red[32];
+    const int64_t lo = (int64_t)blockIdx.x * kSeqChunk, hi = min64(n, lo + kSeqChunk);
+    double s = 0.0;
+    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) s += x[k];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = red[threadIdx.x];
+        v = warp_sum(v);
+        if (threadIdx.x == 0) csum[blockIdx.x] = v;
+    }
+}
+
+// exclusive prefix of the chunk sums (approximate chunk-start values; any order is fine)
+__global__ void __launch_bounds__(1024) seq_chunk_prefix_kernel(const double *__restrict__ csum, int64_t nch,
+                                                                double *__restrict__ cpre) {
+    __shared__ double part[1024];
+    const int64_t per = (nch + 1023) / 1024;
+    const int64_t lo = threadIdx.x * per, hi = min64(nch, lo + per);
+    double s = 0.0;
+    for (int64_t c = lo; c < hi; ++c) s += csum[c];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (int t = 0; t < 1024; ++t) { const double v = part[t]; part[t] = run; run += v; }
+    }
+    __syncthreads();
+    double run = part[threadIdx.x];
+    for (int64_t c = lo; c < hi; ++c) { cpre[c] = run; run += csum[c]; }
+}
+
+__global__ void __launch_bounds__(1024) seq_chunk_fn_kernel(const double *__restrict__ x, int64_t n,
+                                                            const double *__restrict__ cpre, SeqFn *__restrict__ fn) {
+    __shared__ SeqFn wred[32];
+    const int64_t lo = (int64_t)blockIdx.x * kSeqChunk;
+    const double A = cpre[blockIdx.x];
+    const bool known = A > 0.0 && isfinite(A);
+    const int ue = known ? grid_exp(A) : 0;
+    SeqFn f{0, 0, 0, 1, ue, known ? 1 : 0};
+    const int64_t k0 = lo + (int64_t)threadIdx.x * kSeqItems;
+#pragma unroll
+    for (int q = 0; q < kSeqItems; ++q) {
+        const int64_t k = k0 + q;
+        if (k >= n) break;
+        const double xv = x[k];
+        const double y = ldexp(xv, -ue);                // exact scaling
+        SeqFn e{0, 0, 0, 1, ue, 1};
+        if (!(y >= 0.0 && y < 9007199254740992.0)) {   // negative, >= 2^53 units, NaN / inf
+            e.ok = 0;
+        } else {
+            const double fl = floor(y), fr = y - fl;
+            const uint64_t di = (uint64_t)fl;
+            if (fr == 0.5) {   // tie: the even result
+                e.d0 = di + (di & 1u);            // start parity 0: sum parity = di's
+                e.d1 = di + ((di & 1u) ^ 1u);
+                e.o0 = 0;
+                e.o1 = 0;
+            } else {
+                const uint64_t d = di + (fr > 0.5 ? 1u : 0u);
+                e.d0 = d;
+                e.d1 = d;
+                e.o0 = (int)(d & 1u);
+                e.o1 = (int)((d & 1u) ^ 1u);
+            }
+        }
+        f = seq_compose(f, e);
+    }
+    // ordered reduction: lane order within the warp, then warp order
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        SeqFn g;
+        g.d0 = __shfl_down_sync(0xffffffffu, f.d0, off);
+        g.d1 = __shfl_down_sync(0xffffffffu, f.d1, off);
+        g.o0 = __shfl_down_sync(0xffffffffu, f.o0, off);
+        g.o1 = __shfl_down_sync(0xffffffffu, f.o1, off);
+        g.ok = __shfl_down_sync(0xffffffffu, f.ok, off);
+        g.uexp = ue;
+        if ((lane & (2 * off - 1)) == 0) f = seq_compose(f, g);
+    }
+    if (lane == 0) wred[threadIdx.x >> 5] = f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        SeqFn r = wred[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = seq_compose(r, wred[w]);
+        r.ok &= known ? 1 : 0;
+        fn[blockIdx.x] = r;
+    }
+}
+
+// one CTA walks the chunks with the exact running sum (dynamic shared: kSeqChunk doubles).
+// The chunk functions are staged 1024 at a time; from the current chunk on, the CTA scans
+// them (composition in chunk order) and finds the first chunk that is not on S's grid or
+// whose sum leaves S's binade; every chunk before it is applied at once (the scanned prefix),
+// that one is added term by term, and the scan restarts after it.
+__device__ __forceinline__ SeqFn shfl_up_fn(const SeqFn &f, int off) {
+    SeqFn g;
+    g.d0 = __shfl_up_sync(0xffffffffu, f.d0, off);
+    g.d1 = __shfl_up_sync(0xffffffffu, f.d1, off);
+    g.o0 = __shfl_up_sync(0xffffffffu, f.o0, off);
+    g.o1 = __shfl_up_sync(0xffffffffu, f.o1, off);
+    g.ok = __shfl_up_sync(0xffffffffu, f.ok, off);
+    g.uexp = f.uexp;
+    return g;
+}
+
+// inclusive scan over the CTA's 1024 threads (thread order = chunk order)
+__device__ SeqFn block_scan_fn(SeqFn f, SeqFn *s_warp) {
+    const unsigned lane = lane_id();
+    const int w = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const SeqFn g = shfl_up_fn(f, off);
+        if ((int)lane >= off) f = seq_compose(g, f);
+    }
+    if (lane == 31) s_warp[w] = f;
+    __syncthreads();
+    if (w == 0) {
+        SeqFn t = s_warp[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const SeqFn g = shfl_up_fn(t, off);
+            if ((int)lane >= off) t = seq_compose(g, t);
+        }
+        s_warp[lane] = t;
+    }
+    __syncthreads();
+    if (w > 0) f = seq_compose(s_warp[w - 1], f);
+    __syncthreads();   // s_warp is reused by the next scan
+    return f;
+}
+
+__global__ void __launch_bounds__(1024) seq_walk_kernel(const double *__restrict__ x, int64_t n, int64_t nch,
+                                                        const SeqFn *__restrict__ fn, int as_rmse,
+                                                        double *__restrict__ out) {
+    extern __shared__ double sbuf[];
+    __shared__ SeqFn s_fn[1024];
+    __shared__ SeqFn s_warp[32];
+    __shared__ double s_S;
+    __shared__ int s_k;
+    const SeqFn ident{0, 0, 0, 1, 0, 1};
+    if (threadIdx.x == 0) s_S = 0.0;
+    for (int64_t base = 0; base < nch; base += 1024) {
+        const int cnt = (int)min64(1024, nch - base);
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) s_fn[threadIdx.x] = fn[base + threadIdx.x];
+        if (threadIdx.x == 0) s_k = 1 << 30;
+        __syncthreads();
+        int idx = 0;
+        while (idx < cnt) {
+            const double S = s_S;
+            int k;   // chunks [idx, idx + k) are applied at once; chunk idx + k term by term
+            if (isnan(S)) {
+                k = cnt - idx;   // NaN stays NaN
+            } else if (!(S > 0.0) || isinf(S)) {
+                k = 0;           // S == 0 (or inf): term by term
+            } else {
+                const int ue = grid_exp(S);
+                const uint64_t Si0 = (uint64_t)ldexp(S, -ue);   // exact: S is on its grid
+                const int c = idx + (int)threadIdx.x;
+                const SeqFn f = c < cnt ? s_fn[c] : ident;
+                const bool valid = c >= cnt || (f.ok && f.uexp == ue);
+                const SeqFn P = block_scan_fn(f, s_warp);
+                const uint64_t D = (Si0 & 1u) ? P.d1 : P.d0;   // through chunk c, from S
+                const bool bad = c < cnt && (!valid || !P.ok || Si0 + D >= (1ull << 53));
+                if (bad) atomicMin(&s_k, (int)threadIdx.x);
+                __syncthreads();
+                k = min(s_k, cnt - idx);
+                if ((int)threadIdx.x == k - 1) s_S = ldexp((double)(Si0 + D), ue);   // exact
+                __syncthreads();
+                if (threadIdx.x == 0) s_k = 1 << 30;
+            }
+            idx += k;
+            __syncthreads();
+            if (idx < cnt) {   // term by term, staged so the adds run at add latency
+                const int64_t lo = (base + idx) * kSeqChunk;
+                const int m = (int)min64(kSeqChunk, n - lo);
+                for (int q = threadIdx.x; q < m; q += blockDim.x) sbuf[q] = x[lo + q];
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    double T = s_S;
+                    for (int q = 0; q < m; ++q) T = __dadd_rn(T, sbuf[q]);
+                    s_S = T;
+                }
+                ++idx;
+                __syncthreads();
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *out = as_rmse ? sqrt(s_S / (double)n) : s_S;
+}
+
+// the one-thread loop's result as a plain sum (small n)
+__global__ void seq_to_sum_kernel(const double *__restrict__ x, int64_t n, double *__restrict__ out) {
+    double S = 0.0;
+    for (int64_t k = 0; k < n; ++k) S = __dadd_rn(S, x[k]);
+    *out = S;
+}
+
+// exact sequential sum for any n (the parallel form above; the one-thread loop for small n)
+int seq_sum_exact(const double *sq, int64_t n, double *out, cudaStream_t st, bool as_rmse = true) {
+    if (n <= 4 * kSeqChunk) {
+        if (as_rmse) seq_sum_kernel<<<1, 1024, 0, st>>>(sq, n, out);
+        else seq_to_sum_kernel<<<1, 1, 0, st>>>(sq, n, out);
+        return cudaGetLastError() == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
+    }
+    const int64_t nch = (n + kSeqChunk - 1) / kSeqChunk;
+    void *scratch = nullptr;
+    const size_t bytes = (size_t)nch * (2 * sizeof(double) + sizeof(SeqFn));
+    CULSH_CHECK(cudaMallocAsync(&scratch, bytes, st));
+    double *csum = static_cast<double *>(scratch), *cpre = csum + nch;
+    SeqFn *fn = reinterpret_cast<SeqFn *>(cpre + nch);
+    seq_chunk_sum_kernel<<<(unsigned)nch, 1024, 0, st>>>(sq, n, csum);
+    seq_chunk_prefix_kernel<<<1, 1024, 0, st>>>(csum, nch, cpre);
+    seq_chunk_fn_kernel<<<(unsigned)nch, 1024, 0, st>>>(sq, n, cpre, fn);
+    // (set on every call: the attribute is per device)
+    CULSH_CHECK(cudaFuncSetAttribute(seq_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kSeqChunk * sizeof(double))));
+    seq_walk_kernel<<<1, 1024, kSeqChunk * sizeof(double), st>>>(sq, n, nch, fn, as_rmse ? 1 : 0, out);
+    const cudaError_t e = cudaGetLastError();
+    CULSH_CHECK(cudaFreeAsync(scratch, st));
+    return e == cudaSuccess ? CULSH_OK : CULSH_ECUDA;
+}
+
 int reduce_rmse(const double *sq, int64_t n, double *out, double *scratch_partials, bool sequential,
                 cudaStream_t st) {
     if (sequential) {
-        seq_sum_kernel<<<1, 1024, 0, st>>>(sq, n, out);
+        return seq_sum_exact(sq, n, out, st);
     } else {
         const int np = 256;
         tree_sum_kernel<<<np, 1024, 0, st>>>(sq, n, scratch_partials);
@@ -553,7 +825,15 @@ int reduce_rmse(const double *sq, int64_t n, double *out, double *scratch_partia
 
 using namespace culsh;
 
-// sqerr_scratch must hold n + 256 doubles.  Sequential (bit-exact) sum for n <= 2^22.
+// fl(...fl(fl(0 + x[0]) + x[1]) ... + x[n-1]) -- numpy's np.add.accumulate(x)[-1] -- for
+// non-negative x (any other term is added one by one), n >= 1
+extern "C" int culsh_sequential_sum(const double *x, int64_t n, double *out, void *stream) {
+    CULSH_REQUIRE(n >= 1, "empty input");
+    return seq_sum_exact(x, n, out, (cudaStream_t)stream, false);
+}
+
+// sqerr_scratch must hold n + 256 doubles.  The sum is the reference's sequential one, bit
+// for bit, at any n (seq_sum_exact).
 extern "C" int culsh_rmse(const CulshData *d, const CulshModel64 *m, const int32_t *t_rows,
                           const int32_t *t_cols, const double *t_vals, int64_t n, int do_clamp,
                           double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
@@ -566,7 +846,7 @@ extern "C" int culsh_rmse(const CulshData *d, const CulshModel64 *m, const int32
                                                             PreLookup{}, 0, do_clamp, clamp_lo, clamp_hi, unscale,
                                                             sqerr_scratch);
     CULSH_LAUNCH_CHECK();
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, true, st);
 }
 
 extern "C" int culsh_train_lookup(const CulshData *d, const int32_t *nbr, int K, const uint32_t *mask,
@@ -598,7 +878,7 @@ extern "C" int culsh_rmse_train(const CulshData *d, const CulshModel64 *m, const
                                                            m->nbr, m->F, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
                                                            do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, true, st);
 }
 
 extern "C" int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int32_t *nbr,
@@ -643,7 +923,7 @@ extern "C" int culsh_rmse_m32(const CulshData *d, const CulshModel32 *m, double 
                                                            PreLookup{}, 0, do_clamp, clamp_lo, clamp_hi, unscale,
                                                            sqerr_scratch);
     CULSH_LAUNCH_CHECK();
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, true, st);
 }
 
 extern "C" int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, double mu, int F,
@@ -662,7 +942,7 @@ extern "C" int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, d
                                                           nbr, F, m->F, m->K, nullptr, nullptr, nullptr, n, pre, 0,
                                                           do_clamp, clamp_lo, clamp_hi, unscale, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, n <= (1LL << 22), st);
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, true, st);
 }
 
 // factorization.py:559-579 rmse in row order (pred_row_kernel; N <= 65,536, no lookup
@@ -672,7 +952,7 @@ extern "C" int culsh_rmse_train_m32(const CulshData *d, const CulshModel32 *m, d
 // the test set).  The sum runs in entry order like culsh_rmse / culsh_rmse_train.
 static int rows_finish(int rc, const double *sq, int64_t n, double *out, double *scratch, cudaStream_t st) {
     if (rc != CULSH_OK) return rc;
-    return reduce_rmse(sq, n, out, scratch, n <= (1LL << 22), st);
+    return reduce_rmse(sq, n, out, scratch, true, st);
 }
 
 extern "C" int culsh_rmse_train_rows(const CulshData *d, const CulshModel64 *m, const int32_t *csr_entry,

@@ -424,3 +424,56 @@ def test_build_indices_duplicate_check_on_device(P):
     import re
     with pytest.raises(ValueError, match=re.escape(f"duplicate entry at (row={rows2[k]}, col={cols2[k]})")):
         P.build_indices(P.Triplets(rows2, cols2, vals), M=M, N=N)
+
+
+def _seq_sum_device(x):
+    from paper_2111_11682_b200 import _native as nat
+    xd = nat.to_dev(np.ascontiguousarray(x, np.float64))
+    out = nat.empty((1,), "float64")
+    nat.call("culsh_sequential_sum", nat.ptr(xd), len(x), nat.ptr(out), nat.stream_ptr())
+    return float(out.item())
+
+
+def _seq_cases():
+    rng = np.random.default_rng(42)
+    e = rng.standard_normal(3_000_000)
+    yield "squares_3M", e * e
+    # ties to even: on a grid where S ~ 1, terms of 0.5 / 1.5 / 2.5 ulp
+    u = 2.0 ** -52
+    t = rng.choice(np.array([0.5, 1.5, 2.5, 1.0, 0.0]) * u, 400_000)
+    t[0] = 1.0
+    yield "ties", t
+    # many binade changes: geometric growth, then tiny terms
+    yield "binades", np.concatenate([2.0 ** (np.arange(200_000) / 4000.0), rng.random(100_000) * 1e-12])
+    # leading zeros, subnormals, a huge term mid-way
+    z = np.zeros(150_000)
+    sub = rng.random(120_000) * 1e-310
+    mid = rng.random(90_000)
+    mid[45_000] = 1e300
+    yield "zeros_subnormal_huge", np.concatenate([z, sub, mid])
+    for n in (1, 7, 8192, 32768, 32769, 40_000, 100_003):
+        yield f"n{n}", rng.random(n) * 3.0
+
+
+@pytest.mark.parametrize("name,x", list(_seq_cases()), ids=lambda v: v if isinstance(v, str) else "")
+def test_exact_sequential_sum(P, name, x):
+    """culsh_sequential_sum (every rmse's sum) == numpy's sequential accumulate, bit for bit,
+    through ties-to-even, binade changes, zeros, subnormals and a huge term."""
+    ref = np.add.accumulate(x)[-1]
+    assert _seq_sum_device(x) == ref, name
+
+
+def test_exact_sequential_sum_nonfinite(P):
+    x = np.random.default_rng(1).random(200_000)
+    x[150_000] = np.inf
+    assert _seq_sum_device(x) == np.inf
+    x[170_000] = np.nan
+    assert np.isnan(_seq_sum_device(x))
+
+
+def test_exact_sequential_sum_100m(P):
+    """At the C3 training-set size (rmse over 100M squared errors, cli.py's train RMSE)."""
+    e = np.random.default_rng(3).standard_normal(100_000_000) * 0.9
+    x = e * e
+    del e
+    assert _seq_sum_device(x) == np.add.accumulate(x)[-1]
