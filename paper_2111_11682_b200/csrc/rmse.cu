@@ -891,7 +891,7 @@ extern "C" int culsh_rmse32(const CulshData *d, const CulshModel32 *m, const int
                                                            nbr, m->F, m->F, m->K, t_rows, t_cols, t_vals, n, PreLookup{},
                                                            0, 0, 0.0, 0.0, 1.0, sqerr_scratch);
     CULSH_LAUNCH_CHECK();
-    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, false, st);
+    return reduce_rmse(sqerr_scratch, n, rmse_out, sqerr_scratch + n, true, st);
 }
 
 extern "C" int culsh_predict(const CulshData *d, const CulshModel64 *m, const int32_t *rows,
