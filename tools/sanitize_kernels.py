@@ -51,6 +51,22 @@ def main():
     p0 = P.train_full(base, t0, tc)
     P.absorb_increment(p0, s0, base, batch, tc)
     P.rmse(p, r.triplets(), r)
+    # the exact parallel serial sum (chunk sums / prefix / functions / scanned walk), with a
+    # binade change and ties inside, against numpy's sequential accumulate
+    from paper_2111_11682_b200 import _native as nat
+    xs = np.random.default_rng(5).random(70_000) ** 4
+    xs[:300] = 2.0 ** -53
+    xs[0] = 1.0
+    xd, sd = nat.to_dev(xs), nat.empty((1,), "float64")
+    nat.call("culsh_sequential_sum", nat.ptr(xd), len(xs), nat.ptr(sd), nat.stream_ptr())
+    assert float(sd.item()) == np.add.accumulate(xs)[-1]
+    # K above two mask words (exact column kernel with four words)
+    tw, _ = P.simlsh_topk(r, cfg, 70)
+    pw = P.train_full(r, tw, P.TrainConfig(F=16, K=70, epochs=1, seed=2))
+    dw, muw = orc.build_csr(r.M, r.N, r.entry_rows, r.entry_cols, r.entry_values)
+    mw = orc.train_full(dw, muw, tw.entries, 16, 70, 1, 2, P.TrainConfig(F=16, K=70).rates_at,
+                        P.TrainConfig(F=16, K=70).regs)
+    assert pw.U.tobytes() == mw.U.tobytes() and pw.W.tobytes() == mw.W.tobytes()
     P.gsm_topk(r, P.SimilarityConfig(K=6), method="count")
     P.gsm_topk(r, P.SimilarityConfig(K=6), method="merge")
     if which == "all":
