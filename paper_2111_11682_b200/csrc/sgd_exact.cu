@@ -443,7 +443,7 @@ __host__ __device__ constexpr int exact_kpl(int K) { return K <= 32 ? 1 : K <= 6
 
 #define CULSH_DISPATCH_FK(F, K, CALL)                                  \
     do {                                                               \
-        const int _fpl = (F) <= 32 ? 1 : (F) <= 64 ? 2 : (F) <= 128 ? 4 : 8; \
+        const int _fpl = (F) <= 32 ? 1 : (F) <= 64 ? 2 : (F) <= 128 ? 4 : (F) <= 256 ? 8 : 16; \
         const int _kpl = exact_kpl(K);                                 \
         if (_fpl == 1 && _kpl == 1) return CALL(1, 1);                 \
         if (_fpl == 1 && _kpl == 2) return CALL(1, 2);                 \
@@ -456,7 +456,10 @@ __host__ __device__ constexpr int exact_kpl(int K) { return K <= 32 ? 1 : K <= 6
         if (_fpl == 4 && _kpl == 4) return CALL(4, 4);                 \
         if (_fpl == 8 && _kpl == 1) return CALL(8, 1);                 \
         if (_fpl == 8 && _kpl == 2) return CALL(8, 2);                 \
-        return CALL(8, 4);                                             \
+        if (_fpl == 8 && _kpl == 4) return CALL(8, 4);                 \
+        if (_fpl == 16 && _kpl == 1) return CALL(16, 1);               \
+        if (_fpl == 16 && _kpl == 2) return CALL(16, 2);               \
+        return CALL(16, 4);                                            \
     } while (0)
 
 }  // namespace culsh
@@ -515,7 +518,7 @@ static int exact_colpass_impl(const CulshData *d, CulshModel64 *m, const CulshRa
                               const int32_t *chain_lo, int64_t col_lo, int64_t col_hi, int row_mode,
                               int64_t M_old, int variant, int *row_last, int *ticket, int *status, void *stream,
                               ExactPre pre) {
-    CULSH_REQUIRE(m->F >= 1 && m->F <= 256, "F must be in [1, 256]");
+    CULSH_REQUIRE(m->F >= 1 && m->F <= 512, "F must be in [1, 512]");
     CULSH_REQUIRE(m->K >= 0 && m->K <= 128, "K must be in [0, 128]");
     if (col_hi <= col_lo) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -561,7 +564,7 @@ extern "C" int culsh_sgd_exact_colpass_pre(const CulshData *d, CulshModel64 *m, 
 extern "C" int culsh_sgd_exact_rowpass(const CulshData *d, CulshModel64 *m, const CulshRates *r,
                                        int64_t row_lo, int64_t row_hi, int64_t N_old, int *status,
                                        void *stream) {
-    CULSH_REQUIRE(m->F >= 1 && m->F <= 256, "F must be in [1, 256]");
+    CULSH_REQUIRE(m->F >= 1 && m->F <= 512, "F must be in [1, 512]");
     CULSH_REQUIRE(m->K >= 0 && m->K <= 128, "K must be in [0, 128]");
     if (row_hi <= row_lo) return CULSH_OK;
     cudaStream_t st = (cudaStream_t)stream;

@@ -460,6 +460,8 @@ def _exact_lookups(dev, dm: DeviceModel64, col_lo: int, col_hi: int, mem_fractio
 # four 32-bit explicit-neighbour mask words per rating, the top-K kernels' bound (topk.cu).
 # The fp32 Hogwild mode keeps two (K <= 64, hogwild.hogwild_supported).
 MAX_K = 128
+# the largest F of the same kernels (16 fp64 factors per lane); the Hogwild mode keeps 256
+MAX_F = 512
 
 
 def _mask_words(K: int) -> int:
@@ -469,9 +471,9 @@ def _mask_words(K: int) -> int:
 
 def _check_model_dims(F: int, K: int) -> None:
     # the reference accepts any F and K (factorization.py:75-82); the kernels keep up to
-    # 256 factors per row and MAX_K neighbours per column
-    if not (1 <= F <= 256):
-        raise ValueError(f"F={F} outside the supported range [1, 256] (the reference has no bound)")
+    # MAX_F factors per row and MAX_K neighbours per column
+    if not (1 <= F <= MAX_F):
+        raise ValueError(f"F={F} outside the supported range [1, {MAX_F}] (the reference has no bound)")
     if not (0 <= K <= MAX_K):
         raise ValueError(f"K={K} outside the supported range [0, {MAX_K}] (the reference has no bound)")
 

@@ -1,4 +1,5 @@
-"""K above two mask words (65 <= K <= 128): the exact (reference-order) kernels, the online
+"""K above two mask words (65 <= K <= 128) and F above 256 (up to 512): the exact
+(reference-order) kernels, the online
 path and rmse / predict take four explicit-neighbour mask words per rating and stay
 bit-identical to the oracle (itself pinned to the reference); the fp32 Hogwild mode keeps
 K <= 64 and says so.  The reference accepts any K (factorization.py:75-82)."""
@@ -26,7 +27,7 @@ def _case(P, seed, M=220, N=150, dens=0.25):
     return P.SparseRatings(M, N, rows, cols, vals), rows, cols, vals
 
 
-@pytest.mark.parametrize("F,K", [(40, 100), (128, 128), (8, 65)])
+@pytest.mark.parametrize("F,K", [(40, 100), (128, 128), (8, 65), (300, 32), (512, 70)])
 def test_exact_train_full_wide_k_vs_oracle(P, orc, F, K):
     r, rows, cols, vals = _case(P, seed=K)
     tbl, _ = P.simlsh_topk(r, P.LshConfig(G=8, p=3, q=20, psi_exponent=2, seed=1), K)

@@ -206,8 +206,8 @@ def test_pairwise_plan_combines_to_numpy():
 
 
 def test_model_dims_bounds():
-    """Exact kernels take K <= 128 (four mask words, the top-K kernels' bound); the fp32
-    Hogwild mode K <= 64; the reference has no bound (factorization.py:75-82)."""
+    """Exact kernels take F <= 512 and K <= 128 (four mask words, the top-K kernels' bound);
+    the fp32 Hogwild mode F <= 256, K <= 64; the reference has no bound (factorization.py:75-82)."""
     import pytest
     from paper_2111_11682_b200.factorization import MAX_K, _check_model_dims, _mask_words
     from paper_2111_11682_b200.hogwild import hogwild_supported
@@ -215,7 +215,8 @@ def test_model_dims_bounds():
     _check_model_dims(256, 128)
     with pytest.raises(ValueError, match="K=129"):
         _check_model_dims(8, 129)
-    with pytest.raises(ValueError, match="F=257"):
-        _check_model_dims(257, 8)
+    _check_model_dims(512, 8)
+    with pytest.raises(ValueError, match="F=513"):
+        _check_model_dims(513, 8)
     assert [_mask_words(k) for k in (0, 32, 33, 64, 65, 128)] == [1, 1, 2, 2, 4, 4]
     assert hogwild_supported(128, 64) and not hogwild_supported(128, 65)
