@@ -220,3 +220,69 @@ def test_model_dims_bounds():
         _check_model_dims(513, 8)
     assert [_mask_words(k) for k in (0, 32, 33, 64, 65, 128)] == [1, 1, 2, 2, 4, 4]
     assert hogwild_supported(128, 64) and not hogwild_supported(128, 65)
+
+
+def _seq_sum_by_binade_runs(x, chunk=64):
+    """Host restatement of rmse.cu's exact parallel serial sum (seq_chunk_fn_kernel /
+    seq_walk_kernel): per chunk, the function b -> (D_b, b') on the grid of the chunk's
+    approximate starting sum; a chunk on S's grid that stays in S's binade is applied as one
+    integer step, any other chunk term by term."""
+    import math
+    n = len(x)
+    csum = [math.fsum(x[c:c + chunk]) for c in range(0, n, chunk)]
+    approx = np.concatenate([[0.0], np.cumsum(csum)[:-1]])
+
+    def grid(S):
+        return max(math.frexp(S)[1] - 53, -1074)
+
+    fns = []
+    for ci, c in enumerate(range(0, n, chunk)):
+        A = approx[ci]
+        ok = A > 0 and math.isfinite(A)
+        ue = grid(A) if ok else 0
+        d0, d1, o0, o1 = 0, 0, 0, 1
+        for v in x[c:c + chunk]:
+            try:
+                y = math.ldexp(v, -ue)
+            except OverflowError:   # the device's ldexp gives inf: not on this grid
+                y = math.inf
+            if not (0.0 <= y < 2.0 ** 53):
+                ok = False
+                break
+            fl = math.floor(y)
+            fr = y - fl
+            if fr == 0.5:
+                e0, e1, p0, p1 = fl + (fl & 1), fl + ((fl & 1) ^ 1), 0, 0
+            else:
+                d = fl + (1 if fr > 0.5 else 0)
+                e0, e1, p0, p1 = d, d, d & 1, (d & 1) ^ 1
+            d0, o0 = d0 + (e1 if o0 else e0), (p1 if o0 else p0)
+            d1, o1 = d1 + (e1 if o1 else e0), (p1 if o1 else p0)
+        fns.append((ok, ue, d0, d1))
+    S = 0.0
+    for ci, c in enumerate(range(0, n, chunk)):
+        ok, ue, d0, d1 = fns[ci]
+        if ok and S > 0 and math.isfinite(S) and grid(S) == ue:
+            Si = int(math.ldexp(S, -ue))
+            D = d1 if Si & 1 else d0
+            if Si + D < 2 ** 53:
+                S = math.ldexp(float(Si + D), ue)
+                continue
+        for v in x[c:c + chunk]:
+            S = S + v
+    return S
+
+
+def test_sequential_sum_algebra_matches_accumulate():
+    """The binade-run algebra behind culsh_sequential_sum equals numpy's sequential
+    accumulate bit for bit: normal squares, exact ties (to even), binade changes, leading
+    zeros and subnormals (the CUDA kernels are checked the same way on the GPU)."""
+    rng = np.random.default_rng(7)
+    e = rng.standard_normal(6000)
+    u = 2.0 ** -52
+    ties = rng.choice(np.array([0.5, 1.5, 2.5, 1.0, 0.0]) * u, 3000)
+    ties[0] = 1.0
+    cases = [e * e, ties, 2.0 ** (np.arange(3000) / 60.0),
+             np.concatenate([np.zeros(300), rng.random(500) * 1e-310, rng.random(800)])]
+    for x in cases:
+        assert _seq_sum_by_binade_runs(list(map(float, x))) == np.add.accumulate(x)[-1]
