@@ -45,37 +45,37 @@ def test_exact_train_full_wide_k_vs_oracle(P, orc, F, K):
     assert P.rmse(p, sub, r, clamp=(1.0, 5.0)) == orc.rmse(d, m, sub.rows, sub.cols, sub.values, clamp=(1.0, 5.0))
 
 
-def test_parallel_train_wide_k_vs_oracle(P, orc):
+@pytest.mark.parametrize("F,K", [(32, 96), (384, 16)])
+def test_parallel_train_wide_k_vs_oracle(P, orc, F, K):
     r, rows, cols, vals = _case(P, seed=5)
-    K = 96
     tbl, _ = P.simlsh_topk(r, P.LshConfig(G=8, p=3, q=20, psi_exponent=2, seed=1), K)
-    tc = P.TrainConfig(F=32, K=K, epochs=2, seed=0)
+    tc = P.TrainConfig(F=F, K=K, epochs=2, seed=0)
     p = P.parallel_train(r, tbl, tc, 3)
     p = p[0] if isinstance(p, tuple) else p
     d, mu = orc.build_csr(r.M, r.N, rows, cols, vals)
-    m = orc.parallel_train(d, mu, tbl.entries, 32, K, 2, 0, tc.rates_at, tc.regs, 3)
+    m = orc.parallel_train(d, mu, tbl.entries, F, K, 2, 0, tc.rates_at, tc.regs, 3)
     for a, b in ((p.U, m.U), (p.V, m.V), (p.W, m.W), (p.C, m.C), (p.b, m.b), (p.b_hat, m.bhat)):
         assert a.tobytes() == b.tobytes()
 
 
-def test_absorb_increment_wide_k_vs_oracle(P, orc):
+@pytest.mark.parametrize("F,K", [(16, 80), (272, 24)])
+def test_absorb_increment_wide_k_vs_oracle(P, orc, F, K):
     full, *_ = _case(P, seed=9, M=240, N=160, dens=0.2)
-    K = 80
     lc = P.LshConfig(G=4, p=2, q=10, psi_exponent=2, seed=2)
-    cfg = P.TrainConfig(F=16, K=K, epochs=2, seed=3)
+    cfg = P.TrainConfig(F=F, K=K, epochs=2, seed=3)
     orig, batch3, _, _ = P.holdback_variables(full, 12, 6, seed=0)
     tbl, state = P.simlsh_topk(orig, lc, K)
     params = P.train_full(orig, tbl, cfg)
     acc0 = state.acc.copy()
     d0, mu0 = orc.build_csr(orig.M, orig.N, orig.entry_rows, orig.entry_cols, orig.entry_values)
-    m = orc.train_full(d0, mu0, tbl.entries, 16, K, 2, 3, cfg.rates_at, cfg.regs)
+    m = orc.train_full(d0, mu0, tbl.entries, F, K, 2, 3, cfg.rates_at, cfg.regs)
     batch = P.IncrementBatch(orig.M, orig.N, 12, 6, batch3.rows, batch3.cols, batch3.values)
     params, state, _, tbl = P.absorb_increment(params, state, orig, batch, cfg)
     m, acc, ent, _ = orc.absorb_increment(
         m, acc0, (lc.G, lc.p, lc.q, lc.psi_exponent, lc.seed), None,
         (orig.entry_rows, orig.entry_cols, orig.entry_values),
         (batch.base_M, batch.base_N, batch.new_row_count, batch.new_col_count, batch.rows, batch.cols,
-         batch.values), 16, K, 2, 3, cfg.rates_at, cfg.regs)
+         batch.values), F, K, 2, 3, cfg.rates_at, cfg.regs)
     assert state.acc.tobytes() == acc.tobytes()
     assert tbl.entries.tobytes() == ent.tobytes()
     for a, b in ((params.U, m.U), (params.V, m.V), (params.W, m.W), (params.C, m.C),
