@@ -332,7 +332,7 @@ int culsh_train_lookup(const CulshData *d, const int32_t *nbr, int K, const uint
 /* factorization.py:559-579 rmse over the TRAINING set itself (cli.py:204-210 calls it
  * every epoch): the CSC entries of d, neighbour values from the lookup cache, the squared
  * error of CSC position c stored at entry index perm[c] (NULL: identity) so the sum runs
- * in the reference's entry order (sequential for nnz <= 2^22, else the fixed tree). */
+ * in the reference's entry order (the exact serial sum at any nnz, culsh_sequential_sum). */
 int culsh_rmse_train(const CulshData *d, const CulshModel64 *m, const uint32_t *mask,
                      const int64_t *group_base, const int32_t *pos, const int64_t *perm, int do_clamp,
                      double clamp_lo, double clamp_hi, double unscale, double *sqerr_scratch,
